@@ -1,0 +1,360 @@
+"""Benchmark: sharded dropout (BASELINE config 2) on 1..N B200s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1)
+
+Workload (BASELINE.json configs[1]): x = bf16 [8, 4096, 4096] activations
+(synthetic, torch.randn seed 0), dropout p = 0.1, Shard(1) (sequence parallel)
+over the N ranks of a 1-d mesh.  The global tensor is fixed, so scaling is
+strong: rank r owns x[:, r*4096/N : (r+1)*4096/N, :].
+
+A step = one forward dropout of the rank's shard with single-device semantics:
+the keep-mask is the rank's slice of ONE global Bernoulli(0.9) draw from the
+shared RngState (no communication), y = (x*m)*(1/0.9) in one fused sm_100a
+kernel (mask not stored; backward regenerates it).  Metric: GB/s of
+algorithmic bytes (read x 2 B + write y 2 B per element), whole job.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SHAPE = (8, 4096, 4096)
+P_DROP = 0.1
+SEED = 20240817
+METRIC = "sharded randn/dropout GB/s per GPU & aggregate at 1/2/4/8 B200 vs roofline; bit-exact"
+BYTES_PER_ELEM = 4  # bf16 read + bf16 write
+PHILOX_OPS = 80     # INT32 ops per Philox4x32-10 block
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the oracle port of the reference path, timed on host cores.
+# ---------------------------------------------------------------------------
+def _cpu_sample(args):
+    """Dropout of rows [r0, r0+nrows) of batch b: mask via the oracle's
+    restatement of rng.py + engine.k_dropout_apply (numpy, 1 core)."""
+    import ml_dtypes
+    import numpy as np
+    from oracle import rng_oracle as O
+    b, r0, nrows, seed = args
+    rs = np.random.default_rng(b * 100003 + r0)
+    x = rs.standard_normal((nrows, SHAPE[2]), dtype=np.float32).astype(ml_dtypes.bfloat16)
+    j = (np.arange(nrows * SHAPE[2], dtype=np.int64) + (b * SHAPE[1] + r0) * SHAPE[2])
+    t0 = time.perf_counter()
+    keep = O.fill_indices(j, seed, 0, 65536, "bernoulli", (1.0 - P_DROP,), ml_dtypes.bfloat16)
+    y = O.dropout_apply(x.reshape(-1), keep, P_DROP)
+    dt = time.perf_counter() - t0
+    return dt, y.size
+
+
+def cpu_measure(n_elems: int, cores: int):
+    """Time the oracle on `n_elems` elements split over `cores` processes.
+    Returns (elements/s, seconds)."""
+    rows = max(1, n_elems // SHAPE[2])
+    per = max(1, rows // cores)
+    jobs = [(0, i * per, per, SEED) for i in range(cores)]
+    t0 = time.perf_counter()
+    if cores == 1:
+        res = [_cpu_sample(jobs[0])]
+    else:
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(cores) as pool:
+            res = pool.map(_cpu_sample, jobs)
+    wall = time.perf_counter() - t0
+    elems = sum(n for _, n in res)
+    return elems / wall, wall, elems
+
+
+def run_reference(a):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    sample = 2 * cores * SHAPE[2] * 64  # 64 rows per core per step
+    for _ in range(a.warmup):
+        cpu_measure(sample // 8, cores)
+    rates, walls = [], []
+    for _ in range(a.steps):
+        r, wall, _ = cpu_measure(sample, cores)
+        rates.append(r)
+        walls.append(wall)
+    rate = statistics.median(rates)
+    gbs = rate * BYTES_PER_ELEM / 1e9
+    ms = statistics.median(walls) * 1e3  # one bounded-sample step
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 6), "unit": "GB/s",
+        "n_gpus": ws, "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": "cfg2: dropout p=0.1 on bf16 [8,4096,4096], Shard(1) sequence-parallel",
+                   "global_shape": list(SHAPE), "p": P_DROP, "placement": "S(1)",
+                   "parallelism": f"sp{ws}"},
+        "cpu_baseline": {"value": round(gbs, 6), "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"{sample} elements per step ({cores} procs x 64 rows x 2 x 4096),"
+                                   " numpy restatement of rng.py + engine.k_dropout_apply"},
+        "e2e": {"value": round(gbs, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU side.
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.gpu = gpu_index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *exc):
+        if self.p is not None:
+            self.p.terminate()
+            self.p.wait()
+        return False
+
+    def summary(self):
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def run_ours(a):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    if ws != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={ws}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2509_07003_b200 import _lib, create_mesh, ops, rng as R
+    from paper_2509_07003_b200.placement import ShardSpec, local_shape_and_offset, parse_placements
+
+    mesh = create_mesh([("sp", ws)])
+    spec = ShardSpec(mesh, parse_placements("S(1)"))
+    view = local_shape_and_offset(spec, SHAPE, mesh.coords_of_rank(rank))
+    s0, n = view.local_offset[1], view.local_shape[1]
+    gen = torch.Generator(device=dev).manual_seed(0)
+    x_full_rows = torch.randn((SHAPE[0], SHAPE[1], SHAPE[2]), generator=gen, device=dev,
+                              dtype=torch.bfloat16) if ws == 1 else None
+    if ws == 1:
+        x = x_full_rows
+    else:  # same synthetic global tensor, generated per batch to bound memory
+        x = torch.empty(view.local_shape, dtype=torch.bfloat16, device=dev)
+        for b in range(SHAPE[0]):
+            xb = torch.randn((SHAPE[1], SHAPE[2]), generator=gen, device=dev, dtype=torch.bfloat16)
+            x[b].copy_(xb[s0:s0 + n])
+            del xb
+    y = torch.empty_like(x)
+    n_local = x.numel()
+    local_bytes = n_local * BYTES_PER_ELEM
+    l2_bytes = 126 * 1024 * 1024
+    need_flush = x.numel() * 2 < 2 * l2_bytes
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev) if need_flush else None
+    stream = torch.cuda.current_stream(dev)
+    state = R.RngState(SEED, 0, 65536)
+
+    def step():
+        ops.dropout_apply(x, P_DROP, state, view, out=y)
+        state.advance(math.prod(SHAPE))  # every rank, no communication (rng.py:95-98)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # --- timed region: K steps, barrier + synchronize on both sides ---------
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for i in range(a.steps):
+            if flush is not None:
+                flush.fill_(i & 0xFF)  # evict x / y from L2 between timed steps (untimed)
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms_local = sum(step_ms) / len(step_ms)
+    clocks = clk.summary()
+
+    # --- e2e through the public API with host buffers -------------------------
+    xh = x.cpu().pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    xd = torch.empty_like(x)
+    e_starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    e_ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    st2 = R.RngState(SEED, 0, 65536)
+
+    def e2e_step():
+        xd.copy_(xh, non_blocking=True)
+        yd = ops.dropout_apply(xd, P_DROP, st2, view)
+        yh.copy_(yd, non_blocking=True)
+        st2.advance(math.prod(SHAPE))
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    for i in range(a.steps):
+        e_starts[i].record(stream)
+        e2e_step()
+        e_ends[i].record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms_local = sum(s.elapsed_time(e) for s, e in zip(e_starts, e_ends)) / a.steps
+
+    # --- max over ranks -------------------------------------------------------
+    t = torch.tensor([ms_local, e2e_ms_local], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, e2e_ms = t.tolist()
+    total_elems = math.prod(SHAPE)
+    gbs = total_elems * BYTES_PER_ELEM / (ms * 1e-3) / 1e9
+    e2e_gbs = total_elems * BYTES_PER_ELEM / (e2e_ms * 1e-3) / 1e9
+
+    # --- roofline (rank 0's kernel) --------------------------------------------
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback B200_PROFILING.md"
+    import ctypes as C
+    imad, lop3, phx = C.c_double(), C.c_double(), C.c_double()
+    _lib.check(_lib.LIB.sdr_probe_int32(local, C.byref(imad), C.byref(lop3), C.byref(phx)),
+               "sdr_probe_int32")
+    # Philox needs 20 IMAD.WIDE (= 40 INT32 mul ops) per block; the fma pipe is
+    # the binding pipe, so the Philox-proportion INT32 peak is 4 x IMAD.WIDE/s.
+    int_peak_tops = 4.0 * imad.value / 1e12
+    achieved_tops = n_local / (ms_local * 1e-3) * PHILOX_OPS / 1e12
+    achieved_gbs_local = local_bytes / (ms_local * 1e-3) / 1e9
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if not a.no_cpu_baseline and ws == 1:
+            sample = 2 * 1024 * SHAPE[2]  # 8.4 M elements, 1 core
+            rate, wall, elems = cpu_measure(sample, 1)
+            cpu = {"value": round(rate * BYTES_PER_ELEM / 1e9, 6), "unit": "GB/s", "cores": 1,
+                   "kind": "port",
+                   "sample": f"{elems} elements (2048 rows x 4096 of batch 0), numpy restatement of "
+                             f"rng.py:185-242 + engine.py:80-81, {wall:.1f}s wall"}
+        line = {
+            "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": ws,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": "cfg2: dropout p=0.1 on bf16 [8,4096,4096], Shard(1) sequence-parallel",
+                       "global_shape": list(SHAPE), "p": P_DROP, "placement": "S(1)",
+                       "parallelism": f"sp{ws}", "per_gpu_elements": n_local,
+                       "l2": "flushed between timed steps (256 MiB write)" if need_flush
+                             else "input 268 MB > 126 MB L2 (no flush needed)",
+                       "per_gpu_gbs": round(gbs / ws, 3),
+                       "elements_per_s": round(total_elems / (ms * 1e-3), 1)},
+            "roofline": {
+                "bound": "int32", "achieved": round(achieved_tops, 3), "peak": round(int_peak_tops, 3),
+                "unit": "TOP/s INT32 (80 per Philox block)", "frac": round(achieved_tops / int_peak_tops, 4),
+                "traffic": None,
+                "int32_probe": {"imad_wide_per_s": imad.value, "lop3_per_s": lop3.value,
+                                "philox_blocks_per_s_no_hoist": phx.value,
+                                "how": "sdr_probe_int32: independent IMAD.WIDE / LOP3 chains, live"},
+                "hbm": {"achieved": round(achieved_gbs_local, 1), "peak": hbm_peak, "unit": "GB/s",
+                        "frac": round(achieved_gbs_local / hbm_peak, 4), "peak_source": hbm_src},
+                "kernel": "k_dropout_fast<BF16,BF16,-1> (one launch per step)",
+            },
+            "e2e": {"value": round(e2e_gbs, 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": xh.numel() * xh.element_size(),
+                    "d2h_bytes_per_step": yh.numel() * yh.element_size(),
+                    "how": "pinned host x -> H2D, paper_2509_07003_b200.ops.dropout_apply, D2H y"},
+            "gpu_launches": a.steps,
+            "clocks": clocks,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return line
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,171 @@
+/* sdrng.h -- C ABI of the B200-native single-device-semantic distributed RNG
+ * and the multi-DTensor pack/unpack used by the fused redistribute.
+ *
+ * The reference (veScale spmdsim, /root/reference/pkg/src/spmdsim) is pure
+ * Python/NumPy and has no FFI; its boundary for this path is the Python API of
+ * spmdsim.rng / placement / dtensor / comm.  Each entry point below replaces
+ * one reference function (cited), and the Python package
+ * paper_2509_07003_b200 binds them with ctypes.
+ *
+ * Conventions
+ *  - Every call is asynchronous on `stream` (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream) and returns an sdr_status (0 = OK).
+ *  - The caller owns every buffer.  Device buffers are plain device pointers.
+ *  - The library holds no RNG state: (seed, offset, theta) are passed by value
+ *    and advanced by the caller exactly as rng.py:95-98.
+ *  - A window ("view") of a row-major global tensor of rank `ndim` is given per
+ *    tensor dim d by global_shape[d], local_start[d], local_len[d], and for
+ *    InterleavedShard dims groups[d] (m) and group_stride[d] (global distance
+ *    between groups); groups == NULL means every dim is contiguous.  Local
+ *    element order is row-major over local_len (placement.py:202-223).
+ */
+#ifndef SDRNG_H_
+#define SDRNG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDR_MAX_NDIM 8
+
+typedef enum {
+  SDR_OK = 0,
+  SDR_E_INVALID = 1,     /* bad shape / window / pointer / count            */
+  SDR_E_DTYPE = 2,       /* dtype unsupported for this distribution/op      */
+  SDR_E_DIST = 3,        /* unknown distribution kind                       */
+  SDR_E_PARAM = 4,       /* distribution parameter out of domain (ValueError) */
+  SDR_E_CUDA = 5,        /* CUDA launch/runtime error                       */
+  SDR_E_NOTABLES = 6,    /* normal() before sdr_normal_tables_load          */
+  SDR_E_ALIGN = 7        /* buffer misaligned for the requested op          */
+} sdr_status;
+
+typedef enum {
+  SDR_F32 = 0, SDR_F64 = 1, SDR_BF16 = 2, SDR_F16 = 3,
+  SDR_I64 = 4, SDR_I32 = 5, SDR_U8 = 6, SDR_BOOL = 7
+} sdr_dtype;
+
+typedef enum {
+  SDR_UNIFORM01 = 0,  /* rng.py:118-127  */
+  SDR_UNIFORM = 1,    /* rng.py:130-138  fparam = {lo, hi}      */
+  SDR_NORMAL = 2,     /* rng.py:141-156  fparam = {mean, std}   */
+  SDR_RANDINT = 3,    /* rng.py:159-171  iparam = {lo, hi}      */
+  SDR_BERNOULLI = 4   /* rng.py:174-182  fparam = {p}           */
+} sdr_dist_kind;
+
+typedef struct {
+  int32_t kind;        /* sdr_dist_kind */
+  double fparam[2];
+  int64_t iparam[2];
+} sdr_dist;
+
+typedef struct {        /* generator state, by value (rng.py:85-101) */
+  uint64_t seed;
+  uint64_t offset;
+  uint64_t theta;       /* global_threads, >= 1 */
+} sdr_rng;
+
+typedef struct {        /* one window of a row-major global tensor */
+  int32_t ndim;
+  int64_t global_shape[SDR_MAX_NDIM];
+  int64_t local_start[SDR_MAX_NDIM];
+  int64_t local_len[SDR_MAX_NDIM];
+  int64_t groups[SDR_MAX_NDIM];        /* 1 = contiguous; m for IS(d, m)       */
+  int64_t group_stride[SDR_MAX_NDIM];  /* global index distance between groups */
+} sdr_view;
+
+/* Library identity / errors. */
+int32_t sdr_version(void);
+const char* sdr_strerror(int32_t status);
+/* Last CUDA error string recorded by a failing call on this thread. */
+const char* sdr_last_cuda_error(void);
+
+/* Philox4x32-10 of one (seed, tau, beta) on the host: the same __host__
+ * __device__ round function the kernels use.  Replaces backend_block
+ * (rng.py:62-73).  out[4] = the four output words. */
+int32_t sdr_philox_block_host(uint64_t seed, uint64_t tau, uint64_t beta, uint32_t out[4]);
+
+/* Device Philox words for n (tau, beta) pairs (device arrays), writing
+ * words[4*i + w].  Replaces philox_4x32_10 over arrays (rng.py:34-59). */
+int32_t sdr_philox_blocks(const uint64_t* tau, const uint64_t* beta, int64_t n, uint64_t seed,
+                          uint32_t* words, void* stream);
+
+/* Fill one window: fill_random (rng.py:185-205) with any distribution
+ * transform (rng.py:113-182).  `out` is the contiguous local tensor. */
+int32_t sdr_fill(void* out, int32_t out_dtype, const sdr_dist* dist, const sdr_rng* rng,
+                 const sdr_view* view, void* stream);
+
+/* Multi-tensor fill: n independent fills in ONE launch (Module.materialize,
+ * model.py:121-132 -> generate_distributed, rng.py:220-235).  Each fill has
+ * its own dist/rng/view/dtype.  Table arrays are host memory. */
+int32_t sdr_fill_batch(void* const* outs, const int32_t* out_dtypes, const sdr_dist* dists,
+                       const sdr_rng* rngs, const sdr_view* views, int32_t n, void* stream);
+
+/* Fused dropout on one window: keep-mask Bernoulli(1-p) (rng.py:238-242,
+ * dispatch.py:567-576) applied as y = (x*m)*(1/(1-p)) (engine.py:80-81).
+ * x, y: contiguous local tensors; y_dtype = x_dtype, or SDR_F32 for a BF16 x
+ * (the reference's exact float32 result).  mask may be NULL; mask_dtype is
+ * SDR_U8/SDR_BOOL or x_dtype.  Also serves the backward (gx = (gy*m)*s, the
+ * mask regenerated from (seed, offset, view) instead of stored). */
+int32_t sdr_dropout(const void* x, int32_t x_dtype, void* y, int32_t y_dtype, void* mask,
+                    int32_t mask_dtype, double p, const sdr_rng* rng, const sdr_view* view,
+                    void* stream);
+
+/* NumPy transcendental mirror for Normal (rng.py:154-155): the float64 tables
+ * r[k] = sqrt(-2*log1p(-k*2^-24)) and c[k] = cos(2*pi*(k*2^-24)) for
+ * k in [0, 2^24), computed by the host's NumPy (host pointers).  Uploads them
+ * to `device`, calibrates the device fast path against them exhaustively and
+ * reports the max errors (relative for r, absolute for c). */
+int32_t sdr_normal_tables_load(int32_t device, const double* r_table, const double* c_table,
+                               double* max_rel_err_r, double* max_abs_err_c);
+int32_t sdr_normal_tables_loaded(int32_t device);
+/* Count of elements that took the exact (table) fallback since load. */
+int32_t sdr_normal_fallback_count(int32_t device, uint64_t* count);
+
+/* ---- pack / unpack for coalesced collectives (dtensor.py:261-298,
+ *      comm.py:189-199, 269-279) ---------------------------------------- */
+
+/* One member tensor of a coalesced collective.  The tensor is viewed as
+ * [outer, rows, inner] (row-major, contiguous); along the middle dim it is
+ * split into `nranks` chunks of `chunk_rows` rows (the last chunk may be
+ * shorter / empty: ceil-block split, placement.py:226-231).  Rank-major packed
+ * layout: packed[r][member m at byte offset seg_off[m]] holds chunk r of m,
+ * padded to outer*chunk_rows*inner elements.  Members may mix dtypes for
+ * gathers (bytes are moved); a reduce-scatter packs one dtype. */
+typedef struct {
+  void* data;           /* device pointer to the member tensor             */
+  int64_t outer;        /* product of dims before the split dim            */
+  int64_t rows;         /* extent of the split dim in `data`               */
+  int64_t inner;        /* product of dims after the split dim             */
+  int64_t chunk_rows;   /* ceil(global extent / nranks) along the split    */
+  int64_t seg_off;      /* BYTE offset of this member inside one rank segment */
+  int32_t elem_bytes;   /* 1, 2, 4 or 8                                     */
+  int32_t pad_;
+} sdr_pack_member;
+
+/* Gather direction of a Shard->Replicate all-gather: scatter the packed
+ * buffer (nranks segments of seg_elems elements) into full member tensors
+ * (`rows` = full extent; member data = destination). */
+int32_t sdr_unpack_gathered(const sdr_pack_member* members, int32_t n, const void* packed,
+                            int64_t seg_bytes, int32_t nranks, void* stream);
+/* Reduce-scatter input: copy full member tensors (Partial) into the
+ * rank-major packed buffer so rank r's segment holds chunk r of every member. */
+int32_t sdr_pack_scatter(const sdr_pack_member* members, int32_t n, void* packed,
+                         int64_t seg_bytes, int32_t nranks, void* stream);
+/* Copy this rank's shard of each member into (all_gather input) or out of
+ * (reduce-scatter output) one contiguous segment. member.rows = local rows. */
+int32_t sdr_pack_local(const sdr_pack_member* members, int32_t n, void* segment, void* stream);
+int32_t sdr_unpack_local(const sdr_pack_member* members, int32_t n, const void* segment,
+                         void* stream);
+
+/* INT32 pipe microbenchmark: measured IMAD.WIDE.U32 and LOP3 throughput
+ * (ops/s) on `device`, for the roofline denominator. */
+int32_t sdr_probe_int32(int32_t device, double* imad_wide_per_s, double* lop3_per_s,
+                        double* philox_blocks_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SDRNG_H_ */

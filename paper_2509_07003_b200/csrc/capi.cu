@@ -1,0 +1,113 @@
+// capi.cu -- the extern "C" boundary declared in include/sdrng.h.
+#include "sdr_core.cuh"
+
+namespace sdr {
+int fill(void* out, int dt, const sdr_dist& dist, const sdr_rng& rng, const sdr_view& view,
+         cudaStream_t s);
+int fill_batch(void* const* outs, const int32_t* dts, const sdr_dist* dists, const sdr_rng* rngs,
+               const sdr_view* views, int n, cudaStream_t s);
+int dropout(const void* x, int xt, void* y, int yt, void* mask, int mt, double p,
+            const sdr_rng& rng, const sdr_view& view, cudaStream_t s);
+int philox_blocks(const uint64_t* tau, const uint64_t* beta, int64_t n, uint64_t seed,
+                  uint32_t* words, cudaStream_t s);
+int normal_tables_load(int device, const double* r_host, const double* c_host, double* er,
+                       double* ec);
+int normal_tables_loaded(int device);
+int normal_fallback_count(int device, uint64_t* count);
+int probe_int32(int device, double* imad_per_s, double* lop3_per_s, double* philox_per_s);
+const char* last_cuda_error();
+int unpack_gathered(const sdr_pack_member* m, int n, const void* packed, int64_t seg_bytes,
+                    int nranks, cudaStream_t s);
+int pack_scatter(const sdr_pack_member* m, int n, void* packed, int64_t seg_bytes, int nranks,
+                 cudaStream_t s);
+int pack_local(const sdr_pack_member* m, int n, void* seg, cudaStream_t s);
+int unpack_local(const sdr_pack_member* m, int n, const void* seg, cudaStream_t s);
+}  // namespace sdr
+
+static cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+int32_t sdr_version(void) { return 1; }
+
+const char* sdr_strerror(int32_t status) {
+  switch (status) {
+    case SDR_OK: return "ok";
+    case SDR_E_INVALID: return "invalid argument (shape, window, pointer or count)";
+    case SDR_E_DTYPE: return "dtype not supported for this distribution/op";
+    case SDR_E_DIST: return "unknown distribution kind";
+    case SDR_E_PARAM: return "distribution parameter out of domain";
+    case SDR_E_CUDA: return "CUDA error";
+    case SDR_E_NOTABLES: return "normal() needs sdr_normal_tables_load on this device first";
+    case SDR_E_ALIGN: return "buffer misaligned";
+    default: return "unknown status";
+  }
+}
+
+const char* sdr_last_cuda_error(void) { return sdr::last_cuda_error(); }
+
+int32_t sdr_philox_block_host(uint64_t seed, uint64_t tau, uint64_t beta, uint32_t out[4]) {
+  if (out == nullptr) return SDR_E_INVALID;
+  sdr::philox10(seed, tau, beta, out);
+  return SDR_OK;
+}
+
+int32_t sdr_philox_blocks(const uint64_t* tau, const uint64_t* beta, int64_t n, uint64_t seed,
+                          uint32_t* words, void* stream) {
+  return sdr::philox_blocks(tau, beta, n, seed, words, as_stream(stream));
+}
+
+int32_t sdr_fill(void* out, int32_t out_dtype, const sdr_dist* dist, const sdr_rng* rng,
+                 const sdr_view* view, void* stream) {
+  if (dist == nullptr || rng == nullptr || view == nullptr) return SDR_E_INVALID;
+  return sdr::fill(out, out_dtype, *dist, *rng, *view, as_stream(stream));
+}
+
+int32_t sdr_fill_batch(void* const* outs, const int32_t* out_dtypes, const sdr_dist* dists,
+                       const sdr_rng* rngs, const sdr_view* views, int32_t n, void* stream) {
+  return sdr::fill_batch(outs, out_dtypes, dists, rngs, views, n, as_stream(stream));
+}
+
+int32_t sdr_dropout(const void* x, int32_t x_dtype, void* y, int32_t y_dtype, void* mask,
+                    int32_t mask_dtype, double p, const sdr_rng* rng, const sdr_view* view,
+                    void* stream) {
+  if (rng == nullptr || view == nullptr) return SDR_E_INVALID;
+  return sdr::dropout(x, x_dtype, y, y_dtype, mask, mask_dtype, p, *rng, *view, as_stream(stream));
+}
+
+int32_t sdr_normal_tables_load(int32_t device, const double* r_table, const double* c_table,
+                               double* max_rel_err_r, double* max_abs_err_c) {
+  return sdr::normal_tables_load(device, r_table, c_table, max_rel_err_r, max_abs_err_c);
+}
+
+int32_t sdr_normal_tables_loaded(int32_t device) { return sdr::normal_tables_loaded(device); }
+
+int32_t sdr_normal_fallback_count(int32_t device, uint64_t* count) {
+  return sdr::normal_fallback_count(device, count);
+}
+
+int32_t sdr_unpack_gathered(const sdr_pack_member* members, int32_t n, const void* packed,
+                            int64_t seg_bytes, int32_t nranks, void* stream) {
+  return sdr::unpack_gathered(members, n, packed, seg_bytes, nranks, as_stream(stream));
+}
+
+int32_t sdr_pack_scatter(const sdr_pack_member* members, int32_t n, void* packed,
+                         int64_t seg_bytes, int32_t nranks, void* stream) {
+  return sdr::pack_scatter(members, n, packed, seg_bytes, nranks, as_stream(stream));
+}
+
+int32_t sdr_pack_local(const sdr_pack_member* members, int32_t n, void* segment, void* stream) {
+  return sdr::pack_local(members, n, segment, as_stream(stream));
+}
+
+int32_t sdr_unpack_local(const sdr_pack_member* members, int32_t n, const void* segment,
+                         void* stream) {
+  return sdr::unpack_local(members, n, segment, as_stream(stream));
+}
+
+int32_t sdr_probe_int32(int32_t device, double* imad_wide_per_s, double* lop3_per_s,
+                        double* philox_blocks_per_s) {
+  return sdr::probe_int32(device, imad_wide_per_s, lop3_per_s, philox_blocks_per_s);
+}
+
+}  // extern "C"

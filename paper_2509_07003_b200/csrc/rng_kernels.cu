@@ -1,0 +1,1021 @@
+// rng_kernels.cu -- sm_100a kernels for the single-device-semantic RNG.
+//
+// Every element e of a window gets ONE Philox4x32-10 block on counter
+//   (beta_lo, beta_hi, tau_lo, tau_hi),  tau = j mod THETA, beta = j div THETA + offset,
+// j = its global row-major flat index (rng.py:185-205).
+// Values therefore depend only on (seed, offset, THETA, j): any rank produces
+// exactly its slice of the unsharded tensor with no communication.
+//
+// Layout of the work: a thread owns chunks of kV = 8 consecutive local elements
+// (one 16 B bf16 vector / two 16 B f32 vectors), grid-stride over the window.
+// Fast path (inner run % 8 == 0, unit inner stride, 16 B aligned buffers): the
+// chunk's 8 global indices are consecutive, so when they share beta the round-1
+// product M0*beta_lo and the round-2 product M1*y2 are computed once per chunk
+// and the round-1 products M1*(tau+e) are formed by 64-bit adds -- 16 IMAD.WIDE
+// per element instead of 20 (the last round's M0 product is dead for every
+// distribution, which uses words 0-1 only).
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "sdr_core.cuh"
+
+namespace sdr {
+
+// ---------------------------------------------------------------------------
+// Generator parameters shared by fill and dropout.
+// ---------------------------------------------------------------------------
+struct Gen {
+  uint64_t theta;
+  uint64_t offset;
+  FastDiv64 div_theta;
+  RoundKeys keys;
+};
+
+inline Gen make_gen(const sdr_rng& r) {
+  Gen g;
+  g.theta = r.theta;
+  g.offset = r.offset;
+  g.div_theta = FastDiv64(r.theta);
+  g.keys = make_keys(r.seed);
+  return g;
+}
+
+// Rounds [R0, 10) for kV independent counters.
+template <int R0>
+__device__ __forceinline__ void rounds_from(const RoundKeys& K, uint32_t (&x0)[kV],
+                                            uint32_t (&x1)[kV], uint32_t (&x2)[kV],
+                                            uint32_t (&x3)[kV]) {
+#pragma unroll
+  for (int r = R0; r < 10; ++r) {
+#pragma unroll
+    for (int e = 0; e < kV; ++e) philox_round(x0[e], x1[e], x2[e], x3[e], K.k0[r], K.k1[r]);
+  }
+}
+
+// Words 0/1 of the blocks of global indices j0 .. j0+kV-1.
+__device__ __forceinline__ void chunk_words(const Gen& g, uint64_t j0, uint32_t (&w0)[kV],
+                                            uint32_t (&w1)[kV]) {
+  uint64_t b, t;
+  g.div_theta.divmod(j0, b, t);
+  const uint64_t beta = b + g.offset;
+  uint32_t x0[kV], x1[kV], x2[kV], x3[kV];
+  const RoundKeys& K = g.keys;
+  if (g.theta >= kV && t <= g.theta - kV && lo32(t) <= 0xFFFFFFFFu - (kV - 1)) {
+    // Shared beta: hoist the chunk-uniform products of rounds 1 and 2.
+    const uint32_t blo = lo32(beta), bhi = hi32(beta), tlo = lo32(t), thi = hi32(t);
+    const uint64_t pa = mul_wide(blo, kM0);
+    const uint32_t y2 = hi32(pa) ^ thi ^ K.k1[0];
+    const uint32_t y3 = lo32(pa);
+    const uint64_t pb0 = mul_wide(tlo, kM1);
+    const uint64_t pq = mul_wide(y2, kM1);
+    const uint32_t z1 = lo32(pq), hq = hi32(pq);
+#pragma unroll
+    for (int e = 0; e < kV; ++e) {
+      const uint64_t pb = pb0 + static_cast<uint64_t>(e) * kM1;  // == M1*(tlo+e)
+      const uint32_t y0 = hi32(pb) ^ bhi ^ K.k0[0];
+      const uint32_t y1 = lo32(pb);
+      const uint64_t pa2 = mul_wide(y0, kM0);
+      x0[e] = hq ^ y1 ^ K.k0[1];
+      x1[e] = z1;
+      x2[e] = hi32(pa2) ^ y3 ^ K.k1[1];
+      x3[e] = lo32(pa2);
+    }
+    rounds_from<2>(K, x0, x1, x2, x3);
+  } else {
+#pragma unroll
+    for (int e = 0; e < kV; ++e) {
+      uint64_t be, te;
+      g.div_theta.divmod(j0 + e, be, te);
+      be += g.offset;
+      x0[e] = lo32(be);
+      x1[e] = hi32(be);
+      x2[e] = lo32(te);
+      x3[e] = hi32(te);
+    }
+    rounds_from<0>(K, x0, x1, x2, x3);
+  }
+#pragma unroll
+  for (int e = 0; e < kV; ++e) {
+    w0[e] = x0[e];
+    w1[e] = x1[e];
+  }
+}
+
+// Words of one element at global index j (generic path).
+__device__ __forceinline__ void elem_words(const Gen& g, uint64_t j, uint32_t& w0, uint32_t& w1) {
+  uint64_t b, t;
+  g.div_theta.divmod(j, b, t);
+  b += g.offset;
+  uint32_t x0 = lo32(b), x1 = hi32(b), x2 = lo32(t), x3 = hi32(t);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) philox_round(x0, x1, x2, x3, g.keys.k0[r], g.keys.k1[r]);
+  w0 = x0;
+  w1 = x1;
+}
+
+// ---------------------------------------------------------------------------
+// Output element types and conversions (NumPy / ml_dtypes semantics).
+// ---------------------------------------------------------------------------
+template <int DT> struct St;
+template <> struct St<SDR_F32> { using T = float; };
+template <> struct St<SDR_F64> { using T = double; };
+template <> struct St<SDR_BF16> { using T = uint16_t; };
+template <> struct St<SDR_F16> { using T = uint16_t; };
+template <> struct St<SDR_I64> { using T = int64_t; };
+template <> struct St<SDR_I32> { using T = int32_t; };
+template <> struct St<SDR_U8> { using T = uint8_t; };
+template <> struct St<SDR_BOOL> { using T = uint8_t; };
+
+__device__ __forceinline__ uint16_t bf16_bits(float f) {
+  return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+// float64 -> dtype with a single NumPy cast; bfloat16 goes through float32
+// first exactly like ml_dtypes' float64->bfloat16 cast.
+template <int DT>
+__device__ __forceinline__ typename St<DT>::T from_f64(double v) {
+  if constexpr (DT == SDR_F32) return __double2float_rn(v);
+  else if constexpr (DT == SDR_F64) return v;
+  else if constexpr (DT == SDR_BF16) return bf16_bits(__double2float_rn(v));
+  else if constexpr (DT == SDR_F16) return __half_as_ushort(__double2half(v));
+  else return typename St<DT>::T(0);
+}
+
+template <int DT>
+__device__ __forceinline__ typename St<DT>::T one_or_zero(bool b) {
+  if constexpr (DT == SDR_F32) return b ? 1.0f : 0.0f;
+  else if constexpr (DT == SDR_F64) return b ? 1.0 : 0.0;
+  else if constexpr (DT == SDR_BF16) return b ? uint16_t(0x3F80) : uint16_t(0);
+  else if constexpr (DT == SDR_F16) return b ? uint16_t(0x3C00) : uint16_t(0);
+  else return static_cast<typename St<DT>::T>(b ? 1 : 0);
+}
+
+// ---------------------------------------------------------------------------
+// Distribution parameters and the Normal mirror state.
+// ---------------------------------------------------------------------------
+struct NormalMirror {
+  const double* rtab;   // NumPy r[k] = sqrt(-2*log1p(-k*2^-24))
+  const double* ctab;   // NumPy c[k] = cos(2*pi*(k*2^-24))
+  double err_r;         // max |r_fast - r_np| / r_fast over all k
+  double err_c;         // max |c_fast - c_np| over all k
+  unsigned long long* fallbacks;
+};
+
+struct DistP {
+  int32_t kind;
+  float lo32, span32;          // Uniform f32 path
+  double lo, span;             // Uniform f64 path
+  double mean, stdv;           // Normal
+  uint64_t keep_thr;           // Bernoulli: keep <=> u64 < keep_thr (or always)
+  uint32_t keep_all;
+  int64_t ilo;                 // RandInt
+  FastDiv64 ispan;
+  NormalMirror nm;
+};
+
+__device__ __forceinline__ double r_fast(uint32_t k) {
+  const double u = static_cast<double>(k) * 0x1p-24;
+  return sqrt(__dmul_rn(-2.0, log1p(-u)));
+}
+__device__ __forceinline__ double c_fast(uint32_t k) {
+  const double u = static_cast<double>(k) * 0x1p-24;
+  return cos(__dmul_rn(6.283185307179586, u));
+}
+
+// Normal (rng.py:150-156): float64 Box-Muller then one cast.  Fast path with
+// the device functions + a rigorous error bound; elements whose rounding to
+// DT the bound cannot certify take the exact NumPy tables.
+template <int DT>
+__device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, uint32_t w0,
+                                                           uint32_t w1) {
+  const uint32_t k1 = w0 >> 8, k2 = w1 >> 8;
+  if constexpr (DT != SDR_F64) {
+    const double r = r_fast(k1), c = c_fast(k2);
+    const double z = __dmul_rn(r, c);
+    const double s = __dmul_rn(P.stdv, z);
+    const double v = __dadd_rn(P.mean, s);
+    const double u = 0x1p-53;
+    const double d1 = r * (P.nm.err_r * fabs(c) + P.nm.err_c * (1.0 + P.nm.err_r));
+    const double B = 2.0 * (fabs(P.stdv) * (d1 + 2.0 * u * fabs(z)) + 2.0 * u * fabs(s) +
+                            2.0 * u * fabs(v)) + 0x1p-1060;
+    const auto lo = from_f64<DT>(v - B), hi = from_f64<DT>(v + B);
+    if (lo == hi) {
+      // Also reject a signed-zero straddle: from_f64 compares bit patterns
+      // for 16-bit types; for f32 compare bits explicitly.
+      if constexpr (DT == SDR_F32) {
+        if (__float_as_uint(lo) == __float_as_uint(hi)) return lo;
+      } else {
+        return lo;
+      }
+    }
+    atomicAdd(P.nm.fallbacks, 1ull);
+  }
+  const double r = __ldg(P.nm.rtab + k1), c = __ldg(P.nm.ctab + k2);
+  const double z = __dmul_rn(r, c);
+  const double v = __dadd_rn(P.mean, __dmul_rn(P.stdv, z));
+  return from_f64<DT>(v);
+}
+
+template <int DIST, int DT>
+__device__ __forceinline__ typename St<DT>::T dist_value(const DistP& P, uint32_t w0, uint32_t w1) {
+  using T = typename St<DT>::T;
+  const uint64_t u64 = (static_cast<uint64_t>(w1) << 32) | w0;
+  if constexpr (DIST == SDR_UNIFORM01) {
+    if constexpr (DT == SDR_F32) {
+      return __fmul_rn(__uint2float_rn(w0 >> 8), 0x1p-24f);
+    } else {
+      return static_cast<T>(__ull2double_rn(u64 >> 11) * 0x1p-53);
+    }
+  } else if constexpr (DIST == SDR_UNIFORM) {
+    if constexpr (DT == SDR_F32) {
+      const float u = __fmul_rn(__uint2float_rn(w0 >> 8), 0x1p-24f);
+      return __fadd_rn(P.lo32, __fmul_rn(P.span32, u));
+    } else {
+      const double u = __ull2double_rn(u64 >> 11) * 0x1p-53;
+      return from_f64<DT>(__dadd_rn(P.lo, __dmul_rn(P.span, u)));
+    }
+  } else if constexpr (DIST == SDR_NORMAL) {
+    return normal_value<DT>(P, w0, w1);
+  } else if constexpr (DIST == SDR_RANDINT) {
+    uint64_t q, rem;
+    P.ispan.divmod(u64, q, rem);
+    const int64_t x = static_cast<int64_t>(static_cast<uint64_t>(P.ilo) + rem);
+    if constexpr (DT == SDR_I64) return x;
+    else if constexpr (DT == SDR_I32) return static_cast<int32_t>(x);
+    else if constexpr (DT == SDR_F64) return __ll2double_rn(x);
+    else if constexpr (DT == SDR_F32) return __ll2float_rn(x);
+    else return T(0);
+  } else {  // SDR_BERNOULLI
+    return one_or_zero<DT>(P.keep_all || u64 < P.keep_thr);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Vector stores of kV elements.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void store_chunk(T* p, const T (&v)[kV]) {
+  constexpr int bytes = sizeof(T) * kV;
+  if constexpr (bytes == 8) {
+    uint2 q;
+    memcpy(&q, v, 8);
+    __stcs(reinterpret_cast<uint2*>(p), q);
+  } else {
+    static_assert(bytes % 16 == 0, "chunk must be a multiple of 16 bytes");
+    uint4 q[bytes / 16];
+    memcpy(q, v, bytes);
+#pragma unroll
+    for (int i = 0; i < bytes / 16; ++i) __stcs(reinterpret_cast<uint4*>(p) + i, q[i]);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void load_chunk(const T* p, T (&v)[kV]) {
+  constexpr int bytes = sizeof(T) * kV;
+  if constexpr (bytes == 8) {
+    uint2 q = __ldcs(reinterpret_cast<const uint2*>(p));
+    memcpy(v, &q, 8);
+  } else {
+    uint4 q[bytes / 16];
+#pragma unroll
+    for (int i = 0; i < bytes / 16; ++i) q[i] = __ldcs(reinterpret_cast<const uint4*>(p) + i);
+    memcpy(v, q, bytes);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fill kernels.
+// ---------------------------------------------------------------------------
+struct __align__(16) FillArgs {
+  Gen g;
+  DistP d;
+  ViewIndexer ix;
+  void* out;
+  // Fast-path chunk walk: chunk q covers local [8q, 8q+8) inside one row.
+  uint64_t nchunks;
+  uint64_t chunks_per_row;
+  FastDiv64 div_cpr;
+};
+
+// Global flat index of the first element of chunk q (fast path).
+__device__ __forceinline__ uint64_t chunk_base(const FillArgs& A, uint64_t q) {
+  uint64_t row, cq;
+  A.div_cpr.divmod(q, row, cq);
+  uint64_t j = static_cast<uint64_t>(A.ix.cv.base) + cq * kV;
+  const CanonView& cv = A.ix.cv;
+  for (int k = cv.nd - 1; k >= 0; --k) {
+    uint64_t qq, r;
+    A.ix.div_o[k].divmod(row, qq, r);
+    j += r * static_cast<uint64_t>(cv.ostride[k]);
+    row = qq;
+  }
+  return j;
+}
+
+template <int DIST, int DT>
+__device__ __forceinline__ void fill_chunk(const FillArgs& A, uint64_t q) {
+  using T = typename St<DT>::T;
+  const uint64_t j0 = chunk_base(A, q);
+  uint32_t w0[kV], w1[kV];
+  chunk_words(A.g, j0, w0, w1);
+  T v[kV];
+#pragma unroll
+  for (int e = 0; e < kV; ++e) v[e] = dist_value<DIST, DT>(A.d, w0[e], w1[e]);
+  store_chunk(static_cast<T*>(A.out) + q * kV, v);
+}
+
+template <int DIST, int DT>
+__device__ __forceinline__ void fill_elem(const FillArgs& A, uint64_t i) {
+  using T = typename St<DT>::T;
+  uint32_t w0, w1;
+  elem_words(A.g, A.ix.global_of(i), w0, w1);
+  static_cast<T*>(A.out)[i] = dist_value<DIST, DT>(A.d, w0, w1);
+}
+
+template <int DIST, int DT>
+__global__ void __launch_bounds__(256) k_fill_fast(const __grid_constant__ FillArgs A) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < A.nchunks;
+       q += stride)
+    fill_chunk<DIST, DT>(A, q);
+}
+
+template <int DIST, int DT>
+__global__ void __launch_bounds__(256) k_fill_generic(const __grid_constant__ FillArgs A) {
+  const uint64_t n = static_cast<uint64_t>(A.ix.cv.numel);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride)
+    fill_elem<DIST, DT>(A, i);
+}
+
+// Multi-tensor fill (K3): the members of one (distribution, dtype) group are
+// cut into tiles of kTileElems elements; CTAs walk the global tile list, stage
+// the member's descriptor in shared memory once per tile and fill it.  One
+// launch initialises every parameter of a model (model.py:121-132).
+constexpr uint64_t kTileElems = 16384;
+
+template <int DIST, int DT>
+__global__ void __launch_bounds__(256) k_fill_batch(const FillArgs* __restrict__ descs,
+                                                    const uint64_t* __restrict__ tile_prefix,
+                                                    int n, uint64_t ntiles) {
+  __shared__ __align__(16) unsigned char smem[sizeof(FillArgs)];
+  FillArgs& A = *reinterpret_cast<FillArgs*>(smem);
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    // member f: last index with tile_prefix[f] <= t (uniform across the CTA)
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tile_prefix[mid] <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    __syncthreads();  // previous tile done with A
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(descs + lo);
+      uint4* dst = reinterpret_cast<uint4*>(smem);
+      for (int i = threadIdx.x; i < static_cast<int>(sizeof(FillArgs) / 16); i += blockDim.x)
+        dst[i] = src[i];
+    }
+    __syncthreads();
+    const uint64_t lt = t - tile_prefix[lo];
+    if (A.nchunks > 0) {
+      const uint64_t q0 = lt * (kTileElems / kV);
+      uint64_t q1 = q0 + kTileElems / kV;
+      if (q1 > A.nchunks) q1 = A.nchunks;
+      for (uint64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) fill_chunk<DIST, DT>(A, q);
+    } else {
+      const uint64_t i0 = lt * kTileElems;
+      uint64_t i1 = i0 + kTileElems;
+      const uint64_t numel = static_cast<uint64_t>(A.ix.cv.numel);
+      if (i1 > numel) i1 = numel;
+      for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) fill_elem<DIST, DT>(A, i);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused dropout: y = (x*m)*scale, m from Bernoulli(1-p) (engine.py:80-81).
+// ---------------------------------------------------------------------------
+struct DropArgs {
+  Gen g;
+  ViewIndexer ix;
+  const void* x;
+  void* y;
+  void* mask;
+  uint64_t keep_thr;
+  uint32_t keep_all;
+  float scale32;
+  double scale64;
+  uint16_t scale16;  // f16 bits of the scale
+  uint64_t nchunks;
+  uint64_t chunks_per_row;
+  FastDiv64 div_cpr;
+};
+
+template <int XT> struct DropT { using T = typename St<XT>::T; };
+
+// y element for input dtype XT and output dtype YT.
+template <int XT, int YT>
+__device__ __forceinline__ typename St<YT>::T drop_apply(const DropArgs& A, typename St<XT>::T x,
+                                                         bool keep) {
+  if constexpr (XT == SDR_F32) {
+    return __fmul_rn(__fmul_rn(x, keep ? 1.0f : 0.0f), A.scale32);
+  } else if constexpr (XT == SDR_F64) {
+    return __dmul_rn(__dmul_rn(x, keep ? 1.0 : 0.0), A.scale64);
+  } else if constexpr (XT == SDR_BF16) {
+    const float xf = __uint_as_float(static_cast<uint32_t>(x) << 16);
+    const float y = __fmul_rn(__fmul_rn(xf, keep ? 1.0f : 0.0f), A.scale32);
+    if constexpr (YT == SDR_F32) return y;
+    else return bf16_bits(y);
+  } else {  // SDR_F16: x*m exact in f16, then RNE(x16 * scale16)
+    const __half xh = __ushort_as_half(x);
+    const __half xm = __hmul(xh, keep ? __ushort_as_half(0x3C00) : __ushort_as_half(0));
+    return __half_as_ushort(__hmul(xm, __ushort_as_half(A.scale16)));
+  }
+}
+
+__device__ __forceinline__ uint64_t drop_chunk_base(const DropArgs& A, uint64_t q) {
+  uint64_t row, cq;
+  A.div_cpr.divmod(q, row, cq);
+  uint64_t j = static_cast<uint64_t>(A.ix.cv.base) + cq * kV;
+  const CanonView& cv = A.ix.cv;
+  for (int k = cv.nd - 1; k >= 0; --k) {
+    uint64_t qq, r;
+    A.ix.div_o[k].divmod(row, qq, r);
+    j += r * static_cast<uint64_t>(cv.ostride[k]);
+    row = qq;
+  }
+  return j;
+}
+
+template <int XT, int YT, int MT>
+__global__ void __launch_bounds__(256) k_dropout_fast(const __grid_constant__ DropArgs A) {
+  using XTy = typename St<XT>::T;
+  using YTy = typename St<YT>::T;
+  const XTy* x = static_cast<const XTy*>(A.x);
+  YTy* y = static_cast<YTy*>(A.y);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < A.nchunks;
+       q += stride) {
+    XTy xv[kV];
+    load_chunk(x + q * kV, xv);
+    const uint64_t j0 = drop_chunk_base(A, q);
+    uint32_t w0[kV], w1[kV];
+    chunk_words(A.g, j0, w0, w1);
+    YTy yv[kV];
+    bool keep[kV];
+#pragma unroll
+    for (int e = 0; e < kV; ++e) {
+      const uint64_t u64 = (static_cast<uint64_t>(w1[e]) << 32) | w0[e];
+      keep[e] = A.keep_all || u64 < A.keep_thr;
+      yv[e] = drop_apply<XT, YT>(A, xv[e], keep[e]);
+    }
+    store_chunk(y + q * kV, yv);
+    if constexpr (MT >= 0) {
+      using MTy = typename St<MT>::T;
+      if (A.mask != nullptr) {
+        MTy mv[kV];
+#pragma unroll
+        for (int e = 0; e < kV; ++e) mv[e] = one_or_zero<MT>(keep[e]);
+        store_chunk(static_cast<MTy*>(A.mask) + q * kV, mv);
+      }
+    }
+  }
+}
+
+template <int XT, int YT, int MT>
+__global__ void __launch_bounds__(256) k_dropout_generic(const __grid_constant__ DropArgs A) {
+  using XTy = typename St<XT>::T;
+  using YTy = typename St<YT>::T;
+  const XTy* x = static_cast<const XTy*>(A.x);
+  YTy* y = static_cast<YTy*>(A.y);
+  const uint64_t n = static_cast<uint64_t>(A.ix.cv.numel);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    uint32_t w0, w1;
+    elem_words(A.g, A.ix.global_of(i), w0, w1);
+    const uint64_t u64 = (static_cast<uint64_t>(w1) << 32) | w0;
+    const bool keep = A.keep_all || u64 < A.keep_thr;
+    y[i] = drop_apply<XT, YT>(A, x[i], keep);
+    if constexpr (MT >= 0) {
+      using MTy = typename St<MT>::T;
+      if (A.mask != nullptr) static_cast<MTy*>(A.mask)[i] = one_or_zero<MT>(keep);
+    }
+  }
+}
+
+// Raw Philox words for (tau, beta) arrays (KAT / debug entry).
+__global__ void k_philox_blocks(const uint64_t* tau, const uint64_t* beta, int64_t n,
+                                const __grid_constant__ RoundKeys K, uint32_t* words) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t x0 = lo32(beta[i]), x1 = hi32(beta[i]), x2 = lo32(tau[i]), x3 = hi32(tau[i]);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) philox_round(x0, x1, x2, x3, K.k0[r], K.k1[r]);
+  words[4 * i + 0] = x0;
+  words[4 * i + 1] = x1;
+  words[4 * i + 2] = x2;
+  words[4 * i + 3] = x3;
+}
+
+// Exhaustive calibration of the Normal fast path against the NumPy tables.
+__global__ void k_normal_calibrate(const double* rtab, const double* ctab,
+                                   unsigned long long* max_r_bits,
+                                   unsigned long long* max_c_bits) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (1u << 24)) return;
+  const double rg = r_fast(k), rn = rtab[k];
+  double er;
+  if (rg == 0.0 || rn == 0.0) er = (rg == rn) ? 0.0 : __longlong_as_double(0x7FF0000000000000ll);
+  else er = fabs(rg - rn) / rg;
+  const double ec = fabs(c_fast(k) - ctab[k]);
+  unsigned long long br = __double_as_longlong(er), bc = __double_as_longlong(ec);
+  // Non-negative doubles order like their bit patterns; reduce per warp first.
+  for (int o = 16; o > 0; o >>= 1) {
+    br = max(br, __shfl_xor_sync(0xffffffffu, br, o));
+    bc = max(bc, __shfl_xor_sync(0xffffffffu, bc, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(max_r_bits, br);
+    atomicMax(max_c_bits, bc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side.
+// ---------------------------------------------------------------------------
+static thread_local char g_cuda_err[256] = "";
+
+void set_cuda_error(cudaError_t e) {
+  snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+int check_launch() {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_cuda_error(e);
+    return SDR_E_CUDA;
+  }
+  return SDR_OK;
+}
+
+int canonicalize(const sdr_view& v, CanonView& cv) {
+  if (v.ndim < 0 || v.ndim > SDR_MAX_NDIM) return SDR_E_INVALID;
+  int64_t size[kMaxCanon], stride[kMaxCanon];
+  int n = 0;
+  int64_t pi = 1, base = 0, numel = 1;
+  // Row-major global strides, innermost last.
+  int64_t gstr[SDR_MAX_NDIM];
+  for (int d = v.ndim - 1; d >= 0; --d) {
+    if (v.global_shape[d] < 0) return SDR_E_INVALID;
+    gstr[d] = pi;
+    pi *= (v.global_shape[d] > 0 ? v.global_shape[d] : 1);
+  }
+  for (int d = 0; d < v.ndim; ++d) {
+    const int64_t G = v.global_shape[d], s = v.local_start[d], len = v.local_len[d];
+    const int64_t m = v.groups[d] > 0 ? v.groups[d] : 1;
+    if (s < 0 || len < 0) return SDR_E_INVALID;
+    numel *= len;
+    if (m == 1) {
+      if (len > 0 && s + len > G) return SDR_E_INVALID;
+      base += s * gstr[d];
+      size[n] = len;
+      stride[n] = gstr[d];
+      ++n;
+    } else {
+      if (len % m != 0) return SDR_E_INVALID;
+      const int64_t per = len / m, gs = v.group_stride[d];
+      if (per > 0 && (gs < per || s + (m - 1) * gs + per > G)) return SDR_E_INVALID;
+      base += s * gstr[d];
+      size[n] = m;
+      stride[n] = gs * gstr[d];
+      ++n;
+      size[n] = per;
+      stride[n] = gstr[d];
+      ++n;
+    }
+  }
+  cv = CanonView{};
+  cv.numel = numel;
+  cv.base = base;
+  if (numel == 0) {
+    cv.nd = 0;
+    cv.inner = 1;
+    cv.istride = 1;
+    return SDR_OK;
+  }
+  // Drop size-1 dims, then merge (outer, inner) pairs that are contiguous.
+  int64_t ms[kMaxCanon], mst[kMaxCanon];
+  int k = 0;
+  for (int i = 0; i < n; ++i) {
+    if (size[i] == 1) continue;
+    if (k > 0 && mst[k - 1] == size[i] * stride[i]) {
+      ms[k - 1] *= size[i];
+      mst[k - 1] = stride[i];
+    } else {
+      ms[k] = size[i];
+      mst[k] = stride[i];
+      ++k;
+    }
+  }
+  if (k == 0) {
+    cv.nd = 0;
+    cv.inner = 1;
+    cv.istride = 1;
+    return SDR_OK;
+  }
+  cv.inner = ms[k - 1];
+  cv.istride = mst[k - 1];
+  cv.nd = k - 1;
+  for (int i = 0; i < k - 1; ++i) {
+    cv.osize[i] = ms[i];
+    cv.ostride[i] = mst[i];
+  }
+  return SDR_OK;
+}
+
+static int launch_grid(uint64_t work, int threads) {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const uint64_t blocks = (work + threads - 1) / threads;
+  const uint64_t cap = static_cast<uint64_t>(sms) * 8;  // persistent: <= 8 CTAs of 256 per SM
+  return static_cast<int>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+}
+
+// Per-device Normal mirror tables.
+struct NormalState {
+  double* rtab = nullptr;
+  double* ctab = nullptr;
+  unsigned long long* fallbacks = nullptr;
+  double err_r = 0, err_c = 0;
+  bool loaded = false;
+};
+static std::mutex g_nm_mu;
+static NormalState g_nm[64];
+
+static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) {
+  memset(static_cast<void*>(&P), 0, sizeof(P));
+  P.kind = dist.kind;
+  P.ispan = FastDiv64(1);
+  switch (dist.kind) {
+    case SDR_UNIFORM01:
+      if (dt != SDR_F32 && dt != SDR_F64) return SDR_E_DTYPE;
+      break;
+    case SDR_UNIFORM: {
+      const double lo = dist.fparam[0], hi = dist.fparam[1];
+      if (!(lo < hi)) return SDR_E_PARAM;
+      if (dt != SDR_F32 && dt != SDR_F64 && dt != SDR_BF16 && dt != SDR_F16) return SDR_E_DTYPE;
+      // hi - lo is formed in Python float64 then weakly cast (rng.py:138).
+      P.lo = lo;
+      P.span = hi - lo;
+      P.lo32 = static_cast<float>(lo);
+      P.span32 = static_cast<float>(hi - lo);
+      break;
+    }
+    case SDR_NORMAL: {
+      if (!(dist.fparam[1] > 0)) return SDR_E_PARAM;
+      if (dt != SDR_F32 && dt != SDR_F64 && dt != SDR_BF16 && dt != SDR_F16) return SDR_E_DTYPE;
+      P.mean = dist.fparam[0];
+      P.stdv = dist.fparam[1];
+      std::lock_guard<std::mutex> lk(g_nm_mu);
+      if (device < 0 || device >= 64 || !g_nm[device].loaded) return SDR_E_NOTABLES;
+      P.nm.rtab = g_nm[device].rtab;
+      P.nm.ctab = g_nm[device].ctab;
+      P.nm.err_r = g_nm[device].err_r;
+      P.nm.err_c = g_nm[device].err_c;
+      P.nm.fallbacks = g_nm[device].fallbacks;
+      break;
+    }
+    case SDR_RANDINT: {
+      const int64_t lo = dist.iparam[0], hi = dist.iparam[1];
+      if (!(lo < hi)) return SDR_E_PARAM;
+      if (dt != SDR_I64 && dt != SDR_I32 && dt != SDR_F64 && dt != SDR_F32) return SDR_E_DTYPE;
+      P.ilo = lo;
+      P.ispan = FastDiv64(static_cast<uint64_t>(hi) - static_cast<uint64_t>(lo));
+      break;
+    }
+    case SDR_BERNOULLI: {
+      const double p = dist.fparam[0];
+      if (!(p >= 0.0 && p <= 1.0)) return SDR_E_PARAM;
+      // u < p  <=>  k53 < ceil(p * 2^53)  <=>  u64 < ceil(p*2^53) << 11.
+      const double t = ceil(p * 9007199254740992.0);
+      const uint64_t T = static_cast<uint64_t>(t);
+      P.keep_all = (T >= (uint64_t{1} << 53)) ? 1u : 0u;
+      P.keep_thr = P.keep_all ? 0 : (T << 11);
+      break;
+    }
+    default:
+      return SDR_E_DIST;
+  }
+  return SDR_OK;
+}
+
+static void setup_chunks(const CanonView& cv, bool fast, uint64_t& nchunks, uint64_t& cpr,
+                         FastDiv64& div_cpr) {
+  if (fast) {
+    cpr = static_cast<uint64_t>(cv.inner) / kV;
+    nchunks = static_cast<uint64_t>(cv.numel) / kV;
+  } else {
+    cpr = 1;
+    nchunks = 0;
+  }
+  div_cpr = FastDiv64(cpr > 0 ? cpr : 1);
+}
+
+template <int DIST, int DT>
+static void launch_fill(const FillArgs& A, bool fast, cudaStream_t s) {
+  if (fast) {
+    k_fill_fast<DIST, DT><<<launch_grid(A.nchunks, 256), 256, 0, s>>>(A);
+  } else {
+    k_fill_generic<DIST, DT><<<launch_grid(A.ix.cv.numel, 256), 256, 0, s>>>(A);
+  }
+}
+
+template <int DIST>
+static int dispatch_fill_dt(int dt, const FillArgs& A, bool fast, cudaStream_t s) {
+  switch (dt) {
+    case SDR_F32: launch_fill<DIST, SDR_F32>(A, fast, s); break;
+    case SDR_F64: launch_fill<DIST, SDR_F64>(A, fast, s); break;
+    case SDR_BF16:
+      if constexpr (DIST != SDR_UNIFORM01 && DIST != SDR_RANDINT) launch_fill<DIST, SDR_BF16>(A, fast, s);
+      else return SDR_E_DTYPE;
+      break;
+    case SDR_F16:
+      if constexpr (DIST != SDR_UNIFORM01 && DIST != SDR_RANDINT) launch_fill<DIST, SDR_F16>(A, fast, s);
+      else return SDR_E_DTYPE;
+      break;
+    case SDR_I64:
+      if constexpr (DIST == SDR_RANDINT || DIST == SDR_BERNOULLI) launch_fill<DIST, SDR_I64>(A, fast, s);
+      else return SDR_E_DTYPE;
+      break;
+    case SDR_I32:
+      if constexpr (DIST == SDR_RANDINT || DIST == SDR_BERNOULLI) launch_fill<DIST, SDR_I32>(A, fast, s);
+      else return SDR_E_DTYPE;
+      break;
+    case SDR_U8:
+      if constexpr (DIST == SDR_BERNOULLI) launch_fill<DIST, SDR_U8>(A, fast, s);
+      else return SDR_E_DTYPE;
+      break;
+    case SDR_BOOL:
+      if constexpr (DIST == SDR_BERNOULLI) launch_fill<DIST, SDR_BOOL>(A, fast, s);
+      else return SDR_E_DTYPE;
+      break;
+    default:
+      return SDR_E_DTYPE;
+  }
+  return check_launch();
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int fill(void* out, int dt, const sdr_dist& dist, const sdr_rng& rng, const sdr_view& view,
+         cudaStream_t s) {
+  if (rng.theta < 1) return SDR_E_INVALID;
+  if (dtype_size(dt) == 0) return SDR_E_DTYPE;
+  CanonView cv;
+  int st = canonicalize(view, cv);
+  if (st != SDR_OK) return st;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  FillArgs A;
+  memset(static_cast<void*>(&A), 0, sizeof(A));
+  st = fill_dist_params(dist, dt, A.d, dev);
+  if (st != SDR_OK) return st;
+  if (cv.numel == 0) return SDR_OK;
+  if (out == nullptr) return SDR_E_INVALID;
+  A.g = make_gen(rng);
+  A.ix = make_indexer(cv);
+  A.out = out;
+  const bool fast = cv.istride == 1 && cv.inner % kV == 0 && aligned16(out);
+  setup_chunks(cv, fast, A.nchunks, A.chunks_per_row, A.div_cpr);
+  switch (dist.kind) {
+    case SDR_UNIFORM01: return dispatch_fill_dt<SDR_UNIFORM01>(dt, A, fast, s);
+    case SDR_UNIFORM: return dispatch_fill_dt<SDR_UNIFORM>(dt, A, fast, s);
+    case SDR_NORMAL: return dispatch_fill_dt<SDR_NORMAL>(dt, A, fast, s);
+    case SDR_RANDINT: return dispatch_fill_dt<SDR_RANDINT>(dt, A, fast, s);
+    case SDR_BERNOULLI: return dispatch_fill_dt<SDR_BERNOULLI>(dt, A, fast, s);
+    default: return SDR_E_DIST;
+  }
+}
+
+template <int XT, int YT, int MT>
+static int launch_drop(const DropArgs& A, bool fast, cudaStream_t s) {
+  if (fast) k_dropout_fast<XT, YT, MT><<<launch_grid(A.nchunks, 256), 256, 0, s>>>(A);
+  else k_dropout_generic<XT, YT, MT><<<launch_grid(A.ix.cv.numel, 256), 256, 0, s>>>(A);
+  return check_launch();
+}
+
+template <int XT, int YT>
+static int dispatch_drop_mask(int mt, const DropArgs& A, bool fast, cudaStream_t s) {
+  if (A.mask == nullptr) return launch_drop<XT, YT, -1>(A, fast, s);
+  if (mt == SDR_U8 || mt == SDR_BOOL) return launch_drop<XT, YT, SDR_U8>(A, fast, s);
+  if (mt == XT) return launch_drop<XT, YT, XT>(A, fast, s);
+  return SDR_E_DTYPE;
+}
+
+int dropout(const void* x, int xt, void* y, int yt, void* mask, int mt, double p,
+            const sdr_rng& rng, const sdr_view& view, cudaStream_t s) {
+  if (!(p >= 0.0 && p < 1.0)) return SDR_E_PARAM;
+  if (rng.theta < 1) return SDR_E_INVALID;
+  CanonView cv;
+  int st = canonicalize(view, cv);
+  if (st != SDR_OK) return st;
+  if (cv.numel == 0) return SDR_OK;
+  if (x == nullptr || y == nullptr) return SDR_E_INVALID;
+  DropArgs A;
+  memset(static_cast<void*>(&A), 0, sizeof(A));
+  A.g = make_gen(rng);
+  A.ix = make_indexer(cv);
+  A.x = x;
+  A.y = y;
+  A.mask = mask;
+  // keep-prob 1-p in float64 (rng.py:242), threshold ceil((1-p)*2^53).
+  const double pk = 1.0 - p;
+  const uint64_t T = static_cast<uint64_t>(ceil(pk * 9007199254740992.0));
+  A.keep_all = (T >= (uint64_t{1} << 53)) ? 1u : 0u;
+  A.keep_thr = A.keep_all ? 0 : (T << 11);
+  const double scale = 1.0 / (1.0 - p);
+  A.scale64 = scale;
+  A.scale32 = static_cast<float>(scale);
+  A.scale16 = __half_as_ushort(__double2half(scale));
+  bool fast = cv.istride == 1 && cv.inner % kV == 0 && aligned16(x) && aligned16(y) &&
+              (mask == nullptr || (reinterpret_cast<uintptr_t>(mask) & 7u) == 0);
+  setup_chunks(cv, fast, A.nchunks, A.chunks_per_row, A.div_cpr);
+  if (xt == SDR_F32 && yt == SDR_F32) return dispatch_drop_mask<SDR_F32, SDR_F32>(mt, A, fast, s);
+  if (xt == SDR_F64 && yt == SDR_F64) return dispatch_drop_mask<SDR_F64, SDR_F64>(mt, A, fast, s);
+  if (xt == SDR_BF16 && yt == SDR_BF16) return dispatch_drop_mask<SDR_BF16, SDR_BF16>(mt, A, fast, s);
+  if (xt == SDR_BF16 && yt == SDR_F32) return dispatch_drop_mask<SDR_BF16, SDR_F32>(mt, A, fast, s);
+  if (xt == SDR_F16 && yt == SDR_F16) return dispatch_drop_mask<SDR_F16, SDR_F16>(mt, A, fast, s);
+  return SDR_E_DTYPE;
+}
+
+int philox_blocks(const uint64_t* tau, const uint64_t* beta, int64_t n, uint64_t seed,
+                  uint32_t* words, cudaStream_t s) {
+  if (n < 0) return SDR_E_INVALID;
+  if (n == 0) return SDR_OK;
+  const RoundKeys K = make_keys(seed);
+  k_philox_blocks<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(tau, beta, n, K, words);
+  return check_launch();
+}
+
+int normal_tables_load(int device, const double* r_host, const double* c_host, double* er,
+                       double* ec) {
+  if (device < 0 || device >= 64 || r_host == nullptr || c_host == nullptr) return SDR_E_INVALID;
+  std::lock_guard<std::mutex> lk(g_nm_mu);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  NormalState& S = g_nm[device];
+  const size_t bytes = sizeof(double) << 24;
+  cudaError_t e = cudaSuccess;
+  if (S.rtab == nullptr) {
+    e = cudaMalloc(&S.rtab, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&S.ctab, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&S.fallbacks, 3 * sizeof(unsigned long long));
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(S.rtab, r_host, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(S.ctab, c_host, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(S.fallbacks, 0, 3 * sizeof(unsigned long long));
+  if (e == cudaSuccess) {
+    k_normal_calibrate<<<(1u << 24) / 256, 256>>>(S.rtab, S.ctab, S.fallbacks + 1, S.fallbacks + 2);
+    e = cudaGetLastError();
+  }
+  unsigned long long bits[2] = {0, 0};
+  if (e == cudaSuccess) e = cudaMemcpy(bits, S.fallbacks + 1, 2 * sizeof(bits[0]), cudaMemcpyDeviceToHost);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    set_cuda_error(e);
+    return SDR_E_CUDA;
+  }
+  memcpy(&S.err_r, &bits[0], 8);
+  memcpy(&S.err_c, &bits[1], 8);
+  S.loaded = true;
+  if (er) *er = S.err_r;
+  if (ec) *ec = S.err_c;
+  return SDR_OK;
+}
+
+int normal_tables_loaded(int device) {
+  std::lock_guard<std::mutex> lk(g_nm_mu);
+  return (device >= 0 && device < 64 && g_nm[device].loaded) ? 1 : 0;
+}
+
+int normal_fallback_count(int device, uint64_t* count) {
+  std::lock_guard<std::mutex> lk(g_nm_mu);
+  if (device < 0 || device >= 64 || !g_nm[device].loaded || count == nullptr) return SDR_E_NOTABLES;
+  unsigned long long c = 0;
+  cudaError_t e = cudaMemcpy(&c, g_nm[device].fallbacks, sizeof(c), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    set_cuda_error(e);
+    return SDR_E_CUDA;
+  }
+  *count = c;
+  return SDR_OK;
+}
+
+template <int DIST, int DT>
+static void launch_batch(const FillArgs* d_descs, const uint64_t* d_prefix, int n, uint64_t ntiles,
+                         cudaStream_t s) {
+  k_fill_batch<DIST, DT><<<launch_grid(ntiles * 256, 256), 256, 0, s>>>(d_descs, d_prefix, n, ntiles);
+}
+
+template <int DIST>
+static int dispatch_batch_dt(int dt, const FillArgs* d, const uint64_t* p, int n, uint64_t nt,
+                             cudaStream_t s) {
+  switch (dt) {
+    case SDR_F32: launch_batch<DIST, SDR_F32>(d, p, n, nt, s); break;
+    case SDR_F64: launch_batch<DIST, SDR_F64>(d, p, n, nt, s); break;
+    case SDR_BF16:
+      if constexpr (DIST != SDR_UNIFORM01 && DIST != SDR_RANDINT) launch_batch<DIST, SDR_BF16>(d, p, n, nt, s);
+      else return SDR_E_DTYPE;
+      break;
+    case SDR_F16:
+      if constexpr (DIST != SDR_UNIFORM01 && DIST != SDR_RANDINT) launch_batch<DIST, SDR_F16>(d, p, n, nt, s);
+      else return SDR_E_DTYPE;
+      break;
+    default:
+      return SDR_E_DTYPE;
+  }
+  return check_launch();
+}
+
+int fill_batch(void* const* outs, const int32_t* dts, const sdr_dist* dists, const sdr_rng* rngs,
+               const sdr_view* views, int n, cudaStream_t s) {
+  if (n < 0 || (n > 0 && (outs == nullptr || dts == nullptr || dists == nullptr ||
+                          rngs == nullptr || views == nullptr)))
+    return SDR_E_INVALID;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  // Validate everything first; group members by (distribution kind, dtype).
+  struct Member { FillArgs a; uint64_t tiles; };
+  std::vector<std::vector<Member>> groups(5 * 8);
+  for (int i = 0; i < n; ++i) {
+    if (rngs[i].theta < 1) return SDR_E_INVALID;
+    const int dt = dts[i];
+    if (dtype_size(dt) == 0 || dists[i].kind < 0 || dists[i].kind > 4) return SDR_E_DTYPE;
+    CanonView cv;
+    int st = canonicalize(views[i], cv);
+    if (st != SDR_OK) return st;
+    Member m;
+    memset(static_cast<void*>(&m), 0, sizeof(m));
+    st = fill_dist_params(dists[i], dt, m.a.d, dev);
+    if (st != SDR_OK) return st;
+    if (dt != SDR_F32 && dt != SDR_F64 && dt != SDR_BF16 && dt != SDR_F16) return SDR_E_DTYPE;
+    if (cv.numel == 0) continue;
+    if (outs[i] == nullptr) return SDR_E_INVALID;
+    m.a.g = make_gen(rngs[i]);
+    m.a.ix = make_indexer(cv);
+    m.a.out = outs[i];
+    const bool fast = cv.istride == 1 && cv.inner % kV == 0 && aligned16(outs[i]);
+    setup_chunks(cv, fast, m.a.nchunks, m.a.chunks_per_row, m.a.div_cpr);
+    m.tiles = (static_cast<uint64_t>(cv.numel) + kTileElems - 1) / kTileElems;
+    groups[dists[i].kind * 8 + dt].push_back(m);
+  }
+  for (int gi = 0; gi < static_cast<int>(groups.size()); ++gi) {
+    auto& G = groups[gi];
+    if (G.empty()) continue;
+    const int kind = gi / 8, dt = gi % 8, m = static_cast<int>(G.size());
+    std::vector<FillArgs> descs(m);
+    std::vector<uint64_t> prefix(m);
+    uint64_t tiles = 0;
+    for (int i = 0; i < m; ++i) {
+      descs[i] = G[i].a;
+      prefix[i] = tiles;
+      tiles += G[i].tiles;
+    }
+    FillArgs* d_descs = nullptr;
+    uint64_t* d_prefix = nullptr;
+    cudaError_t e = cudaMallocAsync(&d_descs, sizeof(FillArgs) * m, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(&d_prefix, sizeof(uint64_t) * m, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_descs, descs.data(), sizeof(FillArgs) * m, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_prefix, prefix.data(), sizeof(uint64_t) * m, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) {
+      set_cuda_error(e);
+      return SDR_E_CUDA;
+    }
+    int st;
+    switch (kind) {
+      case SDR_UNIFORM01: st = dispatch_batch_dt<SDR_UNIFORM01>(dt, d_descs, d_prefix, m, tiles, s); break;
+      case SDR_UNIFORM: st = dispatch_batch_dt<SDR_UNIFORM>(dt, d_descs, d_prefix, m, tiles, s); break;
+      case SDR_NORMAL: st = dispatch_batch_dt<SDR_NORMAL>(dt, d_descs, d_prefix, m, tiles, s); break;
+      case SDR_RANDINT: st = dispatch_batch_dt<SDR_RANDINT>(dt, d_descs, d_prefix, m, tiles, s); break;
+      default: st = dispatch_batch_dt<SDR_BERNOULLI>(dt, d_descs, d_prefix, m, tiles, s); break;
+    }
+    cudaFreeAsync(d_descs, s);
+    cudaFreeAsync(d_prefix, s);
+    if (st != SDR_OK) return st;
+  }
+  return SDR_OK;
+}
+
+const char* last_cuda_error() { return g_cuda_err; }
+
+}  // namespace sdr

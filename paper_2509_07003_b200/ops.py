@@ -1,0 +1,107 @@
+"""Random ops on torch tensors: fused sharded dropout with mask recomputation.
+
+Mirrors the dropout call path of the reference -- ops.dropout (reference
+/root/reference/pkg/src/spmdsim/ops.py:168-190) -> dispatch._execute's mask
+branch (dispatch.py:567-576) -> rng.dropout_mask_local (rng.py:238-242) ->
+engine.k_dropout_apply (engine.py:80-81) -- as ONE sm_100a kernel
+(`sdr_dropout`) that draws the keep-mask and applies it in a single pass.
+
+Backward regenerates the mask from the saved (seed, offset, THETA, window)
+instead of storing it: gx = (g * m) * (1/(1-p)), the same
+expression the reference's backward closure evaluates (ops.py:187-188).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+
+from . import _lib, runtime as runtime_mod
+from .placement import ShardView, full_view
+from .rng import RngState, dtype_code
+
+_DROP_TYPES = (torch.float32, torch.float64, torch.bfloat16, torch.float16)
+
+
+def _check_p(status):
+    if status == _lib.E_PARAM:
+        return ValueError("dropout needs p in [0, 1)")
+    if status == _lib.E_DTYPE:
+        return TypeError("dtype not supported by dropout")
+    return None
+
+
+def dropout_apply(x: torch.Tensor, p: float, state: RngState, view: ShardView | None = None, *,
+                  out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None,
+                  mask: torch.Tensor | None = None) -> torch.Tensor:
+    """One fused launch: y = (x * m) * (1/(1-p)) with m the keep-mask of
+    Bernoulli(1-p) drawn at `state` over `view` (the window x holds; default:
+    x is the whole tensor).  Does NOT advance `state`.
+
+    out_dtype: x.dtype (default), or torch.float32 for a bfloat16 x -- the
+    reference's own result dtype (ml_dtypes bf16 * Python float -> float32).
+    mask: optional uint8/bool or x.dtype tensor receiving m."""
+    if not 0.0 <= p < 1.0:
+        raise ValueError(f"dropout needs p in [0, 1), got {p}")
+    if x.dtype not in _DROP_TYPES:
+        raise TypeError(f"dropout supports {_DROP_TYPES}, got {x.dtype}")
+    if not x.is_cuda:
+        raise ValueError("dropout runs on CUDA tensors only")
+    view = full_view(tuple(x.shape)) if view is None else view
+    if tuple(x.shape) != view.local_shape:
+        raise ValueError(f"x has shape {tuple(x.shape)}, window is {view.local_shape}")
+    x = x.contiguous()
+    yd = x.dtype if out_dtype is None else out_dtype
+    if out is None:
+        out = torch.empty(x.shape, dtype=yd, device=x.device)
+    mcode = -1
+    if mask is not None:
+        if mask.shape != x.shape or not mask.is_contiguous():
+            raise ValueError("mask must be contiguous with x's shape")
+        mcode = dtype_code(mask.dtype)
+    if x.numel() == 0:
+        return out
+    nr, nv = state.native(), view.to_native()
+    with torch.cuda.device(x.device):
+        st = _lib.LIB.sdr_dropout(x.data_ptr(), dtype_code(x.dtype), out.data_ptr(), dtype_code(yd),
+                                  None if mask is None else mask.data_ptr(), mcode, float(p),
+                                  C.byref(nr), C.byref(nv), _lib.stream_handle(x.device))
+    _lib.check(st, "sdr_dropout", _check_p)
+    return out
+
+
+class _Dropout(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, p, state_tuple, view):
+        st = RngState(*state_tuple)
+        ctx.p, ctx.state_tuple, ctx.view = p, state_tuple, view
+        return dropout_apply(x, p, st, view)
+
+    @staticmethod
+    def backward(ctx, g):
+        gx = dropout_apply(g.contiguous(), ctx.p, RngState(*ctx.state_tuple), ctx.view)
+        return gx, None, None, None
+
+
+def dropout(x: torch.Tensor, p: float, state: RngState | None = None,
+            view: ShardView | None = None, training: bool = True) -> torch.Tensor:
+    """Dropout with single-device semantics (reference ops.py:168-190).
+
+    `view` is the window of the global tensor that x holds (default: all of
+    it); the mask is the slice of ONE global Bernoulli draw, so any sharding
+    gives the same merged output.  p == 0 returns x and consumes no random
+    numbers (ops.py:174-175); otherwise the state advances by
+    ceil(global_numel / THETA) on every rank."""
+    if not training or p == 0.0:
+        return x
+    state = runtime_mod.current().rng if state is None else state
+    view = full_view(tuple(x.shape)) if view is None else view
+    snap = (state.seed, state.offset, state.global_threads)
+    if x.requires_grad and torch.is_grad_enabled():
+        y = _Dropout.apply(x, p, snap, view)
+    else:
+        y = dropout_apply(x, p, state, view)
+    state.advance(math.prod(view.global_shape))
+    return y

@@ -1,0 +1,117 @@
+"""GPU parity of the fused sharded dropout (mask + apply in one sm_100a kernel).
+
+Reference semantics: ops.dropout (ops.py:168-190), dispatch dropout branch
+(dispatch.py:567-576), dropout_mask_local (rng.py:238-242), k_dropout_apply
+(engine.py:80-81); placement invariance (test_dispatch.py:183-193) and the
+dropout gradient = rescaled mask (test_engine.py:86-95).
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import bits, decode
+from oracle import rng_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2509_07003_b200 as S
+    from paper_2509_07003_b200 import ops, rng as R
+    from paper_2509_07003_b200.placement import ShardSpec, full_view, local_shape_and_offset, parse_placements
+
+TORCH_DT = {"float32": torch.float32, "float64": torch.float64, "bfloat16": torch.bfloat16,
+            "float16": torch.float16}
+
+
+def test_golden_dropout(golden):
+    man, arr = golden
+    for c in man["dropout"]:
+        x = decode(arr[c["key"] + "_x"], c["dtype"]).cuda()
+        st = R.RngState(c["seed"], c["offset"], c["theta"])
+        mask = torch.empty(x.shape, dtype=x.dtype, device="cuda")
+        y_ref_dtype = torch.float32 if c["dtype"] == "bfloat16" else x.dtype
+        y = ops.dropout_apply(x, c["p"], st, out_dtype=y_ref_dtype, mask=mask)
+        assert torch.equal(bits(mask.cpu()), bits(decode(arr[c["key"] + "_mask"], c["dtype"])))
+        assert torch.equal(bits(y.cpu()), bits(decode(arr[c["key"] + "_y"], c["y_dtype"]))), c
+        if c["dtype"] == "bfloat16":  # torch-native bf16 output == bf16_rne(reference f32)
+            yb = ops.dropout_apply(x, c["p"], st)
+            assert yb.dtype == torch.bfloat16
+            assert torch.equal(bits(yb.cpu()), bits(decode(arr[c["key"] + "_y"], "float32").to(torch.bfloat16)))
+        # sharded masks are slices of the same draw
+        mesh = S.create_mesh([("d", c["mesh"][0])])
+        spec = ShardSpec(mesh, parse_placements(c["placements"]))
+        for coord in mesh.iter_coords():
+            v = local_shape_and_offset(spec, tuple(c["shape"]), coord)
+            m = R.dropout_mask_local(v, st, c["p"], dtype=TORCH_DT[c["dtype"]])
+            ref = decode(arr[c["key"] + "_mask_" + "_".join(map(str, coord))], c["dtype"]).reshape(m.shape)
+            assert torch.equal(bits(m.cpu()), bits(ref))
+
+
+@pytest.mark.parametrize("dt", ["float32", "bfloat16", "float16", "float64"])
+@pytest.mark.parametrize("p", [0.1, 0.5, 0.999])
+def test_sharded_dropout_matches_oracle(dt, p):
+    shape = (4, 96, 80)
+    g = torch.Generator().manual_seed(5)
+    x = torch.randn(shape, generator=g).to(TORCH_DT[dt]).cuda()
+    x.view(-1)[:3] = torch.tensor([float("nan"), float("inf"), -0.0], dtype=x.dtype)
+    seed, off = 91, 12
+    import ml_dtypes
+    np_dt = ml_dtypes.bfloat16 if dt == "bfloat16" else np.dtype(dt)
+    xn = x.cpu().view(torch.int16).numpy().view(np.uint16).view(ml_dtypes.bfloat16) if dt == "bfloat16" \
+        else x.cpu().numpy()
+    idx = [np.arange(n) for n in shape]
+    m = O.keep_mask(shape, idx, seed, off, 65536, p, np_dt)
+    yref = O.dropout_apply(xn, m, p)
+    yref_t = torch.from_numpy(np.ascontiguousarray(yref))
+    for P, pl in [(1, "S(1)"), (2, "S(1)"), (8, "S(1)"), (4, "S(2)"), (3, "S(0)")]:
+        mesh = S.create_mesh([("sp", P)])
+        spec = ShardSpec(mesh, parse_placements(pl))
+        out_dtype = torch.float32 if dt == "bfloat16" else None
+        for coord in mesh.iter_coords():
+            v = local_shape_and_offset(spec, shape, coord)
+            sl = tuple(slice(o, o + n) for o, n in zip(v.local_offset, v.local_shape))
+            y = ops.dropout_apply(x[sl].contiguous(), p, R.RngState(seed, off), v, out_dtype=out_dtype)
+            assert torch.equal(bits(y.cpu()), bits(yref_t[sl].contiguous())), (dt, p, pl, coord)
+
+
+def test_cfg2_full_size_sequence_parallel():
+    """BASELINE config 2: x bf16 [8,4096,4096], p=0.1, Shard(1) over 1/2/4/8:
+    every shard equals the slice of the unsharded result; oracle spot rows."""
+    shape = (8, 4096, 4096)
+    x = torch.randn(shape, generator=torch.Generator(device="cuda").manual_seed(0), device="cuda",
+                    dtype=torch.bfloat16)
+    st = R.RngState(20240817)
+    full = ops.dropout_apply(x, 0.1, st)
+    for P in (2, 4, 8):
+        mesh = S.create_mesh([("sp", P)])
+        spec = ShardSpec(mesh, parse_placements("S(1)"))
+        for coord in [(0,), (P - 1,)]:
+            v = local_shape_and_offset(spec, shape, coord)
+            s0, n = v.local_offset[1], v.local_shape[1]
+            y = ops.dropout_apply(x[:, s0:s0 + n].contiguous(), 0.1, st, v)
+            assert torch.equal(bits(y), bits(full[:, s0:s0 + n].contiguous()))
+    import ml_dtypes
+    for b, r in [(0, 0), (3, 2047), (7, 4095)]:
+        row = x[b, r].cpu().view(torch.int16).numpy().view(np.uint16).view(ml_dtypes.bfloat16)
+        j = np.arange(4096) + (b * 4096 + r) * 4096
+        keep = O.fill_indices(j, 20240817, 0, 65536, "bernoulli", (1.0 - 0.1,), ml_dtypes.bfloat16)
+        yref = torch.from_numpy(O.dropout_apply(row, keep, 0.1)).to(torch.bfloat16)
+        assert torch.equal(bits(full[b, r].cpu()), bits(yref))
+
+
+def test_dropout_op_autograd_and_state():
+    x = torch.randn(64, 33, device="cuda", requires_grad=True)
+    st = R.RngState(3, 10, 64)
+    y = ops.dropout(x, 0.25, state=st)
+    assert st.offset == 10 + math.ceil(64 * 33 / 64)
+    g = torch.randn_like(y)
+    y.backward(g)
+    mask = R.dropout_mask_local(full_view((64, 33)), R.RngState(3, 10, 64), 0.25, dtype=torch.float32)
+    scale = np.float32(1 / (1 - 0.25))
+    assert torch.equal(bits(x.grad), bits((g * mask) * scale))
+    assert torch.equal(bits(y.detach()), bits((x.detach() * mask) * scale))
+    st2 = R.RngState(3, 10, 64)
+    assert ops.dropout(x, 0.0, state=st2) is x and st2.offset == 10

@@ -1,0 +1,144 @@
+"""CPU tests: host-side index algebra, state, and the C-ABI library surface.
+
+No GPU calls.  Placement / mesh semantics are checked against the oracle's
+restatement of the reference (oracle/rng_oracle.py), which test_oracle.py pins
+to the reference's golden fixtures.
+"""
+
+import ctypes as C
+import itertools
+import os
+import re
+
+import numpy as np
+import pytest
+from hypothesis import given, settings, strategies as st
+
+from conftest import LIB, ROOT
+from oracle import rng_oracle as O
+from paper_2509_07003_b200 import _lib
+from paper_2509_07003_b200.mesh import MeshError, create_mesh
+from paper_2509_07003_b200.placement import (
+    InterleavedShard, Partial, PlacementError, Replicate, Shard, ShardSpec, ShardView, full_view,
+    local_shape_and_offset, parse_placements)
+from paper_2509_07003_b200.rng import RngState
+
+
+def _opl(spec):
+    m = {Shard: lambda p: ("S", p.dim), Replicate: lambda p: ("R",), Partial: lambda p: ("P",),
+         InterleavedShard: lambda p: ("IS", p.dim, p.interleaved_size)}
+    return tuple(m[type(p)](p) for p in spec.placements)
+
+
+def test_header_symbols_exported():
+    hdr = open(os.path.join(ROOT, "include", "sdrng.h")).read()
+    decl = set(re.findall(r"^(?:int32_t|const char\*)\s+(sdr_\w+)\(", hdr, re.M))
+    assert decl == set(_lib.EXPORTED), decl ^ set(_lib.EXPORTED)
+    lib = C.CDLL(LIB)
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert _lib.LIB.sdr_version() == 1
+    assert _lib.LIB.sdr_strerror(_lib.E_PARAM).decode().startswith("distribution parameter")
+
+
+def test_host_philox_entry_matches_oracle():
+    out = (C.c_uint32 * 4)()
+    for s, t, b in [(0, 0, 0), (2 ** 64 - 1, 2 ** 64 - 1, 2 ** 64 - 1), (7, 3, 9), (1, 2, 2 ** 33)]:
+        assert _lib.LIB.sdr_philox_block_host(s, t, b, out) == 0
+        assert tuple(out) == O.block_scalar(s, t, b)
+
+
+@pytest.mark.parametrize("shape,pl,sizes", [
+    ((16, 24), "S(0)", (4,)), ((16, 24), "IS(0,2)", (4,)), ((7, 5, 3), "S(0),S(2)", (2, 2)),
+    ((50257, 64), "S(0),S(1)", (2, 4)), ((2, 8), "S(0)", (4,)), ((6, 40), "R,S(1)", (2, 4)),
+    ((48, 40), "IS(0,3),S(1)", (2, 4)), ((9,), "P", (3,)),
+])
+def test_windows_match_oracle(shape, pl, sizes):
+    mesh = create_mesh([(f"m{i}", s) for i, s in enumerate(sizes)])
+    spec = ShardSpec(mesh, parse_placements(pl))
+    for coord in mesh.iter_coords():
+        v = local_shape_and_offset(spec, shape, coord)
+        ref = O.window(shape, _opl(spec), sizes, coord)
+        assert v.local_shape == tuple(len(i) for i in ref)
+        for a, b in zip(v.index_lists, ref):
+            assert np.array_equal(a, b)
+        jref = O.flat_global_indices(shape, ref)
+        assert np.array_equal(v.global_flat_indices(device="cpu").numpy(), jref)
+        for i in range(0, v.num_local_elements, max(1, v.num_local_elements // 17)):
+            assert v.local_to_global_index(i) == jref[i]
+        # the C-ABI view carries the same window
+        nv = v.to_native()
+        assert [nv.local_len[d] for d in range(len(shape))] == list(v.local_shape)
+
+
+def test_shardview_from_index_lists_roundtrip():
+    v = ShardView((12, 10), [np.array([1, 2, 3, 7, 8, 9]), np.arange(10)])
+    assert v.windows[0].groups == 2 and v.windows[0].group_stride == 6
+    assert np.array_equal(v.index_lists[0], [1, 2, 3, 7, 8, 9])
+    with pytest.raises(PlacementError):
+        ShardView((12,), [np.array([0, 2, 3])])
+
+
+def test_spec_validation_and_parsing():
+    mesh = create_mesh([("a", 2), ("b", 2)])
+    with pytest.raises(PlacementError):
+        ShardSpec(mesh, parse_placements("S(0),S(0)"))
+    with pytest.raises(PlacementError):
+        ShardSpec(mesh, parse_placements("P,IS(0,2)"))
+    with pytest.raises(PlacementError):
+        ShardSpec(mesh, parse_placements("S(0)"))
+    with pytest.raises(PlacementError):
+        parse_placements("Q")
+    s = ShardSpec(mesh, parse_placements("IS(0,2),R"))
+    with pytest.raises(PlacementError):
+        local_shape_and_offset(s, (6,), (0, 0))
+    assert str(ShardSpec(mesh, parse_placements("S(1),P"))) == "[S(1),P]@mesh"
+
+
+def test_mesh_coords_fibers_flatten():
+    m = create_mesh([("dp", 2), ("tp", 4)])
+    assert m.coords_of_rank(6) == (1, 2)
+    assert m.rank_at((1, 3)) == 7
+    assert m.submesh("dp", 2).ranks == (2, 6)
+    assert m.fibers((0,)) == [[0, 4], [1, 5], [2, 6], [3, 7]]
+    f = m.flatten_dims(["dp", "tp"])
+    assert f.sizes == (8,) and f.ranks == tuple(range(8))
+    m3 = create_mesh([("a", 2), ("b", 3), ("c", 2)])
+    f3 = m3.flatten_dims(["c", "a"])
+    assert f3.dims == (("a_c", 4), ("b", 3))
+    assert f3.rank_at((1, 2)) == m3.rank_at((0, 2, 1))
+    with pytest.raises(MeshError):
+        create_mesh([("a", 2)], ranks=[0, 0])
+
+
+def test_rng_state_advance():
+    s = RngState(0, 0, 64)
+    s.advance(100)
+    assert s.offset == 2
+    s.advance(0)
+    assert s.offset == 2
+    s.advance(65, 3)
+    assert s.offset == 2 + 2 * 3
+    assert s.clone() == s and s.clone() is not s
+    with pytest.raises(ValueError):
+        RngState(0, 0, 0)
+
+
+@given(st.lists(st.integers(1, 9), min_size=1, max_size=4), st.data())
+@settings(max_examples=60, deadline=None)
+def test_windows_partition_the_tensor(shape, data):
+    ndim = len(shape)
+    P1 = data.draw(st.integers(1, 4))
+    P2 = data.draw(st.integers(1, 3))
+    d1 = data.draw(st.integers(0, ndim - 1))
+    mesh = create_mesh([("a", P1), ("b", P2)])
+    d2 = data.draw(st.integers(0, ndim - 1))
+    pl = [Shard(d1), Shard(d2) if d2 != d1 else Replicate()]
+    spec = ShardSpec(mesh, tuple(pl))
+    seen = np.zeros(int(np.prod(shape)), dtype=np.int64)
+    for coord in mesh.iter_coords():
+        if d2 == d1 and coord[1] != 0:
+            continue
+        v = local_shape_and_offset(spec, tuple(shape), coord)
+        seen[v.global_flat_indices(device="cpu").numpy()] += 1
+    assert (seen == 1).all()
