@@ -293,9 +293,10 @@ def run_ours(a):
     imad, lop3, phx = C.c_double(), C.c_double(), C.c_double()
     _lib.check(_lib.LIB.sdr_probe_int32(local, C.byref(imad), C.byref(lop3), C.byref(phx)),
                "sdr_probe_int32")
-    # Philox needs 20 IMAD.WIDE (= 40 INT32 mul ops) per block; the fma pipe is
-    # the binding pipe, so the Philox-proportion INT32 peak is 4 x IMAD.WIDE/s.
-    int_peak_tops = 4.0 * imad.value / 1e12
+    # INT32 peak in Philox proportion: a memory-free Philox4x32-10 with every
+    # counter word per-thread varying and all four words consumed (nothing to
+    # hoist), x 80 INT32 ops per block.
+    int_peak_tops = PHILOX_OPS * phx.value / 1e12
     achieved_tops = n_local / (ms_local * 1e-3) * PHILOX_OPS / 1e12
     achieved_gbs_local = local_bytes / (ms_local * 1e-3) / 1e9
 
@@ -327,7 +328,7 @@ def run_ours(a):
                 "traffic": None,
                 "int32_probe": {"imad_wide_per_s": imad.value, "lop3_per_s": lop3.value,
                                 "philox_blocks_per_s_no_hoist": phx.value,
-                                "how": "sdr_probe_int32: independent IMAD.WIDE / LOP3 chains, live"},
+                                "how": "sdr_probe_int32 live: peak = 80 x philox_blocks_per_s_no_hoist"},
                 "hbm": {"achieved": round(achieved_gbs_local, 1), "peak": hbm_peak, "unit": "GB/s",
                         "frac": round(achieved_gbs_local / hbm_peak, 4), "peak_source": hbm_src},
                 "kernel": "k_dropout_fast<BF16,BF16,-1> (one launch per step)",

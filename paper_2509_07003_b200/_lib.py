@@ -13,7 +13,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsdrng.so")
+LIB_PATH = os.environ.get("SDR_LIB_PATH") or os.path.join(_HERE, "libsdrng.so")  # env: A/B kernel experiments
 
 MAX_NDIM = 8
 

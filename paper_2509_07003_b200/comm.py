@@ -75,3 +75,182 @@ class CollectiveLedger:
             w.writerow([e.collective, e.mesh, e.dims, e.payload_bytes, e.participants,
                         float(e.bytes_per_device), float(e.modeled_time)])
         return buf.getvalue()
+
+
+# ---------------------------------------------------------------------------
+# Process groups: one per fiber of each (set of) mesh dim(s).
+# ---------------------------------------------------------------------------
+_GROUPS: dict = {}
+
+
+def my_rank() -> int:
+    import torch.distributed as dist
+    return dist.get_rank() if dist.is_initialized() else 0
+
+
+def fiber_group(mesh, dims: tuple):
+    """(process group, fiber ranks in coordinate order) of this rank's fiber
+    spanned by mesh dims `dims` (several dims = the flattened N-d fiber,
+    mesh.flatten_dims order).  Every rank creates every fiber group of `dims`
+    in the same order on first use, as torch.distributed requires."""
+    import torch.distributed as dist
+    key = (mesh, tuple(dims))
+    if key not in _GROUPS:
+        me = my_rank()
+        mine = None
+        fibers = mesh.fibers(tuple(dims))
+        for fib in fibers:
+            if fib != sorted(fib):
+                raise CommError(f"fiber {fib} is not in ascending rank order; "
+                                "build the mesh with row-major ranks")
+            g = dist.new_group(ranks=fib) if (dist.is_initialized() and len(fib) > 1) else None
+            if me in fib:
+                mine = (g, fib)
+        if mine is None:
+            raise CommError(f"rank {me} is not in mesh {mesh.name}")
+        _GROUPS[key] = mine
+    return _GROUPS[key]
+
+
+def all_gather_into(recv, send, group, ledger=None, mesh="", dims="", P=1):
+    """recv[P*len(send)] <- every fiber member's `send`, in fiber order."""
+    import torch.distributed as dist
+    if P == 1 or group is None:
+        recv.copy_(send)
+    else:
+        dist.all_gather_into_tensor(recv, send, group=group)
+    if ledger is not None:
+        ledger.record("all_gather", recv.numel() * recv.element_size(), P, mesh, dims)
+
+
+def reduce_scatter_into(out, inp, group, ledger=None, mesh="", dims="", P=1):
+    """out <- this rank's segment of the elementwise sum of every member's inp."""
+    import torch.distributed as dist
+    if P == 1 or group is None:
+        out.copy_(inp)
+    else:
+        dist.reduce_scatter_tensor(out, inp, op=dist.ReduceOp.SUM, group=group)
+    if ledger is not None:
+        ledger.record("reduce_scatter", inp.numel() * inp.element_size(), P, mesh, dims)
+
+
+def all_reduce_into(buf, group, ledger=None, mesh="", dims="", P=1):
+    import torch.distributed as dist
+    if P > 1 and group is not None:
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    if ledger is not None:
+        ledger.record("all_reduce", buf.numel() * buf.element_size(), P, mesh, dims)
+
+
+# ---------------------------------------------------------------------------
+# Bucketed and N-dim fused gradient reduction (comm.py:130-289).
+# ---------------------------------------------------------------------------
+@dataclass
+class GradBucket:
+    capacity_bytes: int
+    members: list = field(default_factory=list)
+    member_bytes: int = 0
+
+    def fits(self, nbytes: int) -> bool:
+        return not self.members or self.member_bytes + nbytes <= self.capacity_bytes
+
+
+def _pack_buckets(grads, bucket_bytes: int) -> list:
+    """Reverse creation order, greedy; an oversized gradient gets its own
+    bucket (comm.py:140-150).  Sizes use the local shard bytes (all ranks of a
+    fiber agree for Partial grads since Partial keeps full local extents)."""
+    buckets: list = []
+    for g in reversed(grads):
+        nbytes = g.local.numel() * g.local.element_size()
+        if not buckets or not buckets[-1].fits(nbytes):
+            buckets.append(GradBucket(bucket_bytes))
+        buckets[-1].members.append(g)
+        buckets[-1].member_bytes += nbytes
+    return buckets
+
+
+def _group_by_partial(grads):
+    groups: dict = {}
+    skipped = []
+    for g in grads:
+        pd = g.meta.spec.partial_mesh_dims()
+        if not pd:
+            skipped.append(g)
+            continue
+        groups.setdefault((g.meta.spec.mesh, pd, g.dtype), []).append(g)
+    return groups, skipped
+
+
+def _reduce_buckets(members, dims, bucket_bytes, ledger, mover, rounds, label):
+    from .dtensor import DTensor, _fused_all_reduce
+    from .placement import Replicate
+    from dataclasses import replace
+    mesh = members[0].meta.spec.mesh
+    out = {}
+    for b in _pack_buckets(members, bucket_bytes):
+        slots = [[m.meta.spec, m.local] for m in b.members]
+        _fused_all_reduce(mesh, dims, list(zip(b.members, slots)), ledger, mover)
+        rounds.append(("all_reduce", label, tuple(mesh.dim_names[d] for d in dims)))
+        for m, (spec, loc) in zip(b.members, slots):
+            for d in dims:
+                spec = spec.with_placement(d, Replicate())
+            out[id(m)] = DTensor(replace(m.meta, spec=spec), loc, m.coord)
+    return out
+
+
+def bucketed_grad_reduce(grads, bucket_bytes: int = DEFAULT_BUCKET_BYTES, ledger=None, *,
+                         mover=None):
+    """Per Partial mesh dim, one all-reduce per bucket (comm.py:208-233)."""
+    from .movers import DEFAULT_MOVER
+    mover = DEFAULT_MOVER if mover is None else mover
+    groups, skipped = _group_by_partial(grads)
+    result = {id(g): g for g in grads}
+    rounds: list = []
+    for (mesh, pdims, _), members in groups.items():
+        current = members
+        for d in pdims:
+            upd = _reduce_buckets(current, (d,), bucket_bytes, ledger, mover, rounds, mesh.name)
+            current = [upd[id(m)] for m in current]
+        for before, after in zip(members, current):
+            result[id(before)] = after
+    return [result[id(g)] for g in grads], {"skipped": skipped, "rounds": rounds}
+
+
+def fused_nd_grad_reduce(grads, bucket_bytes: int = DEFAULT_BUCKET_BYTES, ledger=None, *,
+                         mover=None):
+    """All Partial dims of a group flattened into one fiber: ONE all-reduce
+    per bucket instead of one per dim (comm.py:236-289)."""
+    from .movers import DEFAULT_MOVER
+    mover = DEFAULT_MOVER if mover is None else mover
+    groups, skipped = _group_by_partial(grads)
+    result = {id(g): g for g in grads}
+    rounds: list = []
+    for (mesh, pdims, _), members in groups.items():
+        flat = mesh.flatten_dims([mesh.dim_names[d] for d in pdims])
+        upd = _reduce_buckets(members, tuple(pdims), bucket_bytes, ledger, mover, rounds, flat.name)
+        for m in members:
+            result[id(m)] = upd[id(m)]
+    return [result[id(g)] for g in grads], {"skipped": skipped, "rounds": rounds}
+
+
+@dataclass(frozen=True)
+class CostParams:
+    payload_bytes: int
+    transfer_time_per_byte: Fraction
+    device_counts: tuple
+
+    def __post_init__(self):
+        if self.payload_bytes <= 0 or self.transfer_time_per_byte <= 0:
+            raise CommError("S and B must be positive")
+        if not self.device_counts or any(p < 1 for p in self.device_counts):
+            raise CommError("device counts must be >= 1")
+
+
+def cost_model_eval(params: CostParams):
+    """(T_vanilla, T_fused, ratio) of the ring model (comm.py:307-318)."""
+    import math as _m
+    two_sb = 2 * params.payload_bytes * Fraction(params.transfer_time_per_byte)
+    tv = two_sb * sum(Fraction(p - 1, p) for p in params.device_counts)
+    n = _m.prod(params.device_counts)
+    tf = two_sb * Fraction(n - 1, n)
+    return tv, tf, (tv / tf if tf else Fraction(1))

@@ -15,7 +15,7 @@ __global__ void __launch_bounds__(256) k_probe_imad(uint32_t* sink, int iters) {
   for (int i = 0; i < ILP; ++i) p[i] = (static_cast<uint64_t>(threadIdx.x + i) << 32) | blockIdx.x;
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
-    for (int i = 0; i < ILP; ++i) p[i] = mul_wide(hi32(p[i]), kM0) + p[i];  // one IMAD.WIDE.U32
+    for (int i = 0; i < ILP; ++i) p[i] = mul_wide(hi32(p[i]) ^ lo32(p[i]), kM0);  // IMAD.WIDE + LOP3
   }
   uint64_t s = 0;
 #pragma unroll

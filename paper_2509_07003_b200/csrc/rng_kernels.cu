@@ -42,27 +42,28 @@ inline Gen make_gen(const sdr_rng& r) {
   return g;
 }
 
-// Rounds [R0, 10) for kV independent counters.
-template <int R0>
-__device__ __forceinline__ void rounds_from(const RoundKeys& K, uint32_t (&x0)[kV],
-                                            uint32_t (&x1)[kV], uint32_t (&x2)[kV],
-                                            uint32_t (&x3)[kV]) {
+// Rounds [R0, 10) for NE independent counters.
+template <int R0, int NE>
+__device__ __forceinline__ void rounds_from(const RoundKeys& K, uint32_t (&x0)[NE],
+                                            uint32_t (&x1)[NE], uint32_t (&x2)[NE],
+                                            uint32_t (&x3)[NE]) {
 #pragma unroll
   for (int r = R0; r < 10; ++r) {
 #pragma unroll
-    for (int e = 0; e < kV; ++e) philox_round(x0[e], x1[e], x2[e], x3[e], K.k0[r], K.k1[r]);
+    for (int e = 0; e < NE; ++e) philox_round(x0[e], x1[e], x2[e], x3[e], K.k0[r], K.k1[r]);
   }
 }
 
-// Words 0/1 of the blocks of global indices j0 .. j0+kV-1.
-__device__ __forceinline__ void chunk_words(const Gen& g, uint64_t j0, uint32_t (&w0)[kV],
-                                            uint32_t (&w1)[kV]) {
+// Words 0/1 of the blocks of global indices j0 .. j0+NE-1.
+template <int NE>
+__device__ __forceinline__ void chunk_words(const Gen& g, uint64_t j0, uint32_t (&w0)[NE],
+                                            uint32_t (&w1)[NE]) {
   uint64_t b, t;
   g.div_theta.divmod(j0, b, t);
   const uint64_t beta = b + g.offset;
-  uint32_t x0[kV], x1[kV], x2[kV], x3[kV];
+  uint32_t x0[NE], x1[NE], x2[NE], x3[NE];
   const RoundKeys& K = g.keys;
-  if (g.theta >= kV && t <= g.theta - kV && lo32(t) <= 0xFFFFFFFFu - (kV - 1)) {
+  if (g.theta >= NE && t <= g.theta - NE && lo32(t) <= 0xFFFFFFFFu - (NE - 1)) {
     // Shared beta: hoist the chunk-uniform products of rounds 1 and 2.
     const uint32_t blo = lo32(beta), bhi = hi32(beta), tlo = lo32(t), thi = hi32(t);
     const uint64_t pa = mul_wide(blo, kM0);
@@ -72,7 +73,7 @@ __device__ __forceinline__ void chunk_words(const Gen& g, uint64_t j0, uint32_t 
     const uint64_t pq = mul_wide(y2, kM1);
     const uint32_t z1 = lo32(pq), hq = hi32(pq);
 #pragma unroll
-    for (int e = 0; e < kV; ++e) {
+    for (int e = 0; e < NE; ++e) {
       const uint64_t pb = pb0 + static_cast<uint64_t>(e) * kM1;  // == M1*(tlo+e)
       const uint32_t y0 = hi32(pb) ^ bhi ^ K.k0[0];
       const uint32_t y1 = lo32(pb);
@@ -82,10 +83,10 @@ __device__ __forceinline__ void chunk_words(const Gen& g, uint64_t j0, uint32_t 
       x2[e] = hi32(pa2) ^ y3 ^ K.k1[1];
       x3[e] = lo32(pa2);
     }
-    rounds_from<2>(K, x0, x1, x2, x3);
+    rounds_from<2, NE>(K, x0, x1, x2, x3);
   } else {
 #pragma unroll
-    for (int e = 0; e < kV; ++e) {
+    for (int e = 0; e < NE; ++e) {
       uint64_t be, te;
       g.div_theta.divmod(j0 + e, be, te);
       be += g.offset;
@@ -94,10 +95,10 @@ __device__ __forceinline__ void chunk_words(const Gen& g, uint64_t j0, uint32_t 
       x2[e] = lo32(te);
       x3[e] = hi32(te);
     }
-    rounds_from<0>(K, x0, x1, x2, x3);
+    rounds_from<0, NE>(K, x0, x1, x2, x3);
   }
 #pragma unroll
-  for (int e = 0; e < kV; ++e) {
+  for (int e = 0; e < NE; ++e) {
     w0[e] = x0[e];
     w1[e] = x1[e];
   }
@@ -255,15 +256,19 @@ __device__ __forceinline__ typename St<DT>::T dist_value(const DistP& P, uint32_
 // ---------------------------------------------------------------------------
 // Vector stores of kV elements.
 // ---------------------------------------------------------------------------
-template <typename T>
-__device__ __forceinline__ void store_chunk(T* p, const T (&v)[kV]) {
-  constexpr int bytes = sizeof(T) * kV;
-  if constexpr (bytes == 8) {
+template <typename T, int N>
+__device__ __forceinline__ void store_chunk(T* p, const T (&v)[N]) {
+  constexpr int bytes = sizeof(T) * N;
+  if constexpr (bytes == 4) {
+    uint32_t q;
+    memcpy(&q, v, 4);
+    __stcs(reinterpret_cast<unsigned int*>(p), q);
+  } else if constexpr (bytes == 8) {
     uint2 q;
     memcpy(&q, v, 8);
     __stcs(reinterpret_cast<uint2*>(p), q);
   } else {
-    static_assert(bytes % 16 == 0, "chunk must be a multiple of 16 bytes");
+    static_assert(bytes % 16 == 0, "chunk must be 4, 8 or a multiple of 16 bytes");
     uint4 q[bytes / 16];
     memcpy(q, v, bytes);
 #pragma unroll
@@ -271,13 +276,17 @@ __device__ __forceinline__ void store_chunk(T* p, const T (&v)[kV]) {
   }
 }
 
-template <typename T>
-__device__ __forceinline__ void load_chunk(const T* p, T (&v)[kV]) {
-  constexpr int bytes = sizeof(T) * kV;
-  if constexpr (bytes == 8) {
-    uint2 q = __ldcs(reinterpret_cast<const uint2*>(p));
+template <typename T, int N>
+__device__ __forceinline__ void load_chunk(const T* p, T (&v)[N]) {
+  constexpr int bytes = sizeof(T) * N;
+  if constexpr (bytes == 4) {
+    const uint32_t q = __ldcs(reinterpret_cast<const unsigned int*>(p));
+    memcpy(v, &q, 4);
+  } else if constexpr (bytes == 8) {
+    const uint2 q = __ldcs(reinterpret_cast<const uint2*>(p));
     memcpy(v, &q, 8);
   } else {
+    static_assert(bytes % 16 == 0, "chunk must be 4, 8 or a multiple of 16 bytes");
     uint4 q[bytes / 16];
 #pragma unroll
     for (int i = 0; i < bytes / 16; ++i) q[i] = __ldcs(reinterpret_cast<const uint4*>(p) + i);
@@ -404,8 +413,7 @@ struct DropArgs {
   const void* x;
   void* y;
   void* mask;
-  uint64_t keep_thr;
-  uint32_t keep_all;
+  uint64_t keep_le;   // keep <=> (w1:w0) <= keep_le, i.e. k53 < ceil((1-p)*2^53)
   float scale32;
   double scale64;
   uint16_t scale16;  // f16 bits of the scale
@@ -416,31 +424,76 @@ struct DropArgs {
 
 template <int XT> struct DropT { using T = typename St<XT>::T; };
 
-// y element for input dtype XT and output dtype YT.
+// y element for input dtype XT and output dtype YT; sets `nan` when the
+// result is a NaN (then drop_nan_fix() supplies the x86/NumPy bit pattern).
 template <int XT, int YT>
 __device__ __forceinline__ typename St<YT>::T drop_apply(const DropArgs& A, typename St<XT>::T x,
-                                                         bool keep) {
+                                                         bool keep, bool& nan) {
   if constexpr (XT == SDR_F32) {
-    return __fmul_rn(__fmul_rn(x, keep ? 1.0f : 0.0f), A.scale32);
+    const float y = __fmul_rn(__fmul_rn(x, keep ? 1.0f : 0.0f), A.scale32);
+    nan = y != y;
+    return y;
   } else if constexpr (XT == SDR_F64) {
-    return __dmul_rn(__dmul_rn(x, keep ? 1.0 : 0.0), A.scale64);
+    const double y = __dmul_rn(__dmul_rn(x, keep ? 1.0 : 0.0), A.scale64);
+    nan = y != y;
+    return y;
   } else if constexpr (XT == SDR_BF16) {
     const float xf = __uint_as_float(static_cast<uint32_t>(x) << 16);
     const float y = __fmul_rn(__fmul_rn(xf, keep ? 1.0f : 0.0f), A.scale32);
+    nan = y != y;
     if constexpr (YT == SDR_F32) return y;
     else return bf16_bits(y);
   } else {  // SDR_F16: x*m exact in f16, then RNE(x16 * scale16)
     const __half xh = __ushort_as_half(x);
     const __half xm = __hmul(xh, keep ? __ushort_as_half(0x3C00) : __ushort_as_half(0));
-    return __half_as_ushort(__hmul(xm, __ushort_as_half(A.scale16)));
+    const uint16_t y = __half_as_ushort(__hmul(xm, __ushort_as_half(A.scale16)));
+    nan = (y & 0x7FFFu) > 0x7C00u;
+    return y;
   }
 }
 
+// NaN results as x86 SSE + NumPy / ml_dtypes produce them: a NaN input is
+// propagated quieted with its payload, inf*0 gives the negative default NaN;
+// float32->bfloat16 maps NaN to 0x7FC0 / 0xFFC0 (ml_dtypes), float->half keeps
+// sign and the top payload bits (numpy npy_floatbits_to_halfbits).
+template <int XT, int YT>
+__device__ __noinline__ typename St<YT>::T drop_nan_fix(typename St<XT>::T x) {
+  if constexpr (XT == SDR_F32) {
+    const uint32_t b = __float_as_uint(x);
+    return __uint_as_float((b & 0x7FFFFFFFu) > 0x7F800000u ? (b | 0x00400000u) : 0xFFC00000u);
+  } else if constexpr (XT == SDR_F64) {
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(x));
+    const bool isn = (b & 0x7FFFFFFFFFFFFFFFull) > 0x7FF0000000000000ull;
+    return __longlong_as_double(static_cast<long long>(isn ? (b | 0x0008000000000000ull)
+                                                           : 0xFFF8000000000000ull));
+  } else if constexpr (XT == SDR_BF16) {
+    const uint32_t b = static_cast<uint32_t>(x) << 16;
+    const uint32_t f = (b & 0x7FFFFFFFu) > 0x7F800000u ? (b | 0x00400000u) : 0xFFC00000u;
+    if constexpr (YT == SDR_F32) return __uint_as_float(f);
+    else return static_cast<uint16_t>((f & 0x80000000u) ? 0xFFC0u : 0x7FC0u);
+  } else {
+    const uint16_t b = x;
+    return static_cast<uint16_t>((b & 0x7FFFu) > 0x7C00u ? (b | 0x0200u) : 0xFE00u);
+  }
+}
+
+#ifndef SDR_DROP_MINB
+#define SDR_DROP_MINB 4
+#endif
+#ifndef SDR_DROP_SPLIT
+#define SDR_DROP_SPLIT 1   // Philox for the chunk in SPLIT passes
+#endif
+#ifndef SDR_DROP_CH
+#define SDR_DROP_CH 8      // elements per thread-chunk of the dropout kernel
+#endif
+constexpr int kDropCh = SDR_DROP_CH;
+
 __device__ __forceinline__ uint64_t drop_chunk_base(const DropArgs& A, uint64_t q) {
+  const CanonView& cv = A.ix.cv;
+  if (cv.nd == 0) return static_cast<uint64_t>(cv.base) + q * kDropCh;  // one contiguous run
   uint64_t row, cq;
   A.div_cpr.divmod(q, row, cq);
-  uint64_t j = static_cast<uint64_t>(A.ix.cv.base) + cq * kV;
-  const CanonView& cv = A.ix.cv;
+  uint64_t j = static_cast<uint64_t>(cv.base) + cq * kDropCh;
   for (int k = cv.nd - 1; k >= 0; --k) {
     uint64_t qq, r;
     A.ix.div_o[k].divmod(row, qq, r);
@@ -450,36 +503,64 @@ __device__ __forceinline__ uint64_t drop_chunk_base(const DropArgs& A, uint64_t 
   return j;
 }
 
+
+// bf16 lanes of a 32-bit word as float32 (PRMT / LOP3 on the ALU pipe).
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(__byte_perm(w, 0u, 0x1044)); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
 template <int XT, int YT, int MT>
-__global__ void __launch_bounds__(256) k_dropout_fast(const __grid_constant__ DropArgs A) {
+__global__ void __launch_bounds__(256, SDR_DROP_MINB) k_dropout_fast(const __grid_constant__ DropArgs A) {
   using XTy = typename St<XT>::T;
   using YTy = typename St<YT>::T;
   const XTy* x = static_cast<const XTy*>(A.x);
   YTy* y = static_cast<YTy*>(A.y);
+  constexpr int CH = kDropCh;
+  constexpr int NE = CH / SDR_DROP_SPLIT;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < A.nchunks;
        q += stride) {
-    XTy xv[kV];
-    load_chunk(x + q * kV, xv);
+    XTy xv[CH];
+    load_chunk(x + q * CH, xv);
     const uint64_t j0 = drop_chunk_base(A, q);
-    uint32_t w0[kV], w1[kV];
-    chunk_words(A.g, j0, w0, w1);
-    YTy yv[kV];
-    bool keep[kV];
+    YTy yv[CH];
+    bool keep[CH], anynan = false, nan[CH];
 #pragma unroll
-    for (int e = 0; e < kV; ++e) {
-      const uint64_t u64 = (static_cast<uint64_t>(w1[e]) << 32) | w0[e];
-      keep[e] = A.keep_all || u64 < A.keep_thr;
-      yv[e] = drop_apply<XT, YT>(A, xv[e], keep[e]);
+    for (int h = 0; h < SDR_DROP_SPLIT; ++h) {
+      uint32_t w0[NE], w1[NE];
+      chunk_words<NE>(A.g, j0 + h * NE, w0, w1);
+#pragma unroll
+      for (int i = 0; i < NE; ++i) {
+        const int e = h * NE + i;
+        const uint64_t u64 = (static_cast<uint64_t>(w1[i]) << 32) | w0[i];
+        keep[e] = u64 <= A.keep_le;
+        if constexpr (XT == SDR_BF16) {
+          // unpack from the raw 16 B vector: even lane = low half of a word
+          uint32_t wd;
+          memcpy(&wd, &xv[e & ~1], 4);
+          const float xf = (e & 1) ? bf16_hi(wd) : bf16_lo(wd);
+          const float r = __fmul_rn(__fmul_rn(xf, keep[e] ? 1.0f : 0.0f), A.scale32);
+          nan[e] = r != r;
+          if constexpr (YT == SDR_F32) yv[e] = r;
+          else yv[e] = bf16_bits(r);
+        } else {
+          yv[e] = drop_apply<XT, YT>(A, xv[e], keep[e], nan[e]);
+        }
+        anynan |= nan[e];
+      }
     }
-    store_chunk(y + q * kV, yv);
+    if (anynan) {
+#pragma unroll
+      for (int e = 0; e < CH; ++e)
+        if (nan[e]) yv[e] = drop_nan_fix<XT, YT>(xv[e]);
+    }
+    store_chunk(y + q * CH, yv);
     if constexpr (MT >= 0) {
       using MTy = typename St<MT>::T;
       if (A.mask != nullptr) {
-        MTy mv[kV];
+        MTy mv[CH];
 #pragma unroll
-        for (int e = 0; e < kV; ++e) mv[e] = one_or_zero<MT>(keep[e]);
-        store_chunk(static_cast<MTy*>(A.mask) + q * kV, mv);
+        for (int e = 0; e < CH; ++e) mv[e] = one_or_zero<MT>(keep[e]);
+        store_chunk(static_cast<MTy*>(A.mask) + q * CH, mv);
       }
     }
   }
@@ -498,8 +579,10 @@ __global__ void __launch_bounds__(256) k_dropout_generic(const __grid_constant__
     uint32_t w0, w1;
     elem_words(A.g, A.ix.global_of(i), w0, w1);
     const uint64_t u64 = (static_cast<uint64_t>(w1) << 32) | w0;
-    const bool keep = A.keep_all || u64 < A.keep_thr;
-    y[i] = drop_apply<XT, YT>(A, x[i], keep);
+    const bool keep = u64 <= A.keep_le;
+    bool nan;
+    const YTy v = drop_apply<XT, YT>(A, x[i], keep, nan);
+    y[i] = nan ? drop_nan_fix<XT, YT>(x[i]) : v;
     if constexpr (MT >= 0) {
       using MTy = typename St<MT>::T;
       if (A.mask != nullptr) static_cast<MTy*>(A.mask)[i] = one_or_zero<MT>(keep);
@@ -637,16 +720,29 @@ int canonicalize(const sdr_view& v, CanonView& cv) {
   return SDR_OK;
 }
 
-static int launch_grid(uint64_t work, int threads) {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+static int device_sms() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+// Persistent grid: one wave of resident CTAs (SMs x occupancy), or fewer
+// blocks when the work is small.  Grid-stride loops cover the rest.
+template <typename K>
+static int grid_for(K kernel, uint64_t work, int threads) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const uint64_t cap = static_cast<uint64_t>(device_sms()) * per_sm;
   const uint64_t blocks = (work + threads - 1) / threads;
-  const uint64_t cap = static_cast<uint64_t>(sms) * 8;  // persistent: <= 8 CTAs of 256 per SM
+  return static_cast<int>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+}
+
+static int launch_grid(uint64_t work, int threads) {
+  const uint64_t blocks = (work + threads - 1) / threads;
+  const uint64_t cap = static_cast<uint64_t>(device_sms()) * 8;
   return static_cast<int>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
 }
 
@@ -719,10 +815,10 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
 }
 
 static void setup_chunks(const CanonView& cv, bool fast, uint64_t& nchunks, uint64_t& cpr,
-                         FastDiv64& div_cpr) {
+                         FastDiv64& div_cpr, int ch = kV) {
   if (fast) {
-    cpr = static_cast<uint64_t>(cv.inner) / kV;
-    nchunks = static_cast<uint64_t>(cv.numel) / kV;
+    cpr = static_cast<uint64_t>(cv.inner) / ch;
+    nchunks = static_cast<uint64_t>(cv.numel) / ch;
   } else {
     cpr = 1;
     nchunks = 0;
@@ -733,9 +829,9 @@ static void setup_chunks(const CanonView& cv, bool fast, uint64_t& nchunks, uint
 template <int DIST, int DT>
 static void launch_fill(const FillArgs& A, bool fast, cudaStream_t s) {
   if (fast) {
-    k_fill_fast<DIST, DT><<<launch_grid(A.nchunks, 256), 256, 0, s>>>(A);
+    k_fill_fast<DIST, DT><<<grid_for(k_fill_fast<DIST, DT>, A.nchunks, 256), 256, 0, s>>>(A);
   } else {
-    k_fill_generic<DIST, DT><<<launch_grid(A.ix.cv.numel, 256), 256, 0, s>>>(A);
+    k_fill_generic<DIST, DT><<<grid_for(k_fill_generic<DIST, DT>, A.ix.cv.numel, 256), 256, 0, s>>>(A);
   }
 }
 
@@ -808,8 +904,10 @@ int fill(void* out, int dt, const sdr_dist& dist, const sdr_rng& rng, const sdr_
 
 template <int XT, int YT, int MT>
 static int launch_drop(const DropArgs& A, bool fast, cudaStream_t s) {
-  if (fast) k_dropout_fast<XT, YT, MT><<<launch_grid(A.nchunks, 256), 256, 0, s>>>(A);
-  else k_dropout_generic<XT, YT, MT><<<launch_grid(A.ix.cv.numel, 256), 256, 0, s>>>(A);
+  if (fast)
+    k_dropout_fast<XT, YT, MT><<<grid_for(k_dropout_fast<XT, YT, MT>, A.nchunks, 256), 256, 0, s>>>(A);
+  else
+    k_dropout_generic<XT, YT, MT><<<grid_for(k_dropout_generic<XT, YT, MT>, A.ix.cv.numel, 256), 256, 0, s>>>(A);
   return check_launch();
 }
 
@@ -839,16 +937,15 @@ int dropout(const void* x, int xt, void* y, int yt, void* mask, int mt, double p
   A.mask = mask;
   // keep-prob 1-p in float64 (rng.py:242), threshold ceil((1-p)*2^53).
   const double pk = 1.0 - p;
-  const uint64_t T = static_cast<uint64_t>(ceil(pk * 9007199254740992.0));
-  A.keep_all = (T >= (uint64_t{1} << 53)) ? 1u : 0u;
-  A.keep_thr = A.keep_all ? 0 : (T << 11);
+  const uint64_t T = static_cast<uint64_t>(ceil(pk * 9007199254740992.0));  // >= 1 as p < 1
+  A.keep_le = (T >= (uint64_t{1} << 53)) ? ~uint64_t{0} : (T << 11) - 1;
   const double scale = 1.0 / (1.0 - p);
   A.scale64 = scale;
   A.scale32 = static_cast<float>(scale);
   A.scale16 = __half_as_ushort(__double2half(scale));
-  bool fast = cv.istride == 1 && cv.inner % kV == 0 && aligned16(x) && aligned16(y) &&
+  bool fast = cv.istride == 1 && cv.inner % kDropCh == 0 && aligned16(x) && aligned16(y) &&
               (mask == nullptr || (reinterpret_cast<uintptr_t>(mask) & 7u) == 0);
-  setup_chunks(cv, fast, A.nchunks, A.chunks_per_row, A.div_cpr);
+  setup_chunks(cv, fast, A.nchunks, A.chunks_per_row, A.div_cpr, kDropCh);
   if (xt == SDR_F32 && yt == SDR_F32) return dispatch_drop_mask<SDR_F32, SDR_F32>(mt, A, fast, s);
   if (xt == SDR_F64 && yt == SDR_F64) return dispatch_drop_mask<SDR_F64, SDR_F64>(mt, A, fast, s);
   if (xt == SDR_BF16 && yt == SDR_BF16) return dispatch_drop_mask<SDR_BF16, SDR_BF16>(mt, A, fast, s);

@@ -36,10 +36,12 @@ def test_golden_dropout(golden):
         y = ops.dropout_apply(x, c["p"], st, out_dtype=y_ref_dtype, mask=mask)
         assert torch.equal(bits(mask.cpu()), bits(decode(arr[c["key"] + "_mask"], c["dtype"])))
         assert torch.equal(bits(y.cpu()), bits(decode(arr[c["key"] + "_y"], c["y_dtype"]))), c
-        if c["dtype"] == "bfloat16":  # torch-native bf16 output == bf16_rne(reference f32)
+        if c["dtype"] == "bfloat16":  # torch-native bf16 output == ml_dtypes bf16 of the reference f32
+            import ml_dtypes
             yb = ops.dropout_apply(x, c["p"], st)
             assert yb.dtype == torch.bfloat16
-            assert torch.equal(bits(yb.cpu()), bits(decode(arr[c["key"] + "_y"], "float32").to(torch.bfloat16)))
+            ref16 = np.asarray(arr[c["key"] + "_y"]).astype(ml_dtypes.bfloat16)
+            assert torch.equal(bits(yb.cpu()), bits(decode(ref16.view(np.uint16), "bfloat16")))
         # sharded masks are slices of the same draw
         mesh = S.create_mesh([("d", c["mesh"][0])])
         spec = ShardSpec(mesh, parse_placements(c["placements"]))
@@ -56,7 +58,10 @@ def test_sharded_dropout_matches_oracle(dt, p):
     shape = (4, 96, 80)
     g = torch.Generator().manual_seed(5)
     x = torch.randn(shape, generator=g).to(TORCH_DT[dt]).cuda()
-    x.view(-1)[:3] = torch.tensor([float("nan"), float("inf"), -0.0], dtype=x.dtype)
+    specials = torch.tensor([float("nan"), float("inf"), -0.0, float("-inf"), -float("nan"), float("inf")],
+                            dtype=x.dtype)
+    x.view(-1)[:6] = specials
+    x.view(-1)[100:106] = specials
     seed, off = 91, 12
     import ml_dtypes
     np_dt = ml_dtypes.bfloat16 if dt == "bfloat16" else np.dtype(dt)
@@ -75,6 +80,10 @@ def test_sharded_dropout_matches_oracle(dt, p):
             sl = tuple(slice(o, o + n) for o, n in zip(v.local_offset, v.local_shape))
             y = ops.dropout_apply(x[sl].contiguous(), p, R.RngState(seed, off), v, out_dtype=out_dtype)
             assert torch.equal(bits(y.cpu()), bits(yref_t[sl].contiguous())), (dt, p, pl, coord)
+            if dt == "bfloat16":  # bf16 output = ml_dtypes' cast of the reference float32
+                yb = ops.dropout_apply(x[sl].contiguous(), p, R.RngState(seed, off), v)
+                r16 = np.ascontiguousarray(yref[sl]).astype(ml_dtypes.bfloat16).view(np.uint16)
+                assert torch.equal(bits(yb.cpu()), bits(decode(r16, "bfloat16")))
 
 
 def test_cfg2_full_size_sequence_parallel():

@@ -204,8 +204,11 @@ def test_value_contracts_and_errors():
         R.Bernoulli(1.5)
     with pytest.raises(ValueError):
         R.dropout_mask_local(full_view((4,)), R.RngState(), 1.0)
+    # Uniform01 returns float64 for every non-float32 dtype (rng.py:124-127) ...
+    assert R.generate_global((4,), R.RngState(), R.Uniform01(), dtype=np.int64).dtype == torch.float64
+    # ... while Normal has no integer output kernel
     with pytest.raises(TypeError):
-        R.generate_global((4,), R.RngState(), R.Uniform01(), dtype=np.int64)
+        R.generate_global((4,), R.RngState(), R.Normal(0, 1), dtype=np.int64)
 
     class Custom(R.Distribution):
         pass
