@@ -104,6 +104,43 @@ __device__ __forceinline__ void chunk_words(const Gen& g, uint64_t j0, uint32_t 
   }
 }
 
+// Fast path when THETA is a power of two >= NE and every chunk starts at a
+// multiple of NE (host-checked): the chunk never straddles a THETA boundary,
+// so beta is chunk-uniform and no 64-bit division is needed.
+template <int NE>
+__device__ __forceinline__ void chunk_words_aligned(const Gen& g, uint64_t j0, uint32_t (&w0)[NE],
+                                                    uint32_t (&w1)[NE]) {
+  const uint32_t sh = g.div_theta.s;
+  const uint64_t beta = (j0 >> sh) + g.offset;
+  const uint64_t t = j0 & (g.theta - 1);
+  const RoundKeys& K = g.keys;
+  uint32_t x0[NE], x1[NE], x2[NE], x3[NE];
+  const uint32_t blo = lo32(beta), bhi = hi32(beta), tlo = lo32(t), thi = hi32(t);
+  const uint64_t pa = mul_wide(blo, kM0);
+  const uint32_t y2 = hi32(pa) ^ thi ^ K.k1[0];
+  const uint32_t y3 = lo32(pa);
+  const uint64_t pb0 = mul_wide(tlo, kM1);
+  const uint64_t pq = mul_wide(y2, kM1);
+  const uint32_t z1 = lo32(pq), hq = hi32(pq);
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const uint64_t pb = pb0 + static_cast<uint64_t>(e) * kM1;
+    const uint32_t y0 = hi32(pb) ^ bhi ^ K.k0[0];
+    const uint32_t y1 = lo32(pb);
+    const uint64_t pa2 = mul_wide(y0, kM0);
+    x0[e] = hq ^ y1 ^ K.k0[1];
+    x1[e] = z1;
+    x2[e] = hi32(pa2) ^ y3 ^ K.k1[1];
+    x3[e] = lo32(pa2);
+  }
+  rounds_from<2, NE>(K, x0, x1, x2, x3);
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    w0[e] = x0[e];
+    w1[e] = x1[e];
+  }
+}
+
 // Words of one element at global index j (generic path).
 __device__ __forceinline__ void elem_words(const Gen& g, uint64_t j, uint32_t& w0, uint32_t& w1) {
   uint64_t b, t;
@@ -414,6 +451,7 @@ struct DropArgs {
   void* y;
   void* mask;
   uint64_t keep_le;   // keep <=> (w1:w0) <= keep_le, i.e. k53 < ceil((1-p)*2^53)
+  uint32_t aligned;   // THETA pow2 >= chunk and every chunk start chunk-aligned
   float scale32;
   double scale64;
   uint16_t scale16;  // f16 bits of the scale
@@ -508,7 +546,7 @@ __device__ __forceinline__ uint64_t drop_chunk_base(const DropArgs& A, uint64_t 
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(__byte_perm(w, 0u, 0x1044)); }
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
-template <int XT, int YT, int MT>
+template <int XT, int YT, int MT, bool ALIGNED>
 __global__ void __launch_bounds__(256, SDR_DROP_MINB) k_dropout_fast(const __grid_constant__ DropArgs A) {
   using XTy = typename St<XT>::T;
   using YTy = typename St<YT>::T;
@@ -527,7 +565,8 @@ __global__ void __launch_bounds__(256, SDR_DROP_MINB) k_dropout_fast(const __gri
 #pragma unroll
     for (int h = 0; h < SDR_DROP_SPLIT; ++h) {
       uint32_t w0[NE], w1[NE];
-      chunk_words<NE>(A.g, j0 + h * NE, w0, w1);
+      if constexpr (ALIGNED) chunk_words_aligned<NE>(A.g, j0 + h * NE, w0, w1);
+      else chunk_words<NE>(A.g, j0 + h * NE, w0, w1);
 #pragma unroll
       for (int i = 0; i < NE; ++i) {
         const int e = h * NE + i;
@@ -814,6 +853,16 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
   return SDR_OK;
 }
 
+// Every chunk start j0 = base + sum(digit*ostride) + c*ch is a multiple of ch
+// and THETA is a power of two >= ch: no chunk straddles a THETA boundary.
+static bool chunks_aligned(const CanonView& cv, uint64_t theta, int ch) {
+  if ((theta & (theta - 1)) != 0 || theta < static_cast<uint64_t>(ch)) return false;
+  if (cv.base % ch != 0) return false;
+  for (int k = 0; k < cv.nd; ++k)
+    if (cv.ostride[k] % ch != 0) return false;
+  return true;
+}
+
 static void setup_chunks(const CanonView& cv, bool fast, uint64_t& nchunks, uint64_t& cpr,
                          FastDiv64& div_cpr, int ch = kV) {
   if (fast) {
@@ -904,8 +953,10 @@ int fill(void* out, int dt, const sdr_dist& dist, const sdr_rng& rng, const sdr_
 
 template <int XT, int YT, int MT>
 static int launch_drop(const DropArgs& A, bool fast, cudaStream_t s) {
-  if (fast)
-    k_dropout_fast<XT, YT, MT><<<grid_for(k_dropout_fast<XT, YT, MT>, A.nchunks, 256), 256, 0, s>>>(A);
+  if (fast && A.aligned)
+    k_dropout_fast<XT, YT, MT, true><<<grid_for(k_dropout_fast<XT, YT, MT, true>, A.nchunks, 256), 256, 0, s>>>(A);
+  else if (fast)
+    k_dropout_fast<XT, YT, MT, false><<<grid_for(k_dropout_fast<XT, YT, MT, false>, A.nchunks, 256), 256, 0, s>>>(A);
   else
     k_dropout_generic<XT, YT, MT><<<grid_for(k_dropout_generic<XT, YT, MT>, A.ix.cv.numel, 256), 256, 0, s>>>(A);
   return check_launch();
@@ -946,6 +997,7 @@ int dropout(const void* x, int xt, void* y, int yt, void* mask, int mt, double p
   bool fast = cv.istride == 1 && cv.inner % kDropCh == 0 && aligned16(x) && aligned16(y) &&
               (mask == nullptr || (reinterpret_cast<uintptr_t>(mask) & 7u) == 0);
   setup_chunks(cv, fast, A.nchunks, A.chunks_per_row, A.div_cpr, kDropCh);
+  A.aligned = fast && chunks_aligned(cv, rng.theta, kDropCh);
   if (xt == SDR_F32 && yt == SDR_F32) return dispatch_drop_mask<SDR_F32, SDR_F32>(mt, A, fast, s);
   if (xt == SDR_F64 && yt == SDR_F64) return dispatch_drop_mask<SDR_F64, SDR_F64>(mt, A, fast, s);
   if (xt == SDR_BF16 && yt == SDR_BF16) return dispatch_drop_mask<SDR_BF16, SDR_BF16>(mt, A, fast, s);

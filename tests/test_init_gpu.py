@@ -1,0 +1,119 @@
+"""GPU parity of the one-launch deferred init (K3) and of the pack kernels.
+
+materialize() must equal the reference's sequential walk (model.py:121-132:
+generate_distributed / generate_global per parameter in definition order) bit
+for bit, and leave the RngState at the same offset (test_plan.py:124-139).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import bits
+from oracle import rng_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2509_07003_b200 as S
+    from paper_2509_07003_b200 import init as I, rng as R
+    from paper_2509_07003_b200.movers import CudaMover, Member, layout
+    from paper_2509_07003_b200.placement import ShardSpec, local_shape_and_offset, parse_placements
+
+
+def _small_llama(dist, dtype):
+    shapes = [("embed", (131, 64))]
+    for i in range(3):
+        shapes += [(f"l{i}.q", (64, 64)), (f"l{i}.k", (16, 64)), (f"l{i}.o", (64, 64)),
+                   (f"l{i}.down", (64, 96)), (f"l{i}.norm", (64,))]
+    shapes += [("lm_head", (131, 64))]
+    return {n: I.Parameter(s, dist, dtype) for n, s in shapes}
+
+
+@pytest.mark.parametrize("dist,dt", [(lambda: R.Normal(0.0, 0.02), "bfloat16"),
+                                     (lambda: R.Uniform(-0.0346, 0.0346), np.float32),
+                                     (lambda: R.Normal(1.0, 2.0), np.float64)])
+def test_materialize_equals_sequential_walk(dist, dt):
+    mesh = S.create_mesh([("dp", 2), ("tp", 4)])
+    for coord in [(0, 0), (1, 3), (0, 2)]:
+        params = _small_llama(dist(), dt)
+        specs = I.llama3_tp_specs(params, mesh, tp_dim=1)
+        specs["embed"] = ShardSpec(mesh, parse_placements("S(0),S(1)"))  # 2-d, uneven rows
+        del specs["l1.q"]                                               # one full-tensor init
+        st = R.RngState(77, 5, 64)
+        got = I.materialize(params, st, specs, coord)
+        ref_state = R.RngState(77, 5, 64)
+        for name, p in params.items():
+            spec = specs.get(name)
+            if spec is None:
+                want = R.generate_global(p.shape, ref_state, p.dist, dt)
+            else:
+                view = local_shape_and_offset(spec, p.shape, coord)
+                want = R.fill_random(view, ref_state, p.dist, dt)
+                ref_state.advance(int(np.prod(p.shape)))
+            assert torch.equal(bits(got[name]), bits(want)), (name, coord)
+        assert st.offset == ref_state.offset
+
+
+def test_materialize_oracle_spot_check():
+    params = {"w": I.Parameter((300, 40), R.Normal(0.0, 0.02), np.float32),
+              "b": I.Parameter((40,), R.Uniform(-1, 1), np.float32)}
+    st = R.RngState(5)
+    out = I.materialize(params, st)
+    ref_w = O.fill_global((300, 40), 5, 0, 65536, "normal", (0.0, 0.02), np.float32)
+    ref_b = O.fill_global((40,), 5, 1, 65536, "uniform", (-1, 1), np.float32)
+    assert out["w"].cpu().numpy().tobytes() == ref_w.tobytes()
+    assert out["b"].cpu().numpy().tobytes() == ref_b.tobytes()
+    assert st.offset == 2
+
+
+def test_cuda_pack_kernels_match_torch_layout():
+    import sys, os
+    sys.path.insert(0, os.path.dirname(__file__))
+    from cpu_mover import TorchCpuMover
+    gpu, cpu = CudaMover(), TorchCpuMover()
+    g = torch.Generator().manual_seed(0)
+    specs = [((5, 7, 3), 1, torch.float32), ((9, 4), 0, torch.bfloat16), ((2, 10), 1, torch.int64),
+             ((7,), 0, torch.uint8), ((1, 3, 5), 2, torch.float16), ((12, 33), 1, torch.float64)]
+    for P in (1, 2, 3, 4, 8):
+        fulls = [torch.randint(-100, 100, shp, generator=g).to(dt) for shp, _, dt in specs]
+        mem_full_c, mem_full_g, mem_loc_c, mem_loc_g, k = [], [], [], [], P // 2
+        for (shp, d, dt), f in zip(specs, fulls):
+            outer, inner, rows = int(np.prod(shp[:d])), int(np.prod(shp[d + 1:])), shp[d]
+            chunk = -(-rows // P)
+            lo = min(rows, k * chunk)
+            n = min(rows, lo + chunk) - lo
+            loc = f.narrow(d, lo, n).contiguous()
+            mem_full_c.append(Member(f, outer, rows, inner, chunk))
+            mem_full_g.append(Member(f.cuda(), outer, rows, inner, chunk))
+            mem_loc_c.append(Member(loc, outer, n, inner, chunk))
+            mem_loc_g.append(Member(loc.cuda(), outer, n, inner, chunk))
+        seg = layout(mem_full_c)
+        for a, b, c, dd in zip(mem_full_g, mem_loc_c, mem_loc_g, mem_full_c):
+            a.seg_off = b.seg_off = c.seg_off = dd.seg_off
+        # reduce-scatter input packing
+        pc = torch.zeros(seg * P, dtype=torch.uint8)
+        pg = torch.zeros(seg * P, dtype=torch.uint8, device="cuda")
+        cpu.pack_scatter(mem_full_c, pc, seg, P)
+        gpu.pack_scatter(mem_full_g, pg, seg, P)
+        assert torch.equal(pc, pg.cpu())
+        # gather: every rank's segment -> full tensors
+        outs_c = [Member(torch.zeros_like(m.tensor), m.outer, m.rows, m.inner, m.chunk, m.seg_off)
+                  for m in mem_full_c]
+        outs_g = [Member(torch.zeros_like(m.tensor), m.outer, m.rows, m.inner, m.chunk, m.seg_off)
+                  for m in mem_full_g]
+        cpu.unpack_gathered(outs_c, pc, seg, P)
+        gpu.unpack_gathered(outs_g, pg, seg, P)
+        for a, b, f in zip(outs_c, outs_g, fulls):
+            assert torch.equal(a.tensor, b.tensor.cpu()) and torch.equal(a.tensor, f)
+        # local segment pack / unpack round trip
+        sc = torch.zeros(seg, dtype=torch.uint8)
+        sg = torch.zeros(seg, dtype=torch.uint8, device="cuda")
+        cpu.pack_local(mem_loc_c, sc)
+        gpu.pack_local(mem_loc_g, sg)
+        assert torch.equal(sc, sg.cpu())
+        back = [Member(torch.zeros_like(m.tensor), m.outer, m.rows, m.inner, m.chunk, m.seg_off)
+                for m in mem_loc_g]
+        gpu.unpack_local(back, sg)
+        for a, m in zip(back, mem_loc_g):
+            assert torch.equal(a.tensor, m.tensor)
