@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", choices=["dropout", "randn", "init", "redistribute"], default="dropout",
+                    help="dropout = BASELINE cfg2 (the driver's line); the others are the secondary "
+                         "configs 1, 4 and 5, printed in the same JSON shape")
     return ap.parse_args()
 
 
@@ -353,8 +356,11 @@ def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
-    else:
+    elif a.workload == "dropout":
         run_ours(a)
+    else:
+        from tools import bench_extra
+        bench_extra.run(a)
 
 
 if __name__ == "__main__":

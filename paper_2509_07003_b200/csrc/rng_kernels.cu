@@ -141,6 +141,47 @@ __device__ __forceinline__ void chunk_words_aligned(const Gen& g, uint64_t j0, u
   }
 }
 
+// Word 1 only, for a keep/drop decision (dropout): the last two rounds need
+// just hi(M0*x0) of round 9 and lo(M1*x2) of round 10.  Same preconditions as
+// chunk_words_aligned.  A tie on the high threshold word (p = 2^-32) is
+// resolved by the caller with the full block.
+template <int NE>
+__device__ __forceinline__ void chunk_w1_aligned(const Gen& g, uint64_t j0, uint32_t (&w1)[NE]) {
+  const uint32_t sh = g.div_theta.s;
+  const uint64_t beta = (j0 >> sh) + g.offset;
+  const uint64_t t = j0 & (g.theta - 1);
+  const RoundKeys& K = g.keys;
+  uint32_t x0[NE], x1[NE], x2[NE], x3[NE];
+  const uint32_t blo = lo32(beta), bhi = hi32(beta), tlo = lo32(t), thi = hi32(t);
+  const uint64_t pa = mul_wide(blo, kM0);
+  const uint32_t y2 = hi32(pa) ^ thi ^ K.k1[0];
+  const uint32_t y3 = lo32(pa);
+  const uint64_t pb0 = mul_wide(tlo, kM1);
+  const uint64_t pq = mul_wide(y2, kM1);
+  const uint32_t z1 = lo32(pq), hq = hi32(pq);
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const uint64_t pb = pb0 + static_cast<uint64_t>(e) * kM1;
+    const uint32_t y0 = hi32(pb) ^ bhi ^ K.k0[0];
+    const uint32_t y1 = lo32(pb);
+    const uint64_t pa2 = mul_wide(y0, kM0);
+    x0[e] = hq ^ y1 ^ K.k0[1];
+    x1[e] = z1;
+    x2[e] = hi32(pa2) ^ y3 ^ K.k1[1];
+    x3[e] = lo32(pa2);
+  }
+#pragma unroll
+  for (int r = 2; r < 8; ++r) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) philox_round(x0[e], x1[e], x2[e], x3[e], K.k0[r], K.k1[r]);
+  }
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const uint32_t x2_9 = __umulhi(x0[e], kM0) ^ x3[e] ^ K.k1[8];  // round 9: x2 only
+    w1[e] = x2_9 * kM1;                                              // round 10: lo(M1*x2)
+  }
+}
+
 // Words of one element at global index j (generic path).
 __device__ __forceinline__ void elem_words(const Gen& g, uint64_t j, uint32_t& w0, uint32_t& w1) {
   uint64_t b, t;
@@ -193,11 +234,23 @@ __device__ __forceinline__ typename St<DT>::T one_or_zero(bool b) {
 // ---------------------------------------------------------------------------
 // Distribution parameters and the Normal mirror state.
 // ---------------------------------------------------------------------------
+// Device lookup tables of the Normal fast path (40 KiB, staged in shared
+// memory by every kernel that draws normals):
+//   logt[j] = (mult_j * 2^-23, ln(inv_j)) for the 512 mantissa intervals
+//             [1 + j/512, 1 + (j+1)/512) of the 24-bit integer 2^24 - k;
+//   trig[i] = (cos, sin)(i * pi/1024), i = 0..2048 (full circle).
+struct NormalLut {
+  double2 logt[512];
+  double2 trig[2049];
+};
+
 struct NormalMirror {
   const double* rtab;   // NumPy r[k] = sqrt(-2*log1p(-k*2^-24))
   const double* ctab;   // NumPy c[k] = cos(2*pi*(k*2^-24))
-  double err_r;         // max |r_fast - r_np| / r_fast over all k
-  double err_c;         // max |c_fast - c_np| over all k
+  const NormalLut* lut; // device copy of the fast-path tables
+  double err_r;         // max |r_fast - r_np| / r_fast over all k (exhaustive)
+  double err_c;         // max |c_fast - c_np| over all k (exhaustive)
+  double bound_r;       // certification bound B = r*bound_r + |v|*2^-51 (+tiny)
   unsigned long long* fallbacks;
 };
 
@@ -213,41 +266,114 @@ struct DistP {
   NormalMirror nm;
 };
 
-__device__ __forceinline__ double r_fast(uint32_t k) {
-  const double u = static_cast<double>(k) * 0x1p-24;
-  return sqrt(__dmul_rn(-2.0, log1p(-u)));
+constexpr double kLn2Hi = 0x1.62e42fefa3800p-1;   // ln 2, low 16 bits zero: e*kLn2Hi exact
+constexpr double kLn2Lo = 0x1.ef35793c76730p-45;
+constexpr double kTwoPiOver2p24 = 0x1.921fb54442d18p-22;  // 2*pi / 2^24
+
+// Polynomial coefficients as constant-bank operands (no per-use materialisation).
+__constant__ double c_npoly[8] = {
+    -1.0 / 6.0, 1.0 / 5.0, -0.25, 1.0 / 3.0, -0.5,   // log1p Horner (with 1/7 folded below)
+    1.0 / 24.0, 1.0 / 120.0, -1.0 / 6.0};             // cos / sin residual
+
+#ifndef SDR_SQRT_NEWTON
+#define SDR_SQRT_NEWTON 1   // Newton steps on the MUFU.RSQ64H seed before the final correction
+#endif
+#ifndef SDR_FILL_MINB
+#define SDR_FILL_MINB 1
+#endif
+
+// Branch-free sqrt for x in (0, 64): MUFU.RSQ64H seed + Newton steps.  Not
+// correctly rounded -- the exhaustive calibration covers its error.
+__host__ __device__ __forceinline__ double sqrt_nb(double x) {
+#ifdef __CUDA_ARCH__
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+#if SDR_SQRT_NEWTON > 1
+  double e = fma(-hx * y, y, 0.5);
+  y = fma(y, e, y);
+#endif
+  const double e1 = fma(-hx * y, y, 0.5);
+  y = fma(y, e1, y);
+  double s = x * y;
+  const double d = fma(-s, s, x);
+  return fma(0.5 * y, d, s);
+#else
+  return sqrt(x);
+#endif
 }
-__device__ __forceinline__ double c_fast(uint32_t k) {
-  const double u = static_cast<double>(k) * 0x1p-24;
-  return cos(__dmul_rn(6.283185307179586, u));
+
+// r(k) = sqrt(-2*log1p(-k*2^-24)) from the exact integer n = 2^24 - k:
+// w = n*2^-24 = 2^e' * m', m' in [0.75, 1.5); ln m' = -ln(inv) + log1p(t) with
+// t = m'*inv - 1 EXACT (24-bit m' times a 20-bit inv); the two intervals next
+// to m' = 1 use inv = 1 so no cancellation occurs for small k.  Branch-free:
+// k = 0 (r = 0 exactly) is selected at the end.
+__host__ __device__ __forceinline__ double r_fast(uint32_t k, const NormalLut* L) {
+  const uint32_t n = (1u << 24) - k - (k == 0 ? 1u : 0u);  // 1 .. 2^24-1
+#ifdef __CUDA_ARCH__
+  const int b = 32 - __clz(n);                    // bit length, 1..24
+#else
+  const int b = 32 - __builtin_clz(n);
+#endif
+  const uint32_t M = n << (24 - b);               // [2^23, 2^24)
+  const int j = static_cast<int>(M >> 14) - 512;  // mantissa interval 0..511
+  const int e = b - 25 + (j >= 256 ? 1 : 0);      // e' of w = 2^e' m'
+  const double2 tb = L->logt[j];
+  const double t = fma(static_cast<double>(M), tb.x, -1.0);  // exact
+#ifdef __CUDA_ARCH__
+  const double* C = c_npoly;
+#else
+  static const double C[8] = {-1.0 / 6.0, 1.0 / 5.0, -0.25, 1.0 / 3.0, -0.5, 1.0 / 24.0, 1.0 / 120.0, -1.0 / 6.0};
+#endif
+  // log1p(t), |t| <= 2^-9: Taylor to t^6 (|t|^7/7 < 2^-66)
+  double p = fma(t, C[0], C[1]);                   // 1/5 - t/6
+  p = fma(t, p, C[2]);
+  p = fma(t, p, C[3]);
+  p = fma(t, p, C[4]);
+  const double lg = fma(t * t, p, t);             // t + t^2*(-1/2 + ...)
+  const double ne = static_cast<double>(-e);
+  const double Lw = fma(ne, kLn2Hi, fma(ne, kLn2Lo, tb.y - lg));  // -ln w
+  const double r = sqrt_nb(Lw + Lw);
+  return k == 0 ? 0.0 : r;
+}
+
+// c(k) = cos(2*pi*k*2^-24): nearest point of a pi/1024 full-circle table + a
+// short Taylor residual (|d| <= 1.54e-3).
+__host__ __device__ __forceinline__ double c_fast(uint32_t k, const NormalLut* L) {
+  const uint32_t i = (k + 4096u) >> 13;            // 0..2048
+  const int dj = static_cast<int>(k) - static_cast<int>(i << 13);  // [-4096, 4095]
+  const double d = static_cast<double>(dj) * kTwoPiOver2p24;
+  const double d2 = d * d;
+#ifdef __CUDA_ARCH__
+  const double* C = c_npoly;
+#else
+  static const double C[8] = {-1.0 / 6.0, 1.0 / 5.0, -0.25, 1.0 / 3.0, -0.5, 1.0 / 24.0, 1.0 / 120.0, -1.0 / 6.0};
+#endif
+  const double cm = d2 * fma(d2, C[5], C[4]);                  // cos d - 1
+  const double sd = fma(d * d2, fma(d2, C[6], C[7]), d);        // sin d
+  const double2 cs = L->trig[i];
+  return cs.x + fma(cs.x, cm, -cs.y * sd);
 }
 
 // Normal (rng.py:150-156): float64 Box-Muller then one cast.  Fast path with
-// the device functions + a rigorous error bound; elements whose rounding to
-// DT the bound cannot certify take the exact NumPy tables.
+// the table functions + a rigorous error bound; elements whose rounding to DT
+// the bound cannot certify recompute from the exact NumPy tables.
 template <int DT>
-__device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, uint32_t w0,
-                                                           uint32_t w1) {
+__device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, const NormalLut* L,
+                                                           uint32_t w0, uint32_t w1) {
   const uint32_t k1 = w0 >> 8, k2 = w1 >> 8;
   if constexpr (DT != SDR_F64) {
-    const double r = r_fast(k1), c = c_fast(k2);
+    const double r = r_fast(k1, L), c = c_fast(k2, L);
     const double z = __dmul_rn(r, c);
     const double s = __dmul_rn(P.stdv, z);
     const double v = __dadd_rn(P.mean, s);
-    const double u = 0x1p-53;
-    const double d1 = r * (P.nm.err_r * fabs(c) + P.nm.err_c * (1.0 + P.nm.err_r));
-    const double B = 2.0 * (fabs(P.stdv) * (d1 + 2.0 * u * fabs(z)) + 2.0 * u * fabs(s) +
-                            2.0 * u * fabs(v)) + 0x1p-1060;
+    // |v_numpy - v| <= r*|std|*(Er + Ac(1+Er) + 5u) + 2u|v|, doubled (host: bound_r)
+    const double B = fma(r, P.nm.bound_r, fabs(v) * 0x1p-51) + 0x1p-1060;
     const auto lo = from_f64<DT>(v - B), hi = from_f64<DT>(v + B);
-    if (lo == hi) {
-      // Also reject a signed-zero straddle: from_f64 compares bit patterns
-      // for 16-bit types; for f32 compare bits explicitly.
-      if constexpr (DT == SDR_F32) {
-        if (__float_as_uint(lo) == __float_as_uint(hi)) return lo;
-      } else {
-        return lo;
-      }
-    }
+    bool ok;
+    if constexpr (DT == SDR_F32) ok = __float_as_uint(lo) == __float_as_uint(hi);
+    else ok = lo == hi;
+    if (__builtin_expect(ok, 1)) return lo;
     atomicAdd(P.nm.fallbacks, 1ull);
   }
   const double r = __ldg(P.nm.rtab + k1), c = __ldg(P.nm.ctab + k2);
@@ -256,8 +382,17 @@ __device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, uint3
   return from_f64<DT>(v);
 }
 
+// Stage the Normal tables in shared memory (whole CTA participates).
+__device__ __forceinline__ void stage_lut(NormalLut* dst, const NormalLut* src) {
+  const double2* s = reinterpret_cast<const double2*>(src);
+  double2* d = reinterpret_cast<double2*>(dst);
+  for (int i = threadIdx.x; i < static_cast<int>(sizeof(NormalLut) / 16); i += blockDim.x) d[i] = s[i];
+  __syncthreads();
+}
+
 template <int DIST, int DT>
-__device__ __forceinline__ typename St<DT>::T dist_value(const DistP& P, uint32_t w0, uint32_t w1) {
+__device__ __forceinline__ typename St<DT>::T dist_value(const DistP& P, const NormalLut* L,
+                                                         uint32_t w0, uint32_t w1) {
   using T = typename St<DT>::T;
   const uint64_t u64 = (static_cast<uint64_t>(w1) << 32) | w0;
   if constexpr (DIST == SDR_UNIFORM01) {
@@ -275,7 +410,7 @@ __device__ __forceinline__ typename St<DT>::T dist_value(const DistP& P, uint32_
       return from_f64<DT>(__dadd_rn(P.lo, __dmul_rn(P.span, u)));
     }
   } else if constexpr (DIST == SDR_NORMAL) {
-    return normal_value<DT>(P, w0, w1);
+    return normal_value<DT>(P, L, w0, w1);
   } else if constexpr (DIST == SDR_RANDINT) {
     uint64_t q, rem;
     P.ispan.divmod(u64, q, rem);
@@ -340,6 +475,7 @@ struct __align__(16) FillArgs {
   ViewIndexer ix;
   void* out;
   // Fast-path chunk walk: chunk q covers local [8q, 8q+8) inside one row.
+  uint32_t aligned;  // THETA pow2 >= 8 and chunk starts 8-aligned (no straddle)
   uint64_t nchunks;
   uint64_t chunks_per_row;
   FastDiv64 div_cpr;
@@ -347,6 +483,7 @@ struct __align__(16) FillArgs {
 
 // Global flat index of the first element of chunk q (fast path).
 __device__ __forceinline__ uint64_t chunk_base(const FillArgs& A, uint64_t q) {
+  if (A.ix.cv.nd == 0) return static_cast<uint64_t>(A.ix.cv.base) + q * kV;  // one contiguous run
   uint64_t row, cq;
   A.div_cpr.divmod(q, row, cq);
   uint64_t j = static_cast<uint64_t>(A.ix.cv.base) + cq * kV;
@@ -360,41 +497,54 @@ __device__ __forceinline__ uint64_t chunk_base(const FillArgs& A, uint64_t q) {
   return j;
 }
 
-template <int DIST, int DT>
-__device__ __forceinline__ void fill_chunk(const FillArgs& A, uint64_t q) {
+template <int DIST, int DT, bool ALIGNED>
+__device__ __forceinline__ void fill_chunk(const FillArgs& A, const NormalLut* L, uint64_t q) {
   using T = typename St<DT>::T;
   const uint64_t j0 = chunk_base(A, q);
   uint32_t w0[kV], w1[kV];
-  chunk_words(A.g, j0, w0, w1);
+  if constexpr (ALIGNED) chunk_words_aligned<kV>(A.g, j0, w0, w1);
+  else chunk_words<kV>(A.g, j0, w0, w1);
   T v[kV];
 #pragma unroll
-  for (int e = 0; e < kV; ++e) v[e] = dist_value<DIST, DT>(A.d, w0[e], w1[e]);
+  for (int e = 0; e < kV; ++e) v[e] = dist_value<DIST, DT>(A.d, L, w0[e], w1[e]);
   store_chunk(static_cast<T*>(A.out) + q * kV, v);
 }
 
 template <int DIST, int DT>
-__device__ __forceinline__ void fill_elem(const FillArgs& A, uint64_t i) {
+__device__ __forceinline__ void fill_elem(const FillArgs& A, const NormalLut* L, uint64_t i) {
   using T = typename St<DT>::T;
   uint32_t w0, w1;
   elem_words(A.g, A.ix.global_of(i), w0, w1);
-  static_cast<T*>(A.out)[i] = dist_value<DIST, DT>(A.d, w0, w1);
+  static_cast<T*>(A.out)[i] = dist_value<DIST, DT>(A.d, L, w0, w1);
 }
 
-template <int DIST, int DT>
-__global__ void __launch_bounds__(256) k_fill_fast(const __grid_constant__ FillArgs A) {
+template <int DIST, int DT, bool ALIGNED>
+__global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_fast(const __grid_constant__ FillArgs A) {
+  const NormalLut* L = nullptr;
+  if constexpr (DIST == SDR_NORMAL) {
+    __shared__ NormalLut s_lut;
+    stage_lut(&s_lut, A.d.nm.lut);
+    L = &s_lut;
+  }
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < A.nchunks;
        q += stride)
-    fill_chunk<DIST, DT>(A, q);
+    fill_chunk<DIST, DT, ALIGNED>(A, L, q);
 }
 
 template <int DIST, int DT>
 __global__ void __launch_bounds__(256) k_fill_generic(const __grid_constant__ FillArgs A) {
+  const NormalLut* L = nullptr;
+  if constexpr (DIST == SDR_NORMAL) {
+    __shared__ NormalLut s_lut;
+    stage_lut(&s_lut, A.d.nm.lut);
+    L = &s_lut;
+  }
   const uint64_t n = static_cast<uint64_t>(A.ix.cv.numel);
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += stride)
-    fill_elem<DIST, DT>(A, i);
+    fill_elem<DIST, DT>(A, L, i);
 }
 
 // Multi-tensor fill (K3): the members of one (distribution, dtype) group are
@@ -409,6 +559,12 @@ __global__ void __launch_bounds__(256) k_fill_batch(const FillArgs* __restrict__
                                                     int n, uint64_t ntiles) {
   __shared__ __align__(16) unsigned char smem[sizeof(FillArgs)];
   FillArgs& A = *reinterpret_cast<FillArgs*>(smem);
+  const NormalLut* L = nullptr;
+  if constexpr (DIST == SDR_NORMAL) {
+    __shared__ NormalLut s_lut;
+    stage_lut(&s_lut, descs[0].d.nm.lut);
+    L = &s_lut;
+  }
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     // member f: last index with tile_prefix[f] <= t (uniform across the CTA)
     int lo = 0, hi = n - 1;
@@ -430,13 +586,17 @@ __global__ void __launch_bounds__(256) k_fill_batch(const FillArgs* __restrict__
       const uint64_t q0 = lt * (kTileElems / kV);
       uint64_t q1 = q0 + kTileElems / kV;
       if (q1 > A.nchunks) q1 = A.nchunks;
-      for (uint64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) fill_chunk<DIST, DT>(A, q);
+      if (A.aligned) {
+        for (uint64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) fill_chunk<DIST, DT, true>(A, L, q);
+      } else {
+        for (uint64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) fill_chunk<DIST, DT, false>(A, L, q);
+      }
     } else {
       const uint64_t i0 = lt * kTileElems;
       uint64_t i1 = i0 + kTileElems;
       const uint64_t numel = static_cast<uint64_t>(A.ix.cv.numel);
       if (i1 > numel) i1 = numel;
-      for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) fill_elem<DIST, DT>(A, i);
+      for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) fill_elem<DIST, DT>(A, L, i);
     }
   }
 }
@@ -565,13 +725,27 @@ __global__ void __launch_bounds__(256, SDR_DROP_MINB) k_dropout_fast(const __gri
 #pragma unroll
     for (int h = 0; h < SDR_DROP_SPLIT; ++h) {
       uint32_t w0[NE], w1[NE];
-      if constexpr (ALIGNED) chunk_words_aligned<NE>(A.g, j0 + h * NE, w0, w1);
-      else chunk_words<NE>(A.g, j0 + h * NE, w0, w1);
+      if constexpr (ALIGNED) {
+        chunk_w1_aligned<NE>(A.g, j0 + h * NE, w1);
+      } else {
+        chunk_words<NE>(A.g, j0 + h * NE, w0, w1);
+      }
 #pragma unroll
       for (int i = 0; i < NE; ++i) {
         const int e = h * NE + i;
-        const uint64_t u64 = (static_cast<uint64_t>(w1[i]) << 32) | w0[i];
-        keep[e] = u64 <= A.keep_le;
+        if constexpr (ALIGNED) {
+          // (w1:w0) <= keep_le is decided by w1 unless w1 equals its high word
+          const uint32_t H = hi32(A.keep_le);
+          keep[e] = w1[i] < H;
+          if (__builtin_expect(w1[i] == H, 0)) {
+            uint32_t f0, f1;
+            elem_words(A.g, j0 + h * NE + i, f0, f1);
+            keep[e] = ((static_cast<uint64_t>(f1) << 32) | f0) <= A.keep_le;
+          }
+        } else {
+          const uint64_t u64 = (static_cast<uint64_t>(w1[i]) << 32) | w0[i];
+          keep[e] = u64 <= A.keep_le;
+        }
         if constexpr (XT == SDR_BF16) {
           // unpack from the raw 16 B vector: even lane = low half of a word
           uint32_t wd;
@@ -644,16 +818,18 @@ __global__ void k_philox_blocks(const uint64_t* tau, const uint64_t* beta, int64
 }
 
 // Exhaustive calibration of the Normal fast path against the NumPy tables.
-__global__ void k_normal_calibrate(const double* rtab, const double* ctab,
+__global__ void k_normal_calibrate(const double* rtab, const double* ctab, const NormalLut* lut,
                                    unsigned long long* max_r_bits,
                                    unsigned long long* max_c_bits) {
+  __shared__ NormalLut s_lut;
+  stage_lut(&s_lut, lut);
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= (1u << 24)) return;
-  const double rg = r_fast(k), rn = rtab[k];
+  const double rg = r_fast(k, &s_lut), rn = rtab[k];
   double er;
   if (rg == 0.0 || rn == 0.0) er = (rg == rn) ? 0.0 : __longlong_as_double(0x7FF0000000000000ll);
   else er = fabs(rg - rn) / rg;
-  const double ec = fabs(c_fast(k) - ctab[k]);
+  const double ec = fabs(c_fast(k, &s_lut) - ctab[k]);
   unsigned long long br = __double_as_longlong(er), bc = __double_as_longlong(ec);
   // Non-negative doubles order like their bit patterns; reduce per warp first.
   for (int o = 16; o > 0; o >>= 1) {
@@ -789,11 +965,50 @@ static int launch_grid(uint64_t work, int threads) {
 struct NormalState {
   double* rtab = nullptr;
   double* ctab = nullptr;
+  NormalLut* lut = nullptr;
   unsigned long long* fallbacks = nullptr;
   double err_r = 0, err_c = 0;
   bool loaded = false;
 };
 static std::mutex g_nm_mu;
+
+static double round_sig(long double x, int bits) {
+  int e = 0;
+  const long double m = frexpl(x, &e);  // x = m * 2^e, m in [0.5, 1)
+  return static_cast<double>(ldexpl(nearbyintl(ldexpl(m, bits)), e - bits));
+}
+
+// Host construction of the fast-path tables (long double arithmetic).
+static void build_normal_lut(NormalLut& L) {
+  for (int j = 0; j < 512; ++j) {
+    long double inv, mult;
+    if (j == 0 || j == 511) {
+      inv = 1.0L;
+      mult = (j == 511) ? 0.5L : 1.0L;
+    } else if (j < 256) {
+      const long double mc = 1.0L + (j + 0.5L) / 512.0L;
+      inv = round_sig(1.0L / mc, 20);
+      mult = inv;
+    } else {
+      const long double mc = (1.0L + (j + 0.5L) / 512.0L) / 2.0L;
+      inv = round_sig(1.0L / mc, 20);
+      mult = inv / 2.0L;
+    }
+    L.logt[j].x = static_cast<double>(ldexpl(mult, -23));
+    L.logt[j].y = (inv == 1.0L) ? 0.0 : static_cast<double>(logl(inv));
+  }
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int i = 0; i <= 2048; ++i) {
+    const long double a = pi * i / 1024.0L;
+    L.trig[i].x = static_cast<double>(cosl(a));
+    L.trig[i].y = static_cast<double>(sinl(a));
+  }
+  // exact table points
+  L.trig[512].x = 0.0;
+  L.trig[1024].y = 0.0;
+  L.trig[1536].x = 0.0;
+  L.trig[2048].y = 0.0;
+}
 static NormalState g_nm[64];
 
 static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) {
@@ -824,8 +1039,13 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
       if (device < 0 || device >= 64 || !g_nm[device].loaded) return SDR_E_NOTABLES;
       P.nm.rtab = g_nm[device].rtab;
       P.nm.ctab = g_nm[device].ctab;
+      P.nm.lut = g_nm[device].lut;
       P.nm.err_r = g_nm[device].err_r;
       P.nm.err_c = g_nm[device].err_c;
+      {
+        const double Er = P.nm.err_r, Ac = P.nm.err_c, u = 0x1p-53;
+        P.nm.bound_r = 2.0 * fabs(P.stdv) * (Er + Ac * (1.0 + Er) + 5.0 * u) * (1.0 + 0x1p-40);
+      }
       P.nm.fallbacks = g_nm[device].fallbacks;
       break;
     }
@@ -877,8 +1097,10 @@ static void setup_chunks(const CanonView& cv, bool fast, uint64_t& nchunks, uint
 
 template <int DIST, int DT>
 static void launch_fill(const FillArgs& A, bool fast, cudaStream_t s) {
-  if (fast) {
-    k_fill_fast<DIST, DT><<<grid_for(k_fill_fast<DIST, DT>, A.nchunks, 256), 256, 0, s>>>(A);
+  if (fast && A.aligned) {
+    k_fill_fast<DIST, DT, true><<<grid_for(k_fill_fast<DIST, DT, true>, A.nchunks, 256), 256, 0, s>>>(A);
+  } else if (fast) {
+    k_fill_fast<DIST, DT, false><<<grid_for(k_fill_fast<DIST, DT, false>, A.nchunks, 256), 256, 0, s>>>(A);
   } else {
     k_fill_generic<DIST, DT><<<grid_for(k_fill_generic<DIST, DT>, A.ix.cv.numel, 256), 256, 0, s>>>(A);
   }
@@ -941,6 +1163,7 @@ int fill(void* out, int dt, const sdr_dist& dist, const sdr_rng& rng, const sdr_
   A.out = out;
   const bool fast = cv.istride == 1 && cv.inner % kV == 0 && aligned16(out);
   setup_chunks(cv, fast, A.nchunks, A.chunks_per_row, A.div_cpr);
+  A.aligned = fast && chunks_aligned(cv, rng.theta, kV);
   switch (dist.kind) {
     case SDR_UNIFORM01: return dispatch_fill_dt<SDR_UNIFORM01>(dt, A, fast, s);
     case SDR_UNIFORM: return dispatch_fill_dt<SDR_UNIFORM>(dt, A, fast, s);
@@ -1029,12 +1252,19 @@ int normal_tables_load(int device, const double* r_host, const double* c_host, d
     e = cudaMalloc(&S.rtab, bytes);
     if (e == cudaSuccess) e = cudaMalloc(&S.ctab, bytes);
     if (e == cudaSuccess) e = cudaMalloc(&S.fallbacks, 3 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&S.lut, sizeof(NormalLut));
+    if (e == cudaSuccess) {
+      NormalLut h;
+      build_normal_lut(h);
+      e = cudaMemcpy(S.lut, &h, sizeof(NormalLut), cudaMemcpyHostToDevice);
+    }
   }
   if (e == cudaSuccess) e = cudaMemcpy(S.rtab, r_host, bytes, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(S.ctab, c_host, bytes, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(S.fallbacks, 0, 3 * sizeof(unsigned long long));
   if (e == cudaSuccess) {
-    k_normal_calibrate<<<(1u << 24) / 256, 256>>>(S.rtab, S.ctab, S.fallbacks + 1, S.fallbacks + 2);
+    k_normal_calibrate<<<(1u << 24) / 256, 256>>>(S.rtab, S.ctab, S.lut, S.fallbacks + 1,
+                                                  S.fallbacks + 2);
     e = cudaGetLastError();
   }
   unsigned long long bits[2] = {0, 0};
@@ -1050,6 +1280,18 @@ int normal_tables_load(int device, const double* r_host, const double* c_host, d
   if (er) *er = S.err_r;
   if (ec) *ec = S.err_c;
   return SDR_OK;
+}
+
+// Host evaluation of the fast functions (accuracy harness in tools/).
+void normal_fast_host(uint32_t k, double* r, double* c) {
+  static NormalLut L;
+  static bool built = false;
+  if (!built) {
+    build_normal_lut(L);
+    built = true;
+  }
+  *r = r_fast(k, &L);
+  *c = c_fast(k, &L);
 }
 
 int normal_tables_loaded(int device) {
@@ -1125,6 +1367,7 @@ int fill_batch(void* const* outs, const int32_t* dts, const sdr_dist* dists, con
     m.a.out = outs[i];
     const bool fast = cv.istride == 1 && cv.inner % kV == 0 && aligned16(outs[i]);
     setup_chunks(cv, fast, m.a.nchunks, m.a.chunks_per_row, m.a.div_cpr);
+    m.a.aligned = fast && chunks_aligned(cv, rngs[i].theta, kV);
     m.tiles = (static_cast<uint64_t>(cv.numel) + kTileElems - 1) / kTileElems;
     groups[dists[i].kind * 8 + dt].push_back(m);
   }

@@ -1,0 +1,126 @@
+"""Secondary bench workloads (BASELINE configs 1, 4, 5), same JSON shape as
+bench.py's main line.  `python bench.py --workload randn|init|redistribute`.
+
+randn        cfg1: Normal(0,1) f32 [4096,4096] Shard(0) over N ranks (strong)
+init         cfg4: all 291 LLaMA-3-8B params, Normal(0,0.02) bf16, TP=N (strong)
+redistribute cfg5: one LLaMA-3-8B layer's params on DP x TP: fused all-gather over
+             DP (S->R) then reduce-scatter of same-shaped grads (P->S); at N=1
+             this measures pack + local copy + unpack only (no peers).
+"""
+import json
+import math
+import os
+import statistics
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+SEED = 20240817
+
+
+def _env():
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def _time(fn, steps, warmup, dev, ws):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+    a.record()
+    for _ in range(steps):
+        fn()
+    b.record()
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.item()
+
+
+def run(a):
+    from paper_2509_07003_b200 import create_mesh, init as I, rng as R
+    from paper_2509_07003_b200.placement import ShardSpec, local_shape_and_offset, parse_placements
+    ws, rank, local = _env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    line = {"n_gpus": ws, "steps": a.steps, "warmup": a.warmup, "higher_is_better": True,
+            "vs_baseline": None, "data": "synthetic", "gpu_launches": a.steps}
+    if a.workload == "randn":
+        shape = (4096, 4096)
+        mesh = create_mesh([("dp", ws)])
+        spec = ShardSpec(mesh, parse_placements("S(0)"))
+        v = local_shape_and_offset(spec, shape, mesh.coords_of_rank(rank))
+        out = torch.empty(v.local_shape, dtype=torch.float32, device=dev)
+        st = R.RngState(SEED)
+        R.ensure_normal_tables(dev)
+        ms = _time(lambda: R.fill_random(v, st, R.Normal(0, 1), np.float32, out=out), a.steps, a.warmup, dev, ws)
+        n = math.prod(shape)
+        line.update(metric="sharded randn GB/s (cfg1)", value=round(n * 4 / ms / 1e6, 3), unit="GB/s",
+                    ms_per_step=round(ms, 4), scaling="strong", dtype="f32",
+                    config={"workload": "cfg1: randn f32 [4096,4096] Shard(0)", "parallelism": f"dp{ws}",
+                            "elements_per_s": round(n / ms * 1e3, 1)})
+    elif a.workload == "init":
+        params = I.llama3_8b_params(lambda nm, s: R.Normal(0.0, 0.02), "bfloat16")
+        mesh = create_mesh([("tp", ws)])
+        specs = I.llama3_tp_specs(params, mesh)
+        coord = mesh.coords_of_rank(rank)
+        n_local = sum(math.prod(local_shape_and_offset(specs[k], p.shape, coord).local_shape)
+                      for k, p in params.items())
+        total = sum(math.prod(p.shape) for p in params.values())
+
+        def step():
+            for p in params.values():
+                p.value = None
+            I.materialize(params, R.RngState(SEED), specs, coord, device=dev)
+        ms = _time(step, a.steps, a.warmup, dev, ws)
+        # unique elements across ranks (norms are replicated: count once)
+        line.update(metric="LLaMA-3-8B sharded init GB/s (cfg4)", value=round(total * 2 / ms / 1e6, 3),
+                    unit="GB/s", ms_per_step=round(ms, 3), scaling="strong", dtype="bf16",
+                    config={"workload": "cfg4: LLaMA-3-8B 291 params normal(0,0.02) bf16, TP placements",
+                            "parallelism": f"tp{ws}", "per_gpu_elements": n_local,
+                            "elements_per_s": round(total / ms * 1e3, 1)})
+    else:
+        from paper_2509_07003_b200.dtensor import from_local, redistribute_many
+        dp = 2 if ws % 2 == 0 else 1
+        tp = ws // dp
+        mesh = create_mesh([("dp", dp), ("tp", tp)])
+        coord = mesh.coords_of_rank(rank)
+        d, ff, kv = 4096, 14336, 1024
+        layer = {"q": ((d, d), "S(1),S(0)"), "k": ((kv, d), "S(1),S(0)"), "v": ((kv, d), "S(1),S(0)"),
+                 "o": ((d, d), "S(0),S(1)"), "gate": ((ff, d), "S(1),S(0)"), "up": ((ff, d), "S(1),S(0)"),
+                 "down": ((d, ff), "S(0),S(1)"), "n1": ((d,), "S(0),R"), "n2": ((d,), "S(0),R")}
+        xs, dsts, grads, gdst = [], [], [], []
+        for name, (shape, pl) in layer.items():
+            spec = ShardSpec(mesh, parse_placements(pl))
+            v = local_shape_and_offset(spec, shape, coord)
+            xs.append(from_local(torch.randn(v.local_shape, device=dev, dtype=torch.bfloat16), spec, shape, coord))
+            dst_pl = ["R"] + [str(p) for p in spec.placements[1:]]
+            dsts.append(ShardSpec(mesh, parse_placements(",".join(dst_pl))))
+            gspec = ShardSpec(mesh, parse_placements(",".join(["P"] + dst_pl[1:])))
+            gv = local_shape_and_offset(gspec, shape, coord)
+            grads.append(from_local(torch.randn(gv.local_shape, device=dev, dtype=torch.bfloat16), gspec, shape, coord))
+            gdst.append(spec)
+        ms_ag = _time(lambda: redistribute_many(xs, dsts), a.steps, a.warmup, dev, ws)
+        ms_rs = _time(lambda: redistribute_many(grads, gdst), a.steps, a.warmup, dev, ws)
+        S = sum(math.prod(x.shape) // tp for x in xs) * 2  # gathered bytes per DP fiber
+        busbw = lambda ms: S / ms / 1e6 * (dp - 1) / dp if dp > 1 else 0.0
+        line.update(metric="fused redistribute busBW (cfg5)", value=round(busbw(ms_ag), 3), unit="GB/s",
+                    ms_per_step=round(ms_ag, 4), scaling="weak", dtype="bf16",
+                    config={"workload": "cfg5: one LLaMA-3-8B layer, fused AG (S->R over dp) + RS (P->S)",
+                            "parallelism": f"dp{dp}xtp{tp}", "ms_allgather": round(ms_ag, 4),
+                            "ms_reducescatter": round(ms_rs, 4),
+                            "busbw_reducescatter": round(busbw(ms_rs), 3),
+                            "payload_bytes_per_fiber": S})
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()

@@ -1,0 +1,29 @@
+"""Summarise an .ncu-rep (run here, no GPU): key throughput/pipe/stall metrics."""
+import csv, io, subprocess, sys
+
+KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_elapsed", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_elapsed", "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.per_cycle_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "launch__occupancy_limit_registers",
+        "smsp__inst_executed.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]
+
+def main(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")]
+        print(f"kernel: {name}")
+        for k in KEYS:
+            if k in hdr:
+                print(f"  {k:70s} {r[hdr.index(k)]:>16s} {units[hdr.index(k)]}")
+        st = sorted(((h.replace("smsp__pcsamp_warps_issue_stalled_", ""), float(r[i] or 0)) for i, h in enumerate(hdr)
+                     if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued")),
+                    key=lambda x: -x[1])
+        tot = sum(v for _, v in st) or 1
+        print("  stall samples: " + ", ".join(f"{n} {100*v/tot:.0f}%" for n, v in st[:6]))
+
+if __name__ == "__main__":
+    main(sys.argv[1])

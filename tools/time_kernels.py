@@ -20,9 +20,8 @@ def timeit(fn, reps=10, warm=3):
         fn()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(True), torch.cuda.Event(True)) for _ in range(reps)]
-    # queue a long GPU op first so the host overhead of fn() is hidden
-    big = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
-    big.fill_(1)
+    # queue a ~reps ms spin first so the host overhead of fn() is hidden
+    torch.cuda._sleep(int(2e6) * max(1, reps // 5))
     for a, b in ev:
         a.record()
         fn()
