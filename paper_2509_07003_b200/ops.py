@@ -105,3 +105,77 @@ def dropout(x: torch.Tensor, p: float, state: RngState | None = None,
         y = dropout_apply(x, p, state, view)
     state.advance(math.prod(view.global_shape))
     return y
+
+
+# ---------------------------------------------------------------------------
+# Dropout on a DTensor (dispatch.py:499-576 for op "dropout").
+# ---------------------------------------------------------------------------
+# Per-mesh-dim redistribution cost in multiples of S*(P-1)/P (dispatch.py:289-302).
+_COST = {("S", "R"): 1, ("IS", "R"): 1, ("P", "R"): 2, ("P", "S"): 1, ("P", "IS"): 1,
+         ("R", "S"): 0, ("R", "IS"): 0, ("S", "S"): 1, ("S", "IS"): 1, ("IS", "S"): 1,
+         ("IS", "IS"): 1}
+
+
+def _kind(p):
+    from .placement import InterleavedShard, Partial, Shard
+    if isinstance(p, Shard):
+        return "S"
+    if isinstance(p, InterleavedShard):
+        return "IS"
+    if isinstance(p, Partial):
+        return "P"
+    return "R"
+
+
+def dropout_input_spec(x):
+    """The placement dropout runs at: the cheapest (in bytes moved) spec among
+    R / S(d) / the input's own IS per mesh dim -- Partial is not allowed --
+    first in enumeration order on ties (dispatch.py:181-191, 330-372).  A
+    Partial input therefore becomes a reduce-scatter to the first free S(d)."""
+    import itertools
+    from fractions import Fraction
+    from .placement import InterleavedShard, PlacementError, Replicate, Shard, ShardSpec
+    spec = x.meta.spec
+    mesh = spec.mesh
+    ndim = len(x.shape)
+    choices = [Replicate()] + [Shard(d) for d in range(ndim)]
+    choices += [p for p in spec.placements if isinstance(p, InterleavedShard) and p not in choices]
+    nbytes = math.prod(x.shape) * x.local.element_size()
+    best = None
+    for combo in itertools.product(choices, repeat=mesh.ndim):
+        try:
+            cand = ShardSpec(mesh, tuple(combo))
+            cand.validate_for_shape(x.shape)
+        except PlacementError:
+            continue
+        cost = Fraction(0)
+        ok = True
+        for i, (s, d) in enumerate(zip(spec.placements, cand.placements)):
+            if s == d:
+                continue
+            key = (_kind(s), _kind(d))
+            if key not in _COST:
+                ok = False
+                break
+            P = mesh.sizes[i]
+            cost += _COST[key] * Fraction(nbytes * (P - 1), P)
+        if ok and (best is None or cost < best[0]):
+            best = (cost, cand)
+    return best[1]
+
+
+def dtensor_dropout(x, p: float, state: RngState | None = None, ledger=None, *, mover=None):
+    """Dropout of a DTensor with single-device semantics.  The mask is this
+    rank's slice of ONE global Bernoulli(1-p) draw over the input window, the
+    state advances by ceil(global_numel/THETA) on every rank (dispatch.py:
+    567-576); p == 0 returns x untouched and draws nothing (ops.py:174-175)."""
+    from .dtensor import DTensor, redistribute
+    if p == 0.0:
+        return x
+    state = runtime_mod.current().rng if state is None else state
+    target = dropout_input_spec(x)
+    if target != x.meta.spec:
+        x = redistribute(x, target, ledger, mover=mover)
+    y = dropout_apply(x.local, p, state, x.view)
+    state.advance(math.prod(x.shape))
+    return DTensor(x.meta, y, x.coord)

@@ -124,3 +124,19 @@ def test_dropout_op_autograd_and_state():
     assert torch.equal(bits(y.detach()), bits((x.detach() * mask) * scale))
     st2 = R.RngState(3, 10, 64)
     assert ops.dropout(x, 0.0, state=st2) is x and st2.offset == 10
+
+
+def test_dtensor_dropout_world_one():
+    """DTensor-level dropout (dispatch.py:567-576) on a 1-rank mesh: same bits
+    as the plain op, state advanced once."""
+    from paper_2509_07003_b200.dtensor import from_local
+    mesh = S.create_mesh([("d", 1)])
+    spec = ShardSpec(mesh, parse_placements("S(0)"))
+    x = torch.randn(16, 24, device="cuda")
+    xd = from_local(x, spec, (16, 24), (0,))
+    st = R.RngState(9)
+    y = ops.dtensor_dropout(xd, 0.2, st)
+    assert st.offset == 1
+    ref = ops.dropout_apply(x, 0.2, R.RngState(9))
+    assert torch.equal(bits(y.local), bits(ref))
+    assert ops.dtensor_dropout(xd, 0.0, st) is xd and st.offset == 1

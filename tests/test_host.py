@@ -142,3 +142,17 @@ def test_windows_partition_the_tensor(shape, data):
         v = local_shape_and_offset(spec, tuple(shape), coord)
         seen[v.global_flat_indices(device="cpu").numpy()] += 1
     assert (seen == 1).all()
+
+
+def test_dropout_strategy_matches_reference_dispatch():
+    """Partial input -> first S(d) that validates (reduce-scatter), as the
+    reference's min-byte propagation picks (dispatch.py:330-372)."""
+    import torch
+    from paper_2509_07003_b200.dtensor import DTensor, DTensorMeta
+    from paper_2509_07003_b200.ops import dropout_input_spec
+    mesh = create_mesh([("a", 2), ("b", 2)])
+    for src, want in [("P,R", "S(0),R"), ("S(0),P", "S(0),S(1)"), ("S(1),S(0)", "S(1),S(0)"),
+                      ("R,P", "R,S(0)"), ("P,P", "S(0),S(1)")]:
+        spec = ShardSpec(mesh, parse_placements(src))
+        x = DTensor(DTensorMeta((8, 8), spec, torch.float32), torch.zeros(1), (0, 0))
+        assert str(dropout_input_spec(x).placements) == str(parse_placements(want)), (src, want)

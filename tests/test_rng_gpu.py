@@ -268,3 +268,36 @@ def test_normal_mirror_calibration_and_large_parity():
         assert _same(g, _oracle_tensor(ref)), name
     after = R.normal_fallback_count()
     assert after >= before
+
+
+def test_64bit_indexing_beyond_2p32_elements():
+    """One launch over > 2^32 elements (u8 Bernoulli, 4.3 GB) and a small
+    window at the end of a 2^40-element tensor: 64-bit j, beta and chunk math."""
+    shape = (65539, 65537)  # 4,295,229,443 elements
+    t = R.generate_global(shape, R.RngState(11, 3), R.Bernoulli(0.3), np.uint8)
+    for r in (0, 32768, 65538):
+        cols = np.array([0, 1, 7, 8, 65535, 65536])
+        j = r * shape[1] + cols
+        ref = O.fill_indices(j, 11, 3, 65536, "bernoulli", (0.3,), np.uint8)
+        got = t[r, torch.as_tensor(cols, device=t.device)].cpu().numpy()
+        assert got.tobytes() == ref.tobytes(), r
+    del t
+    torch.cuda.empty_cache()
+    big = (1 << 20, 1 << 20)
+    view = S.ShardView(big, windows=[S.placement.DimWindow((1 << 20) - 3, 3),
+                                     S.placement.DimWindow((1 << 20) - 40, 40)])
+    got = R.fill_random(view, R.RngState(5, 7), R.Normal(0.0, 1.0), np.float32)
+    ref = O.fill_window(big, [np.arange((1 << 20) - 3, 1 << 20), np.arange((1 << 20) - 40, 1 << 20)], 5, 7,
+                        65536, "normal", (0.0, 1.0), np.float32)
+    assert _same(got, torch.from_numpy(ref))
+
+
+def test_empty_and_single_element_windows():
+    for shape in [(0,), (5, 0, 3), (1,), (1, 1, 1)]:
+        t = R.generate_global(shape, R.RngState(1), R.Normal(0, 1), np.float32)
+        assert tuple(t.shape) == shape
+        ref = O.fill_global(shape, 1, 0, 65536, "normal", (0.0, 1.0), np.float32)
+        assert _same(t, torch.from_numpy(ref))
+    from paper_2509_07003_b200 import ops
+    x = torch.zeros((0, 4), device="cuda")
+    assert ops.dropout_apply(x, 0.5, R.RngState()).shape == (0, 4)
