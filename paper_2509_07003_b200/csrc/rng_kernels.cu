@@ -279,7 +279,7 @@ __constant__ double c_npoly[8] = {
 #define SDR_SQRT_NEWTON 1   // Newton steps on the MUFU.RSQ64H seed before the final correction
 #endif
 #ifndef SDR_FILL_MINB
-#define SDR_FILL_MINB 1
+#define SDR_FILL_MINB 2   // 2 CTAs/SM: <=128 regs so the 8 f64 chains of a chunk interleave
 #endif
 
 // Branch-free sqrt for x in (0, 64): MUFU.RSQ64H seed + Newton steps.  Not
@@ -380,6 +380,44 @@ __device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, const
   const double z = __dmul_rn(r, c);
   const double v = __dadd_rn(P.mean, __dmul_rn(P.stdv, z));
   return from_f64<DT>(v);
+}
+
+// A whole chunk of normals, phase by phase (all r, all c, then combine and
+// certify) so the 8 independent float64 chains interleave; one branch for the
+// rare uncertified elements.
+template <int DT, int NE>
+__device__ __forceinline__ void normal_chunk(const DistP& P, const NormalLut* L, const uint32_t (&w0)[NE],
+                                             const uint32_t (&w1)[NE], typename St<DT>::T (&out)[NE]) {
+  double r[NE], c[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) r[e] = r_fast(w0[e] >> 8, L);
+#pragma unroll
+  for (int e = 0; e < NE; ++e) c[e] = c_fast(w1[e] >> 8, L);
+  bool bad = false;
+  uint32_t badmask = 0;
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const double z = __dmul_rn(r[e], c[e]);
+    const double v = __dadd_rn(P.mean, __dmul_rn(P.stdv, z));
+    const double B = fma(r[e], P.nm.bound_r, fabs(v) * 0x1p-51) + 0x1p-1060;
+    const auto lo = from_f64<DT>(v - B), hi = from_f64<DT>(v + B);
+    bool ok;
+    if constexpr (DT == SDR_F32) ok = __float_as_uint(lo) == __float_as_uint(hi);
+    else ok = lo == hi;
+    out[e] = lo;
+    badmask |= ok ? 0u : (1u << e);
+  }
+  bad = badmask != 0;
+  if (__builtin_expect(bad, 0)) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      if (badmask & (1u << e)) {
+        atomicAdd(P.nm.fallbacks, 1ull);
+        const double rr = __ldg(P.nm.rtab + (w0[e] >> 8)), cc = __ldg(P.nm.ctab + (w1[e] >> 8));
+        out[e] = from_f64<DT>(__dadd_rn(P.mean, __dmul_rn(P.stdv, __dmul_rn(rr, cc))));
+      }
+    }
+  }
 }
 
 // Stage the Normal tables in shared memory (whole CTA participates).
@@ -505,8 +543,12 @@ __device__ __forceinline__ void fill_chunk(const FillArgs& A, const NormalLut* L
   if constexpr (ALIGNED) chunk_words_aligned<kV>(A.g, j0, w0, w1);
   else chunk_words<kV>(A.g, j0, w0, w1);
   T v[kV];
+  if constexpr (DIST == SDR_NORMAL && DT != SDR_F64) {
+    normal_chunk<DT, kV>(A.d, L, w0, w1, v);
+  } else {
 #pragma unroll
-  for (int e = 0; e < kV; ++e) v[e] = dist_value<DIST, DT>(A.d, L, w0[e], w1[e]);
+    for (int e = 0; e < kV; ++e) v[e] = dist_value<DIST, DT>(A.d, L, w0[e], w1[e]);
+  }
   store_chunk(static_cast<T*>(A.out) + q * kV, v);
 }
 
@@ -554,7 +596,7 @@ __global__ void __launch_bounds__(256) k_fill_generic(const __grid_constant__ Fi
 constexpr uint64_t kTileElems = 16384;
 
 template <int DIST, int DT>
-__global__ void __launch_bounds__(256) k_fill_batch(const FillArgs* __restrict__ descs,
+__global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_batch(const FillArgs* __restrict__ descs,
                                                     const uint64_t* __restrict__ tile_prefix,
                                                     int n, uint64_t ntiles) {
   __shared__ __align__(16) unsigned char smem[sizeof(FillArgs)];

@@ -137,3 +137,27 @@ def llama3_tp_specs(params: dict, mesh, tp_dim: int = 0) -> dict:
             pl[tp_dim] = Shard(0)
         specs[name] = ShardSpec(mesh, tuple(pl))
     return specs
+
+
+def materialize_module(module, init_fn, state: RngState, init_specs: dict | None = None, coord=None,
+                       *, device=None) -> dict:
+    """Deferred init of a torch.nn.Module built on the meta device (SURVEY
+    8(f).2; reference plan.parallelize -> model.materialize, plan.py:280-290,
+    model.py:121-132).  Parameters are taken in module.named_parameters() order
+    (registration order, the reference's definition order); init_fn(name, p)
+    returns the Distribution of each; init_specs maps name -> ShardSpec.  All
+    parameters are filled by ONE launch and replaced in the module by their
+    local shards (on `device`).  Returns {name: (global_shape, spec or None)}."""
+    import torch.nn as nn
+    table = {}
+    for name, p in module.named_parameters():
+        table[name] = Parameter(tuple(p.shape), init_fn(name, p), p.dtype, p.requires_grad)
+    locals_ = materialize(table, state, init_specs, coord, device=device)
+    owners = dict(module.named_modules())
+    meta = {}
+    for name, t in locals_.items():
+        mod_name, _, leaf = name.rpartition(".")
+        owner = owners[mod_name] if mod_name else module
+        owner._parameters[leaf] = nn.Parameter(t, requires_grad=table[name].requires_grad)
+        meta[name] = (table[name].shape, (init_specs or {}).get(name))
+    return meta

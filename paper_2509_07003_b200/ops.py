@@ -19,7 +19,7 @@ import math
 import torch
 
 from . import _lib, runtime as runtime_mod
-from .placement import ShardView, full_view
+from .placement import ShardView, full_view  # noqa: F401
 from .rng import RngState, dtype_code
 
 _DROP_TYPES = (torch.float32, torch.float64, torch.bfloat16, torch.float16)
@@ -179,3 +179,89 @@ def dtensor_dropout(x, p: float, state: RngState | None = None, ledger=None, *, 
     y = dropout_apply(x.local, p, state, x.view)
     state.advance(math.prod(x.shape))
     return DTensor(x.meta, y, x.coord)
+
+
+# ---------------------------------------------------------------------------
+# Host-buffer dropout: pipelined H2D -> fused kernel -> D2H.
+# ---------------------------------------------------------------------------
+_PIPE: dict = {}
+
+
+def _pipe_state(device, nbytes_in, nbytes_out, dtype_in, dtype_out, nbuf):
+    key = (device, dtype_in, dtype_out, nbuf)
+    st = _PIPE.get(key)
+    if st is None or st["cap_in"] < nbytes_in or st["cap_out"] < nbytes_out:
+        st = {"cap_in": nbytes_in, "cap_out": nbytes_out,
+              "xin": [torch.empty(nbytes_in, dtype=torch.uint8, device=device) for _ in range(nbuf)],
+              "yout": [torch.empty(nbytes_out, dtype=torch.uint8, device=device) for _ in range(nbuf)],
+              "h2d": torch.cuda.Stream(device), "comp": torch.cuda.Stream(device),
+              "d2h": torch.cuda.Stream(device)}
+        _PIPE[key] = st
+    return st
+
+
+def dropout_host(x_host: torch.Tensor, p: float, state: RngState, view: ShardView | None = None, *,
+                 out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None,
+                 device=None, chunks: int = 8) -> torch.Tensor:
+    """dropout_apply for a tensor in (pinned) HOST memory, result in host
+    memory.  The window is cut into `chunks` row blocks along its first dim;
+    block i's H2D copy, block i-1's fused kernel and block i-2's D2H copy run
+    concurrently on three streams (PCIe is full duplex), so the end-to-end
+    time approaches max(H2D, D2H) instead of their sum.  Values are identical
+    to dropout_apply (each block is a sub-window of the same global draw).
+    Does NOT advance `state`.  Blocks the host until the result is ready."""
+    from .placement import DimWindow
+    if x_host.is_cuda:
+        raise ValueError("dropout_host expects a host tensor; use dropout_apply for device tensors")
+    view = full_view(tuple(x_host.shape)) if view is None else view
+    if tuple(x_host.shape) != view.local_shape:
+        raise ValueError(f"x has shape {tuple(x_host.shape)}, window is {view.local_shape}")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    yd = x_host.dtype if out_dtype is None else out_dtype
+    if out is None:
+        out = torch.empty(x_host.shape, dtype=yd, pin_memory=True)
+    x_host = x_host.contiguous()
+    rows = x_host.shape[0] if x_host.dim() else 1
+    w0 = view.windows[0] if view.windows else None
+    if x_host.dim() == 0 or rows == 0 or w0.groups != 1:
+        chunks = 1
+    chunks = max(1, min(chunks, rows))
+    per = -(-rows // chunks)
+    row_in = x_host[0].numel() * x_host.element_size() if x_host.dim() else x_host.element_size()
+    row_out = row_in // x_host.element_size() * torch.empty((), dtype=yd).element_size()
+    nbuf = 3
+    S = _pipe_state(dev, per * row_in, per * row_out, x_host.dtype, yd, nbuf)
+    cur = torch.cuda.current_stream(dev)
+    h2d_done = [torch.cuda.Event() for _ in range(chunks)]
+    comp_done = [torch.cuda.Event() for _ in range(chunks)]
+    d2h_done = [None] * nbuf
+    for s in (S["h2d"], S["comp"], S["d2h"]):
+        s.wait_stream(cur)
+    for i in range(chunks):
+        r0, r1 = i * per, min(rows, (i + 1) * per)
+        if r0 >= r1:
+            break
+        b = i % nbuf
+        n_in, n_out = (r1 - r0) * row_in, (r1 - r0) * row_out
+        xin = S["xin"][b][:n_in].view(x_host.dtype).view((r1 - r0,) + tuple(x_host.shape[1:]))
+        yout = S["yout"][b][:n_out].view(yd).view(xin.shape)
+        with torch.cuda.stream(S["h2d"]):
+            if d2h_done[b] is not None:
+                S["h2d"].wait_event(d2h_done[b])  # buffer b free again
+            xin.copy_(x_host[r0:r1], non_blocking=True)
+            h2d_done[i].record(S["h2d"])
+        sub = ShardView(view.global_shape,
+                        windows=(DimWindow(w0.start + r0, r1 - r0),) + tuple(view.windows[1:]))
+        with torch.cuda.stream(S["comp"]):
+            S["comp"].wait_event(h2d_done[i])
+            dropout_apply(xin, p, state, sub, out=yout, out_dtype=yd)
+            comp_done[i].record(S["comp"])
+        with torch.cuda.stream(S["d2h"]):
+            S["d2h"].wait_event(comp_done[i])
+            out[r0:r1].copy_(yout, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(S["d2h"])
+            d2h_done[b] = ev
+    cur.wait_stream(S["d2h"])
+    torch.cuda.current_stream(dev).synchronize()
+    return out

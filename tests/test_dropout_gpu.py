@@ -140,3 +140,18 @@ def test_dtensor_dropout_world_one():
     ref = ops.dropout_apply(x, 0.2, R.RngState(9))
     assert torch.equal(bits(y.local), bits(ref))
     assert ops.dtensor_dropout(xd, 0.0, st) is xd and st.offset == 1
+
+
+@pytest.mark.parametrize("dt,out_dtype", [(torch.bfloat16, None), (torch.bfloat16, torch.float32),
+                                          (torch.float32, None)])
+def test_dropout_host_pipeline_matches_device(dt, out_dtype):
+    shape = (6, 37, 64)
+    mesh = S.create_mesh([("sp", 3)])
+    spec = ShardSpec(mesh, parse_placements("S(0)"))
+    v = local_shape_and_offset(spec, (18, 37, 64), (1,))
+    x = torch.randn(shape).to(dt).pin_memory()
+    st = R.RngState(77, 4)
+    for chunks in (1, 4, 6, 100):
+        yh = ops.dropout_host(x, 0.3, st, v, out_dtype=out_dtype, chunks=chunks)
+        yd = ops.dropout_apply(x.cuda(), 0.3, st, v, out_dtype=out_dtype)
+        assert not yh.is_cuda and torch.equal(bits(yh), bits(yd.cpu())), chunks

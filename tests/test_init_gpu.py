@@ -117,3 +117,25 @@ def test_cuda_pack_kernels_match_torch_layout():
         gpu.unpack_local(back, sg)
         for a, m in zip(back, mem_loc_g):
             assert torch.equal(a.tensor, m.tensor)
+
+
+def test_materialize_torch_module_on_meta_device():
+    import torch.nn as nn
+    with torch.device("meta"):
+        model = nn.Sequential(nn.Linear(64, 96, bias=True), nn.ReLU(), nn.Linear(96, 32, bias=False))
+    mesh = S.create_mesh([("tp", 4)])
+    specs = {"0.weight": ShardSpec(mesh, parse_placements("S(0)")),
+             "0.bias": ShardSpec(mesh, parse_placements("S(0)")),
+             "2.weight": ShardSpec(mesh, parse_placements("S(1)"))}
+    init_fn = lambda name, p: R.Normal(0.0, 1.0 / p.shape[-1] ** 0.5) if p.dim() == 2 else R.Uniform(-0.1, 0.1)
+    st = R.RngState(3)
+    meta = I.materialize_module(model, init_fn, st, specs, (2,))
+    ref_st = R.RngState(3)
+    for name, p in model.named_parameters():
+        shape, spec = meta[name]
+        v = local_shape_and_offset(spec, shape, (2,))
+        want = R.fill_random(v, ref_st, init_fn(name, torch.empty(shape, device="meta")), torch.float32)
+        ref_st.advance(int(np.prod(shape)))
+        assert p.is_cuda and torch.equal(bits(p.data), bits(want)), name
+    assert st.offset == ref_st.offset
+    assert model[0].weight.shape == (24, 64) and model[2].weight.shape == (32, 24)
