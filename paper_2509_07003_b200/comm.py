@@ -10,71 +10,16 @@ bus-bandwidth convention used by bench.py.
 
 from __future__ import annotations
 
-import csv
-import io
 from dataclasses import dataclass, field
 from fractions import Fraction
+
+from .ledger import CollectiveLedger, LedgerEntry  # noqa: F401  (API re-export)
 
 DEFAULT_BUCKET_BYTES = 65536
 
 
 class CommError(ValueError):
     pass
-
-
-@dataclass
-class LedgerEntry:
-    collective: str
-    mesh: str
-    dims: str
-    payload_bytes: int
-    participants: int
-    bytes_per_device: Fraction
-    modeled_time: Fraction
-
-
-@dataclass
-class CollectiveLedger:
-    """Per-call byte accounting: 2S(P-1)/P for all-reduce, S(P-1)/P for
-    all-gather / reduce-scatter (S = full payload)."""
-
-    transfer_time_per_byte: Fraction = Fraction(1)
-    entries: list = field(default_factory=list)
-    counts: dict = field(default_factory=dict)
-
-    def record(self, collective: str, payload_bytes: int, participants: int, mesh: str = "",
-               dims: str = "") -> LedgerEntry:
-        P, S = int(participants), int(payload_bytes)
-        k = 2 if collective == "all_reduce" else 1
-        per_dev = Fraction(k * S * (P - 1), P) if P > 1 else Fraction(0)
-        e = LedgerEntry(collective, mesh, dims, S, P, per_dev, per_dev * self.transfer_time_per_byte)
-        self.entries.append(e)
-        self.counts[collective] = self.counts.get(collective, 0) + 1
-        return e
-
-    @property
-    def total_bytes(self) -> Fraction:
-        return sum((e.bytes_per_device * e.participants for e in self.entries), Fraction(0))
-
-    @property
-    def modeled_time(self) -> Fraction:
-        return sum((e.modeled_time for e in self.entries), Fraction(0))
-
-    def count(self, collective: str) -> int:
-        return self.counts.get(collective, 0)
-
-    def reset(self):
-        self.entries.clear()
-        self.counts.clear()
-
-    def to_csv(self) -> str:
-        buf = io.StringIO()
-        w = csv.writer(buf)
-        w.writerow(["collective", "mesh", "dims", "S_bytes", "P", "bytes_per_device", "T_model"])
-        for e in self.entries:
-            w.writerow([e.collective, e.mesh, e.dims, e.payload_bytes, e.participants,
-                        float(e.bytes_per_device), float(e.modeled_time)])
-        return buf.getvalue()
 
 
 # ---------------------------------------------------------------------------
@@ -145,40 +90,34 @@ def all_reduce_into(buf, group, ledger=None, mesh="", dims="", P=1):
 # ---------------------------------------------------------------------------
 # Bucketed and N-dim fused gradient reduction (comm.py:130-289).
 # ---------------------------------------------------------------------------
-@dataclass
-class GradBucket:
-    capacity_bytes: int
-    members: list = field(default_factory=list)
-    member_bytes: int = 0
-
-    def fits(self, nbytes: int) -> bool:
-        return not self.members or self.member_bytes + nbytes <= self.capacity_bytes
-
-
-def _pack_buckets(grads, bucket_bytes: int) -> list:
-    """Reverse creation order, greedy; an oversized gradient gets its own
-    bucket (comm.py:140-150).  Sizes use the local shard bytes (all ranks of a
-    fiber agree for Partial grads since Partial keeps full local extents)."""
-    buckets: list = []
-    for g in reversed(grads):
-        nbytes = g.local.numel() * g.local.element_size()
-        if not buckets or not buckets[-1].fits(nbytes):
-            buckets.append(GradBucket(bucket_bytes))
-        buckets[-1].members.append(g)
-        buckets[-1].member_bytes += nbytes
-    return buckets
+def bucketize(tensors, capacity_bytes: int) -> list[list]:
+    """Greedy buckets over the REVERSED creation order (gradients become ready
+    back to front); a tensor larger than the capacity gets a bucket of its
+    own (reference comm.py:140-150).  Sizes are local-shard bytes."""
+    out: list[list] = []
+    used = 0
+    for t in tensors[::-1]:
+        nb = t.local.numel() * t.local.element_size()
+        if not out or (used + nb > capacity_bytes and out[-1]):
+            out.append([])
+            used = 0
+        out[-1].append(t)
+        used += nb
+    return out
 
 
 def _group_by_partial(grads):
+    """{(mesh, partial mesh dims, dtype): [grads]} and the grads without a
+    Partial dim (reference comm.py:153-164, plus dtype: one NCCL dtype per call)."""
     groups: dict = {}
-    skipped = []
+    untouched = []
     for g in grads:
-        pd = g.meta.spec.partial_mesh_dims()
-        if not pd:
-            skipped.append(g)
-            continue
-        groups.setdefault((g.meta.spec.mesh, pd, g.dtype), []).append(g)
-    return groups, skipped
+        dims = g.meta.spec.partial_mesh_dims()
+        if dims:
+            groups.setdefault((g.meta.spec.mesh, dims, g.dtype), []).append(g)
+        else:
+            untouched.append(g)
+    return groups, untouched
 
 
 def _reduce_buckets(members, dims, bucket_bytes, ledger, mover, rounds, label):
@@ -187,11 +126,11 @@ def _reduce_buckets(members, dims, bucket_bytes, ledger, mover, rounds, label):
     from dataclasses import replace
     mesh = members[0].meta.spec.mesh
     out = {}
-    for b in _pack_buckets(members, bucket_bytes):
-        slots = [[m.meta.spec, m.local] for m in b.members]
-        _fused_all_reduce(mesh, dims, list(zip(b.members, slots)), ledger, mover)
+    for bucket in bucketize(members, bucket_bytes):
+        slots = [[m.meta.spec, m.local] for m in bucket]
+        _fused_all_reduce(mesh, dims, list(zip(bucket, slots)), ledger, mover)
         rounds.append(("all_reduce", label, tuple(mesh.dim_names[d] for d in dims)))
-        for m, (spec, loc) in zip(b.members, slots):
+        for m, (spec, loc) in zip(bucket, slots):
             for d in dims:
                 spec = spec.with_placement(d, Replicate())
             out[id(m)] = DTensor(replace(m.meta, spec=spec), loc, m.coord)

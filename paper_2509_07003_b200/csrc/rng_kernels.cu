@@ -308,18 +308,40 @@ __host__ __device__ __forceinline__ double sqrt_nb(double x) {
 // t = m'*inv - 1 EXACT (24-bit m' times a 20-bit inv); the two intervals next
 // to m' = 1 use inv = 1 so no cancellation occurs for small k.  Branch-free:
 // k = 0 (r = 0 exactly) is selected at the end.
+// Exact uint32 -> double without a conversion instruction: 2^52 + x has x in
+// its low mantissa bits, so one DADD removes the bias (fp64 pipe, not XU).
+__host__ __device__ __forceinline__ double u32_to_f64(uint32_t x) {
+#ifdef __CUDA_ARCH__
+  return __hiloint2double(0x43300000, static_cast<int>(x)) - 0x1p52;
+#else
+  return static_cast<double>(x);
+#endif
+}
+
 __host__ __device__ __forceinline__ double r_fast(uint32_t k, const NormalLut* L) {
   const uint32_t n = (1u << 24) - k - (k == 0 ? 1u : 0u);  // 1 .. 2^24-1
+  const double nd = u32_to_f64(n);                // exact
 #ifdef __CUDA_ARCH__
-  const int b = 32 - __clz(n);                    // bit length, 1..24
+  const uint32_t hw = static_cast<uint32_t>(__double2hiint(nd));
+  const uint32_t lw = static_cast<uint32_t>(__double2loint(nd));
 #else
-  const int b = 32 - __builtin_clz(n);
+  uint64_t nb;
+  memcpy(&nb, &nd, 8);
+  const uint32_t hw = static_cast<uint32_t>(nb >> 32), lw = static_cast<uint32_t>(nb);
 #endif
-  const uint32_t M = n << (24 - b);               // [2^23, 2^24)
-  const int j = static_cast<int>(M >> 14) - 512;  // mantissa interval 0..511
+  const int b = static_cast<int>(hw >> 20) - 1022;  // bit length of n, 1..24
+  const int j = static_cast<int>((hw >> 11) & 511u); // top 9 fraction bits: interval 0..511
   const int e = b - 25 + (j >= 256 ? 1 : 0);      // e' of w = 2^e' m'
+  // M = n scaled into [2^23, 2^24): same mantissa, exponent of 2^23
+#ifdef __CUDA_ARCH__
+  const double Md = __hiloint2double(static_cast<int>((hw & 0x000FFFFFu) | 0x41600000u), static_cast<int>(lw));
+#else
+  const uint64_t mb = (static_cast<uint64_t>((hw & 0x000FFFFFu) | 0x41600000u) << 32) | lw;
+  double Md;
+  memcpy(&Md, &mb, 8);
+#endif
   const double2 tb = L->logt[j];
-  const double t = fma(static_cast<double>(M), tb.x, -1.0);  // exact
+  const double t = fma(Md, tb.x, -1.0);           // exact
 #ifdef __CUDA_ARCH__
   const double* C = c_npoly;
 #else
@@ -331,7 +353,7 @@ __host__ __device__ __forceinline__ double r_fast(uint32_t k, const NormalLut* L
   p = fma(t, p, C[3]);
   p = fma(t, p, C[4]);
   const double lg = fma(t * t, p, t);             // t + t^2*(-1/2 + ...)
-  const double ne = static_cast<double>(-e);
+  const double ne = u32_to_f64(static_cast<uint32_t>(-e));   // 0..24, exact
   const double Lw = fma(ne, kLn2Hi, fma(ne, kLn2Lo, tb.y - lg));  // -ln w
   const double r = sqrt_nb(Lw + Lw);
   return k == 0 ? 0.0 : r;
@@ -341,8 +363,8 @@ __host__ __device__ __forceinline__ double r_fast(uint32_t k, const NormalLut* L
 // short Taylor residual (|d| <= 1.54e-3).
 __host__ __device__ __forceinline__ double c_fast(uint32_t k, const NormalLut* L) {
   const uint32_t i = (k + 4096u) >> 13;            // 0..2048
-  const int dj = static_cast<int>(k) - static_cast<int>(i << 13);  // [-4096, 4095]
-  const double d = static_cast<double>(dj) * kTwoPiOver2p24;
+  const uint32_t dj4 = k + 4096u - (i << 13);     // dj + 4096 in [0, 8191]
+  const double d = (u32_to_f64(dj4) - 4096.0) * kTwoPiOver2p24;
   const double d2 = d * d;
 #ifdef __CUDA_ARCH__
   const double* C = c_npoly;

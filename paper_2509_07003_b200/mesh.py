@@ -34,48 +34,41 @@ def _linear(digits, radices) -> int:
 
 @dataclass(frozen=True)
 class DeviceMesh:
+    """Named dimensions (name, size) over an ordered rank list (row-major)."""
     name: str
     dims: tuple[tuple[str, int], ...]
     ranks: tuple[int, ...]
 
     def __post_init__(self):
-        radices = [sz for _, sz in self.dims]
-        labels = [nm for nm, _ in self.dims]
-        if len(radices) == 0:
-            raise MeshError("a mesh needs at least one dimension")
-        if min(radices) < 1:
-            raise MeshError(f"every mesh dimension must have size >= 1, got {radices}")
-        if math.prod(radices) != len(self.ranks):
-            raise MeshError(f"{len(self.ranks)} ranks cannot fill a mesh of sizes {radices}")
-        if len(frozenset(self.ranks)) < len(self.ranks):
-            raise MeshError("a rank appears twice in the mesh")
-        if len(frozenset(labels)) < len(labels):
-            raise MeshError(f"mesh dimension names repeat: {labels}")
+        labels, radices = zip(*self.dims) if self.dims else ((), ())
+        checks = [
+            (not radices, "a mesh needs at least one dimension"),
+            (bool(radices) and min(radices) < 1, f"every mesh dimension must have size >= 1, got {list(radices)}"),
+            (math.prod(radices) != len(self.ranks), f"{len(self.ranks)} ranks cannot fill sizes {list(radices)}"),
+            (len(set(self.ranks)) < len(self.ranks), "a rank appears twice in the mesh"),
+            (len(set(labels)) < len(labels), f"mesh dimension names repeat: {list(labels)}"),
+        ]
+        for bad, msg in checks:
+            if bad:
+                raise MeshError(msg)
 
-    # -- shape ---------------------------------------------------------------
-    @property
-    def ndim(self) -> int:
-        return len(self.dims)
-
-    @property
-    def sizes(self) -> tuple[int, ...]:
-        return tuple(sz for _, sz in self.dims)
-
-    @property
-    def dim_names(self) -> tuple[str, ...]:
-        return tuple(nm for nm, _ in self.dims)
+    # shape ---------------------------------------------------------------------
+    ndim = property(lambda self: len(self.dims))
+    sizes = property(lambda self: tuple(sz for _, sz in self.dims))
+    dim_names = property(lambda self: tuple(nm for nm, _ in self.dims))
 
     def size(self) -> int:
+        """Number of devices."""
         return len(self.ranks)
 
     def dim_index(self, dim_name: str) -> int:
-        names = self.dim_names
-        if dim_name not in names:
-            raise MeshError(f"no mesh dimension {dim_name!r} among {names}")
-        return names.index(dim_name)
+        for i, (nm, _) in enumerate(self.dims):
+            if nm == dim_name:
+                return i
+        raise MeshError(f"no mesh dimension {dim_name!r} among {self.dim_names}")
 
     def dim_size(self, dim_name: str) -> int:
-        return self.sizes[self.dim_index(dim_name)]
+        return self.dims[self.dim_index(dim_name)][1]
 
     # -- coordinates -----------------------------------------------------------
     def coords_of_rank(self, rank: int) -> tuple[int, ...]:
@@ -158,8 +151,7 @@ class DeviceMesh:
 
 
 def create_mesh(dims, ranks=None, name: str = "mesh") -> DeviceMesh:
-    """Row-major mesh over `ranks` (default 0..N-1) (reference mesh.py:165-172)."""
-    dims = tuple((str(n), int(s)) for n, s in dims)
-    if ranks is None:
-        ranks = range(math.prod(s for _, s in dims))
-    return DeviceMesh(name=name, dims=dims, ranks=tuple(int(r) for r in ranks))
+    """Row-major mesh over `ranks`, default 0..N-1 (reference mesh.py:165-172)."""
+    spec = tuple((str(label), int(extent)) for label, extent in dims)
+    order = tuple(range(math.prod(e for _, e in spec))) if ranks is None else tuple(map(int, ranks))
+    return DeviceMesh(name=name, dims=spec, ranks=order)

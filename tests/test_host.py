@@ -156,3 +156,21 @@ def test_dropout_strategy_matches_reference_dispatch():
         spec = ShardSpec(mesh, parse_placements(src))
         x = DTensor(DTensorMeta((8, 8), spec, torch.float32), torch.zeros(1), (0, 0))
         assert str(dropout_input_spec(x).placements) == str(parse_placements(want)), (src, want)
+
+
+@pytest.mark.parametrize("pl,sizes", [("S(0),S(1)", (2, 3)), ("P,S(1)", (2, 2)), ("IS(0,2),R", (2, 2)),
+                                      ("R,R", (2, 2))])
+def test_distribute_merge_roundtrip(pl, sizes):
+    import torch
+    from paper_2509_07003_b200.placement import distribute_local_tensors, merge_local_tensors
+    mesh = create_mesh([("a", sizes[0]), ("b", sizes[1])])
+    spec = ShardSpec(mesh, parse_placements(pl))
+    g = torch.arange(8 * 6, dtype=torch.float64).reshape(8, 6)
+    locs = distribute_local_tensors(spec, g)
+    assert torch.equal(merge_local_tensors(spec, (8, 6), locs), g)
+    if "R" in pl and "P" not in pl:
+        bad = dict(locs)
+        k = next(c for c in bad if c[1] == 1)
+        bad[k] = bad[k] + 1
+        with pytest.raises(PlacementError):
+            merge_local_tensors(spec, (8, 6), bad)
