@@ -301,6 +301,14 @@ def run_ours(a):
     achieved_tops = n_local / (ms_local * 1e-3) * PHILOX_OPS / 1e12
     achieved_gbs_local = local_bytes / (ms_local * 1e-3) / 1e9
 
+    traffic = None
+    try:  # dram bytes of this kernel from the committed ncu capture (profiles/)
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f)["k_dropout_fast"]
+        traffic = (tr["dram_bytes_read"] + tr["dram_bytes_write"]) * (n_local / math.prod(SHAPE))
+    except (OSError, KeyError, ValueError):
+        pass
+
     line = None
     if rank == 0:
         cpu = None
@@ -326,7 +334,8 @@ def run_ours(a):
             "roofline": {
                 "bound": "int32", "achieved": round(achieved_tops, 3), "peak": round(int_peak_tops, 3),
                 "unit": "TOP/s INT32 (80 per Philox block)", "frac": round(achieved_tops / int_peak_tops, 4),
-                "traffic": None,
+                "traffic": traffic, "traffic_note": "dram read+write bytes per launch, ncu (profiles/traffic.json); "
+                                                    "algorithmic bytes per launch = %d" % local_bytes,
                 "int32_probe": {"imad_wide_per_s": imad.value, "lop3_per_s": lop3.value,
                                 "philox_blocks_per_s_no_hoist": phx.value,
                                 "how": "sdr_probe_int32 live: peak = 80 x philox_blocks_per_s_no_hoist"},

@@ -278,6 +278,9 @@ __constant__ double c_npoly[8] = {
 #ifndef SDR_SQRT_NEWTON
 #define SDR_SQRT_NEWTON 1   // Newton steps on the MUFU.RSQ64H seed before the final correction
 #endif
+#ifndef SDR_NORMAL_SPLIT
+#define SDR_NORMAL_SPLIT 1  // float64 phases of a chunk in SPLIT passes (register pressure)
+#endif
 #ifndef SDR_FILL_MINB
 #define SDR_FILL_MINB 2   // 2 CTAs/SM: <=128 regs so the 8 f64 chains of a chunk interleave
 #endif
@@ -408,8 +411,8 @@ __device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, const
 // certify) so the 8 independent float64 chains interleave; one branch for the
 // rare uncertified elements.
 template <int DT, int NE>
-__device__ __forceinline__ void normal_chunk(const DistP& P, const NormalLut* L, const uint32_t (&w0)[NE],
-                                             const uint32_t (&w1)[NE], typename St<DT>::T (&out)[NE]) {
+__device__ __forceinline__ void normal_chunk(const DistP& P, const NormalLut* L, const uint32_t* w0,
+                                             const uint32_t* w1, typename St<DT>::T* out) {
   double r[NE], c[NE];
 #pragma unroll
   for (int e = 0; e < NE; ++e) r[e] = r_fast(w0[e] >> 8, L);
@@ -566,7 +569,10 @@ __device__ __forceinline__ void fill_chunk(const FillArgs& A, const NormalLut* L
   else chunk_words<kV>(A.g, j0, w0, w1);
   T v[kV];
   if constexpr (DIST == SDR_NORMAL && DT != SDR_F64) {
-    normal_chunk<DT, kV>(A.d, L, w0, w1, v);
+    constexpr int NS = SDR_NORMAL_SPLIT;
+#pragma unroll
+    for (int h = 0; h < NS; ++h)
+      normal_chunk<DT, kV / NS>(A.d, L, w0 + h * (kV / NS), w1 + h * (kV / NS), v + h * (kV / NS));
   } else {
 #pragma unroll
     for (int e = 0; e < kV; ++e) v[e] = dist_value<DIST, DT>(A.d, L, w0[e], w1[e]);
