@@ -64,10 +64,15 @@ def dropout_apply(x: torch.Tensor, p: float, state: RngState, view: ShardView | 
     if x.numel() == 0:
         return out
     nr, nv = state.native(), view.to_native()
-    with torch.cuda.device(x.device):
+    if x.device.index == torch.cuda.current_device():
         st = _lib.LIB.sdr_dropout(x.data_ptr(), dtype_code(x.dtype), out.data_ptr(), dtype_code(yd),
                                   None if mask is None else mask.data_ptr(), mcode, float(p),
                                   C.byref(nr), C.byref(nv), _lib.stream_handle(x.device))
+    else:
+        with torch.cuda.device(x.device):
+            st = _lib.LIB.sdr_dropout(x.data_ptr(), dtype_code(x.dtype), out.data_ptr(), dtype_code(yd),
+                                      None if mask is None else mask.data_ptr(), mcode, float(p),
+                                      C.byref(nr), C.byref(nv), _lib.stream_handle(x.device))
     _lib.check(st, "sdr_dropout", _check_p)
     return out
 
