@@ -33,16 +33,15 @@ struct CopyJob {
 
 constexpr int64_t kTileBytes = 32768;
 
+// Tiles never cross a span: tile t of a job is part (t % tiles_per_span) of
+// span (t / tiles_per_span), so the inner loop is a plain strided vector copy.
 template <typename V>
-__device__ __forceinline__ void copy_range(const CopyJob& J, int64_t b0, int64_t b1) {
-  // Byte range [b0, b1) of the job's logical (span-major) stream, V-aligned.
-  const int64_t w = sizeof(V);
-  for (int64_t b = b0 + static_cast<int64_t>(threadIdx.x) * w; b < b1;
-       b += static_cast<int64_t>(blockDim.x) * w) {
-    const int64_t sp = b / J.span_bytes, off = b - sp * J.span_bytes;
-    const V v = *reinterpret_cast<const V*>(J.src + sp * J.src_stride + off);
-    *reinterpret_cast<V*>(J.dst + sp * J.dst_stride + off) = v;
-  }
+__device__ __forceinline__ void copy_part(const unsigned char* __restrict__ src,
+                                          unsigned char* __restrict__ dst, int64_t nbytes) {
+  const int64_t n = nbytes / static_cast<int64_t>(sizeof(V));
+  const V* s = reinterpret_cast<const V*>(src);
+  V* d = reinterpret_cast<V*>(dst);
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) d[i] = s[i];
 }
 
 __global__ void __launch_bounds__(256) k_copy_jobs(const CopyJob* __restrict__ jobs,
@@ -55,15 +54,19 @@ __global__ void __launch_bounds__(256) k_copy_jobs(const CopyJob* __restrict__ j
       if (prefix[mid] <= t) lo = mid;
       else hi = mid - 1;
     }
-    const CopyJob J = jobs[lo];
-    const int64_t total = J.nspans * J.span_bytes;
-    const int64_t b0 = (t - prefix[lo]) * kTileBytes;
-    const int64_t b1 = b0 + kTileBytes < total ? b0 + kTileBytes : total;
+    const CopyJob& J = jobs[lo];
+    const int64_t tps = (J.span_bytes + kTileBytes - 1) / kTileBytes;  // tiles per span
+    const int64_t lt = t - prefix[lo];
+    const int64_t span = lt / tps, part = lt - span * tps;
+    const int64_t off = part * kTileBytes;
+    const int64_t len = min(kTileBytes, J.span_bytes - off);
+    const unsigned char* src = J.src + span * J.src_stride + off;
+    unsigned char* dst = J.dst + span * J.dst_stride + off;
     switch (J.vec) {
-      case 16: copy_range<uint4>(J, b0, b1); break;
-      case 8: copy_range<uint2>(J, b0, b1); break;
-      case 4: copy_range<uint32_t>(J, b0, b1); break;
-      default: copy_range<unsigned char>(J, b0, b1); break;
+      case 16: copy_part<uint4>(src, dst, len); break;
+      case 8: copy_part<uint2>(src, dst, len); break;
+      case 4: copy_part<uint32_t>(src, dst, len); break;
+      default: copy_part<unsigned char>(src, dst, len); break;
     }
   }
 }
@@ -88,7 +91,7 @@ static void add_job(std::vector<CopyJob>& jobs, const void* src, void* dst, int6
   J.span_bytes = span_bytes;
   J.src_stride = src_stride;
   J.dst_stride = dst_stride;
-  J.tiles = (nspans * span_bytes + kTileBytes - 1) / kTileBytes;
+  J.tiles = nspans * ((span_bytes + kTileBytes - 1) / kTileBytes);
   J.vec = widest({static_cast<int64_t>(reinterpret_cast<uintptr_t>(src)),
                   static_cast<int64_t>(reinterpret_cast<uintptr_t>(dst)), span_bytes, src_stride,
                   dst_stride});

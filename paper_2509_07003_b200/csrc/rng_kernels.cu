@@ -745,6 +745,14 @@ __device__ __noinline__ typename St<YT>::T drop_nan_fix(typename St<XT>::T x) {
   }
 }
 
+// Full-block keep decision for the rare w1 tie (kept out of line so the hot
+// loop stays compact).
+__device__ __noinline__ bool keep_full(const Gen& g, uint64_t j, uint64_t keep_le) {
+  uint32_t f0, f1;
+  elem_words(g, j, f0, f1);
+  return ((static_cast<uint64_t>(f1) << 32) | f0) <= keep_le;
+}
+
 #ifndef SDR_DROP_MINB
 #define SDR_DROP_MINB 4
 #endif
@@ -800,19 +808,26 @@ __global__ void __launch_bounds__(256, SDR_DROP_MINB) k_dropout_fast(const __gri
       } else {
         chunk_words<NE>(A.g, j0 + h * NE, w0, w1);
       }
+      if constexpr (ALIGNED) {
+        // (w1:w0) <= keep_le is decided by w1 unless w1 equals its high word
+        // (p = 2^-32 per element): one rare branch per chunk, not per element.
+        const uint32_t H = hi32(A.keep_le);
+        bool tie = false;
+#pragma unroll
+        for (int i = 0; i < NE; ++i) {
+          keep[h * NE + i] = w1[i] < H;
+          tie |= w1[i] == H;
+        }
+        if (__builtin_expect(tie, 0)) {
+#pragma unroll
+          for (int i = 0; i < NE; ++i)
+            if (w1[i] == H) keep[h * NE + i] = keep_full(A.g, j0 + h * NE + i, A.keep_le);
+        }
+      }
 #pragma unroll
       for (int i = 0; i < NE; ++i) {
         const int e = h * NE + i;
-        if constexpr (ALIGNED) {
-          // (w1:w0) <= keep_le is decided by w1 unless w1 equals its high word
-          const uint32_t H = hi32(A.keep_le);
-          keep[e] = w1[i] < H;
-          if (__builtin_expect(w1[i] == H, 0)) {
-            uint32_t f0, f1;
-            elem_words(A.g, j0 + h * NE + i, f0, f1);
-            keep[e] = ((static_cast<uint64_t>(f1) << 32) | f0) <= A.keep_le;
-          }
-        } else {
+        if constexpr (!ALIGNED) {
           const uint64_t u64 = (static_cast<uint64_t>(w1[i]) << 32) | w0[i];
           keep[e] = u64 <= A.keep_le;
         }

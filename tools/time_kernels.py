@@ -86,3 +86,32 @@ for tp in (8, 1):
         p.value = None
     del params
     torch.cuda.empty_cache()
+# cfg5 pack / unpack (HBM-bound copies around the coalesced NCCL call):
+# one LLaMA-3-8B layer's 9 bf16 tensors on DP=2 (rank 0 shards), packed
+# rank-major for a reduce-scatter and unpacked after an all-gather.
+from paper_2509_07003_b200.movers import CudaMover, Member, layout
+d, ff, kv = 4096, 14336, 1024
+shapes = [((d, d), 1), ((kv, d), 1), ((kv, d), 1), ((d, d), 0), ((ff, d), 1), ((ff, d), 1), ((d, ff), 0),
+          ((d,), 0), ((d,), 0)]
+P = 2
+fulls, full_m, loc_m = [], [], []
+for shp, dim in shapes:
+    f = torch.randn(shp, device="cuda", dtype=torch.bfloat16)
+    outer, inner, rows = int(np.prod(shp[:dim])), int(np.prod(shp[dim + 1:])), shp[dim]
+    chunk = -(-rows // P)
+    full_m.append(Member(f, outer, rows, inner, chunk))
+    loc = f.narrow(dim, 0, chunk).contiguous()
+    loc_m.append(Member(loc, outer, chunk, inner, chunk))
+seg = layout(full_m)
+for a, b in zip(loc_m, full_m):
+    a.seg_off = b.seg_off
+mv = CudaMover()
+packed = torch.empty(seg * P, dtype=torch.uint8, device="cuda")
+nbytes = sum(m.tensor.numel() * 2 for m in full_m)
+line("cfg5 pack_scatter (9 tensors, P=2)", timeit(lambda: mv.pack_scatter(full_m, packed, seg, P)), nbytes // 2,
+     2 * nbytes)
+line("cfg5 unpack_gathered (9 tensors, P=2)", timeit(lambda: mv.unpack_gathered(full_m, packed, seg, P)),
+     nbytes // 2, 2 * nbytes)
+segbuf = torch.empty(seg, dtype=torch.uint8, device="cuda")
+line("cfg5 pack_local (9 shards)", timeit(lambda: mv.pack_local(loc_m, segbuf)), nbytes // 4, nbytes)
+print("(pack rows: 'G elem/s' column = bf16 elements moved; GB/s = read + write bytes; HBM peak 6552 GB/s)")
