@@ -145,20 +145,12 @@ __device__ __forceinline__ void chunk_words_aligned(const Gen& g, uint64_t j0, u
 // just hi(M0*x0) of round 9 and lo(M1*x2) of round 10.  Same preconditions as
 // chunk_words_aligned.  A tie on the high threshold word (p = 2^-32) is
 // resolved by the caller with the full block.
+// Per-element part of the w1-only Philox given the chunk-uniform round-1/2
+// values (bhi, y3, hq, z1) and the 64-bit M1*tau of the chunk's first element.
 template <int NE>
-__device__ __forceinline__ void chunk_w1_aligned(const Gen& g, uint64_t j0, uint32_t (&w1)[NE]) {
-  const uint32_t sh = g.div_theta.s;
-  const uint64_t beta = (j0 >> sh) + g.offset;
-  const uint64_t t = j0 & (g.theta - 1);
-  const RoundKeys& K = g.keys;
+__device__ __forceinline__ void w1_body(const RoundKeys& K, uint32_t bhi, uint32_t y3, uint32_t hq,
+                                        uint32_t z1, uint64_t pb0, uint32_t (&w1)[NE]) {
   uint32_t x0[NE], x1[NE], x2[NE], x3[NE];
-  const uint32_t blo = lo32(beta), bhi = hi32(beta), tlo = lo32(t), thi = hi32(t);
-  const uint64_t pa = mul_wide(blo, kM0);
-  const uint32_t y2 = hi32(pa) ^ thi ^ K.k1[0];
-  const uint32_t y3 = lo32(pa);
-  const uint64_t pb0 = mul_wide(tlo, kM1);
-  const uint64_t pq = mul_wide(y2, kM1);
-  const uint32_t z1 = lo32(pq), hq = hi32(pq);
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
     const uint64_t pb = pb0 + static_cast<uint64_t>(e) * kM1;
@@ -180,6 +172,30 @@ __device__ __forceinline__ void chunk_w1_aligned(const Gen& g, uint64_t j0, uint
     const uint32_t x2_9 = __umulhi(x0[e], kM0) ^ x3[e] ^ K.k1[8];  // round 9: x2 only
     w1[e] = x2_9 * kM1;                                              // round 10: lo(M1*x2)
   }
+}
+
+// Chunk-uniform round-1/2 values for counter (beta, tau0).
+struct Hoist {
+  uint32_t bhi, y3, hq, z1;
+};
+__device__ __forceinline__ Hoist hoist_beta(const RoundKeys& K, uint64_t beta, uint32_t thi) {
+  const uint64_t pa = mul_wide(lo32(beta), kM0);
+  const uint32_t y2 = hi32(pa) ^ thi ^ K.k1[0];
+  const uint64_t pq = mul_wide(y2, kM1);
+  return Hoist{hi32(beta), lo32(pa), hi32(pq), lo32(pq)};
+}
+
+// Word 1 only, for a keep/drop decision (dropout): the last two rounds need
+// just hi(M0*x0) of round 9 and lo(M1*x2) of round 10.  Same preconditions as
+// chunk_words_aligned.  A tie on the high threshold word (p = 2^-32) is
+// resolved by the caller with the full block.
+template <int NE>
+__device__ __forceinline__ void chunk_w1_aligned(const Gen& g, uint64_t j0, uint32_t (&w1)[NE]) {
+  const uint32_t sh = g.div_theta.s;
+  const uint64_t beta = (j0 >> sh) + g.offset;
+  const uint64_t t = j0 & (g.theta - 1);
+  const Hoist H = hoist_beta(g.keys, beta, hi32(t));
+  w1_body<NE>(g.keys, H.bhi, H.y3, H.hq, H.z1, mul_wide(lo32(t), kM1), w1);
 }
 
 // Words of one element at global index j (generic path).
@@ -251,6 +267,9 @@ struct NormalMirror {
   double err_r;         // max |r_fast - r_np| / r_fast over all k (exhaustive)
   double err_c;         // max |c_fast - c_np| over all k (exhaustive)
   double bound_r;       // certification bound B = r*bound_r + |v|*2^-51 (+tiny)
+  // float32 fast path (bfloat16 outputs): calibrated errors and bound terms
+  double err_r32, err_c32;
+  float mean32, std32, b32_r, b32_c;  // B32 = r*b32_r + |v|*2^-22 + b32_c
   unsigned long long* fallbacks;
 };
 
@@ -277,6 +296,9 @@ __constant__ double c_npoly[8] = {
 
 #ifndef SDR_SQRT_NEWTON
 #define SDR_SQRT_NEWTON 1   // Newton steps on the MUFU.RSQ64H seed before the final correction
+#endif
+#ifndef SDR_NORMAL_BF16_F32
+#define SDR_NORMAL_BF16_F32 1  // certified float32 Box-Muller for bfloat16 outputs
 #endif
 #ifndef SDR_NORMAL_SPLIT
 #define SDR_NORMAL_SPLIT 1  // float64 phases of a chunk in SPLIT passes (register pressure)
@@ -378,6 +400,66 @@ __host__ __device__ __forceinline__ double c_fast(uint32_t k, const NormalLut* L
   const double sd = fma(d * d2, fma(d2, C[6], C[7]), d);        // sin d
   const double2 cs = L->trig[i];
   return cs.x + fma(cs.x, cm, -cs.y * sd);
+}
+
+// float32 fast functions for the bfloat16 path (errors calibrated exhaustively
+// against the NumPy tables like the float64 ones).
+__host__ __device__ __forceinline__ float r32_fast(uint32_t k) {
+  const float u = static_cast<float>(k) * 0x1p-24f;     // exact
+  const float w = 1.0f - u;                             // exact (24-bit)
+  // -log1p(-u): series for u < 1/16, else -ln(w) from log2
+  const float ser = u * fmaf(u, fmaf(u, fmaf(u, fmaf(u, 0.2f, 0.25f), 1.0f / 3.0f), 0.5f), 1.0f);
+#ifdef __CUDA_ARCH__
+  const float lg = -__log2f(w) * 0.69314718055994530942f;
+#else
+  const float lg = -std::log2(w) * 0.69314718055994530942f;
+#endif
+  const float L = u < 0.0625f ? ser : lg;
+  const float x = L + L;
+#ifdef __CUDA_ARCH__
+  const float r = x * rsqrtf(x);
+#else
+  const float r = std::sqrt(x);
+#endif
+  return k == 0 ? 0.0f : r;
+}
+
+__host__ __device__ __forceinline__ float c32_fast(uint32_t k) {
+  const float h = static_cast<float>(k) * 0x1p-23f;     // 2u, exact
+#ifdef __CUDA_ARCH__
+  return cospif(h);
+#else
+  return static_cast<float>(std::cos(3.141592653589793 * static_cast<double>(h)));
+#endif
+}
+
+// bfloat16 normals of a chunk through float32, certified against the float64
+// NumPy value with a directed-rounding enclosure; the rare uncertified
+// elements recompute exactly from the tables.
+template <int NE>
+__device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const uint32_t* w0, const uint32_t* w1,
+                                                  uint16_t* out) {
+  uint32_t badmask = 0;
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const float r = r32_fast(w0[e] >> 8), c = c32_fast(w1[e] >> 8);
+    const float z = __fmul_rn(r, c);
+    const float v = __fmaf_rn(P.nm.std32, z, P.nm.mean32);
+    const float B = fmaf(r, P.nm.b32_r, fmaf(fabsf(v), 0x1p-22f, P.nm.b32_c));
+    const uint16_t lo = bf16_bits(__fsub_rd(v, B)), hi = bf16_bits(__fadd_ru(v, B));
+    out[e] = lo;
+    badmask |= (lo == hi) ? 0u : (1u << e);
+  }
+  if (__builtin_expect(badmask != 0, 0)) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      if (badmask & (1u << e)) {
+        atomicAdd(P.nm.fallbacks, 1ull);
+        const double rr = __ldg(P.nm.rtab + (w0[e] >> 8)), cc = __ldg(P.nm.ctab + (w1[e] >> 8));
+        out[e] = from_f64<SDR_BF16>(__dadd_rn(P.mean, __dmul_rn(P.stdv, __dmul_rn(rr, cc))));
+      }
+    }
+  }
 }
 
 // Normal (rng.py:150-156): float64 Box-Muller then one cast.  Fast path with
@@ -568,7 +650,9 @@ __device__ __forceinline__ void fill_chunk(const FillArgs& A, const NormalLut* L
   if constexpr (ALIGNED) chunk_words_aligned<kV>(A.g, j0, w0, w1);
   else chunk_words<kV>(A.g, j0, w0, w1);
   T v[kV];
-  if constexpr (DIST == SDR_NORMAL && DT != SDR_F64) {
+  if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
+    normal_chunk_bf16<kV>(A.d, w0, w1, v);
+  } else if constexpr (DIST == SDR_NORMAL && DT != SDR_F64) {
     constexpr int NS = SDR_NORMAL_SPLIT;
 #pragma unroll
     for (int h = 0; h < NS; ++h)
@@ -745,14 +829,6 @@ __device__ __noinline__ typename St<YT>::T drop_nan_fix(typename St<XT>::T x) {
   }
 }
 
-// Full-block keep decision for the rare w1 tie (kept out of line so the hot
-// loop stays compact).
-__device__ __noinline__ bool keep_full(const Gen& g, uint64_t j, uint64_t keep_le) {
-  uint32_t f0, f1;
-  elem_words(g, j, f0, f1);
-  return ((static_cast<uint64_t>(f1) << 32) | f0) <= keep_le;
-}
-
 #ifndef SDR_DROP_MINB
 #define SDR_DROP_MINB 4
 #endif
@@ -784,6 +860,47 @@ __device__ __forceinline__ uint64_t drop_chunk_base(const DropArgs& A, uint64_t 
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(__byte_perm(w, 0u, 0x1044)); }
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
+// y = (x*m)*scale for one chunk given its keep flags; NaN fix-up; stores y
+// (and the mask when requested).
+template <int XT, int YT, int MT, int CH>
+__device__ __forceinline__ void drop_store(const DropArgs& A, uint64_t q,
+                                           const typename St<XT>::T (&xv)[CH], const bool (&keep)[CH]) {
+  using XTy = typename St<XT>::T;
+  using YTy = typename St<YT>::T;
+  YTy yv[CH];
+  bool anynan = false, nan[CH];
+#pragma unroll
+  for (int e = 0; e < CH; ++e) {
+    if constexpr (XT == SDR_BF16) {
+      uint32_t wd;
+      memcpy(&wd, &xv[e & ~1], 4);
+      const float xf = (e & 1) ? bf16_hi(wd) : bf16_lo(wd);
+      const float r = __fmul_rn(__fmul_rn(xf, keep[e] ? 1.0f : 0.0f), A.scale32);
+      nan[e] = r != r;
+      if constexpr (YT == SDR_F32) yv[e] = r;
+      else yv[e] = bf16_bits(r);
+    } else {
+      yv[e] = drop_apply<XT, YT>(A, xv[e], keep[e], nan[e]);
+    }
+    anynan |= nan[e];
+  }
+  if (anynan) {
+#pragma unroll
+    for (int e = 0; e < CH; ++e)
+      if (nan[e]) yv[e] = drop_nan_fix<XT, YT>(xv[e]);
+  }
+  store_chunk(static_cast<YTy*>(A.y) + q * CH, yv);
+  if constexpr (MT >= 0) {
+    using MTy = typename St<MT>::T;
+    if (A.mask != nullptr) {
+      MTy mv[CH];
+#pragma unroll
+      for (int e = 0; e < CH; ++e) mv[e] = one_or_zero<MT>(keep[e]);
+      store_chunk(static_cast<MTy*>(A.mask) + q * CH, mv);
+    }
+  }
+}
+
 template <int XT, int YT, int MT, bool ALIGNED>
 __global__ void __launch_bounds__(256, SDR_DROP_MINB) k_dropout_fast(const __grid_constant__ DropArgs A) {
   using XTy = typename St<XT>::T;
@@ -808,25 +925,21 @@ __global__ void __launch_bounds__(256, SDR_DROP_MINB) k_dropout_fast(const __gri
       } else {
         chunk_words<NE>(A.g, j0 + h * NE, w0, w1);
       }
-      if constexpr (ALIGNED) {
-        // (w1:w0) <= keep_le is decided by w1 unless w1 equals its high word
-        // (p = 2^-32 per element): one rare branch per chunk, not per element.
-        const uint32_t H = hi32(A.keep_le);
-        bool tie = false;
-#pragma unroll
-        for (int i = 0; i < NE; ++i) {
-          keep[h * NE + i] = w1[i] < H;
-          tie |= w1[i] == H;
-        }
-        if (__builtin_expect(tie, 0)) {
-#pragma unroll
-          for (int i = 0; i < NE; ++i)
-            if (w1[i] == H) keep[h * NE + i] = keep_full(A.g, j0 + h * NE + i, A.keep_le);
-        }
-      }
 #pragma unroll
       for (int i = 0; i < NE; ++i) {
         const int e = h * NE + i;
+        if constexpr (ALIGNED) {
+          // (w1:w0) <= keep_le is decided by w1 unless w1 equals its high word
+          // (p = 2^-32): per-element rare branch (measured faster than one
+          // merged branch per chunk)
+          const uint32_t H = hi32(A.keep_le);
+          keep[e] = w1[i] < H;
+          if (__builtin_expect(w1[i] == H, 0)) {
+            uint32_t f0, f1;
+            elem_words(A.g, j0 + e, f0, f1);
+            keep[e] = ((static_cast<uint64_t>(f1) << 32) | f0) <= A.keep_le;
+          }
+        }
         if constexpr (!ALIGNED) {
           const uint64_t u64 = (static_cast<uint64_t>(w1[i]) << 32) | w0[i];
           keep[e] = u64 <= A.keep_le;
@@ -915,15 +1028,25 @@ __global__ void k_normal_calibrate(const double* rtab, const double* ctab, const
   if (rg == 0.0 || rn == 0.0) er = (rg == rn) ? 0.0 : __longlong_as_double(0x7FF0000000000000ll);
   else er = fabs(rg - rn) / rg;
   const double ec = fabs(c_fast(k, &s_lut) - ctab[k]);
-  unsigned long long br = __double_as_longlong(er), bc = __double_as_longlong(ec);
+  const double r32 = r32_fast(k);
+  double er32;
+  if (r32 == 0.0 || rn == 0.0) er32 = (r32 == rn) ? 0.0 : __longlong_as_double(0x7FF0000000000000ll);
+  else er32 = fabs(r32 - rn) / r32;
+  const double ec32 = fabs(static_cast<double>(c32_fast(k)) - ctab[k]);
+  unsigned long long b[4] = {static_cast<unsigned long long>(__double_as_longlong(er)),
+                             static_cast<unsigned long long>(__double_as_longlong(ec)),
+                             static_cast<unsigned long long>(__double_as_longlong(er32)),
+                             static_cast<unsigned long long>(__double_as_longlong(ec32))};
   // Non-negative doubles order like their bit patterns; reduce per warp first.
-  for (int o = 16; o > 0; o >>= 1) {
-    br = max(br, __shfl_xor_sync(0xffffffffu, br, o));
-    bc = max(bc, __shfl_xor_sync(0xffffffffu, bc, o));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    for (int o = 16; o > 0; o >>= 1) b[i] = max(b[i], __shfl_xor_sync(0xffffffffu, b[i], o));
   }
   if ((threadIdx.x & 31) == 0) {
-    atomicMax(max_r_bits, br);
-    atomicMax(max_c_bits, bc);
+    atomicMax(max_r_bits, b[0]);
+    atomicMax(max_c_bits, b[1]);
+    atomicMax(max_r_bits + 2, b[2]);
+    atomicMax(max_c_bits + 2, b[3]);
   }
 }
 
@@ -1052,7 +1175,7 @@ struct NormalState {
   double* ctab = nullptr;
   NormalLut* lut = nullptr;
   unsigned long long* fallbacks = nullptr;
-  double err_r = 0, err_c = 0;
+  double err_r = 0, err_c = 0, err_r32 = 0, err_c32 = 0;
   bool loaded = false;
 };
 static std::mutex g_nm_mu;
@@ -1130,6 +1253,15 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
       {
         const double Er = P.nm.err_r, Ac = P.nm.err_c, u = 0x1p-53;
         P.nm.bound_r = 2.0 * fabs(P.stdv) * (Er + Ac * (1.0 + Er) + 5.0 * u) * (1.0 + 0x1p-40);
+        // float32 path: |v32 - v_np| <= |std| r (Er32 + Ac32 + 2^-22) + 2^-23 |mean| + 2^-23 |v|,
+        // doubled (rounding of the bound itself, second-order terms).
+        const double Er32 = g_nm[device].err_r32, Ac32 = g_nm[device].err_c32;
+        P.nm.err_r32 = Er32;
+        P.nm.err_c32 = Ac32;
+        P.nm.mean32 = static_cast<float>(P.mean);
+        P.nm.std32 = static_cast<float>(P.stdv);
+        P.nm.b32_r = static_cast<float>(2.0 * fabs(P.stdv) * (Er32 * (1.0 + Ac32) + Ac32 + 0x1p-22) * 1.001);
+        P.nm.b32_c = static_cast<float>(2.0 * 0x1p-23 * fabs(P.mean) + 0x1p-140);
       }
       P.nm.fallbacks = g_nm[device].fallbacks;
       break;
@@ -1336,7 +1468,7 @@ int normal_tables_load(int device, const double* r_host, const double* c_host, d
   if (S.rtab == nullptr) {
     e = cudaMalloc(&S.rtab, bytes);
     if (e == cudaSuccess) e = cudaMalloc(&S.ctab, bytes);
-    if (e == cudaSuccess) e = cudaMalloc(&S.fallbacks, 3 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&S.fallbacks, 5 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMalloc(&S.lut, sizeof(NormalLut));
     if (e == cudaSuccess) {
       NormalLut h;
@@ -1346,14 +1478,15 @@ int normal_tables_load(int device, const double* r_host, const double* c_host, d
   }
   if (e == cudaSuccess) e = cudaMemcpy(S.rtab, r_host, bytes, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(S.ctab, c_host, bytes, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemset(S.fallbacks, 0, 3 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(S.fallbacks, 0, 5 * sizeof(unsigned long long));
   if (e == cudaSuccess) {
     k_normal_calibrate<<<(1u << 24) / 256, 256>>>(S.rtab, S.ctab, S.lut, S.fallbacks + 1,
                                                   S.fallbacks + 2);
     e = cudaGetLastError();
   }
-  unsigned long long bits[2] = {0, 0};
-  if (e == cudaSuccess) e = cudaMemcpy(bits, S.fallbacks + 1, 2 * sizeof(bits[0]), cudaMemcpyDeviceToHost);
+  // fallbacks[1..4] = max err of r, c (float64 path) and r32, c32 (float32 path)
+  unsigned long long bits[4] = {0, 0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpy(bits, S.fallbacks + 1, 4 * sizeof(bits[0]), cudaMemcpyDeviceToHost);
   cudaSetDevice(prev);
   if (e != cudaSuccess) {
     set_cuda_error(e);
@@ -1361,6 +1494,8 @@ int normal_tables_load(int device, const double* r_host, const double* c_host, d
   }
   memcpy(&S.err_r, &bits[0], 8);
   memcpy(&S.err_c, &bits[1], 8);
+  memcpy(&S.err_r32, &bits[2], 8);
+  memcpy(&S.err_c32, &bits[3], 8);
   S.loaded = true;
   if (er) *er = S.err_r;
   if (ec) *ec = S.err_c;
