@@ -406,15 +406,7 @@ __host__ __device__ __forceinline__ double c_fast(uint32_t k, const NormalLut* L
 // against the NumPy tables like the float64 ones).
 __host__ __device__ __forceinline__ float r32_fast(uint32_t k) {
   const float u = static_cast<float>(k) * 0x1p-24f;     // exact
-  const float w = 1.0f - u;                             // exact (24-bit)
-  // -log1p(-u): series for u < 1/16, else -ln(w) from log2
-  const float ser = u * fmaf(u, fmaf(u, fmaf(u, fmaf(u, 0.2f, 0.25f), 1.0f / 3.0f), 0.5f), 1.0f);
-#ifdef __CUDA_ARCH__
-  const float lg = -__log2f(w) * 0.69314718055994530942f;
-#else
-  const float lg = -std::log2(w) * 0.69314718055994530942f;
-#endif
-  const float L = u < 0.0625f ? ser : lg;
+  const float L = -log1pf(-u);                          // ~1 ulp relative (accurate libm)
   const float x = L + L;
 #ifdef __CUDA_ARCH__
   const float r = x * rsqrtf(x);
@@ -436,29 +428,30 @@ __host__ __device__ __forceinline__ float c32_fast(uint32_t k) {
 // bfloat16 normals of a chunk through float32, certified against the float64
 // NumPy value with a directed-rounding enclosure; the rare uncertified
 // elements recompute exactly from the tables.
+template <int DT>
+__device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, const NormalLut* L,
+                                                           uint32_t w0, uint32_t w1);
+
 template <int NE>
-__device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const uint32_t* w0, const uint32_t* w1,
-                                                  uint16_t* out) {
+__device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLut* L, const uint32_t* w0,
+                                                  const uint32_t* w1, uint16_t* out) {
   uint32_t badmask = 0;
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
     const float r = r32_fast(w0[e] >> 8), c = c32_fast(w1[e] >> 8);
     const float z = __fmul_rn(r, c);
     const float v = __fmaf_rn(P.nm.std32, z, P.nm.mean32);
-    const float B = fmaf(r, P.nm.b32_r, fmaf(fabsf(v), 0x1p-22f, P.nm.b32_c));
+    // |v - v_numpy| <= |z|*b32_r + |v|*2^-23 + b32_c   (host: bound terms)
+    const float B = fmaf(fabsf(z), P.nm.b32_r, fmaf(fabsf(v), 0x1p-23f, P.nm.b32_c));
     const uint16_t lo = bf16_bits(__fsub_rd(v, B)), hi = bf16_bits(__fadd_ru(v, B));
     out[e] = lo;
-    badmask |= (lo == hi) ? 0u : (1u << e);
+    // c == 0 only at u2 = 1/4, 3/4 where NumPy's cos(fl(pi/2)) != 0: exact path
+    badmask |= (lo == hi && c != 0.0f) ? 0u : (1u << e);
   }
   if (__builtin_expect(badmask != 0, 0)) {
 #pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      if (badmask & (1u << e)) {
-        atomicAdd(P.nm.fallbacks, 1ull);
-        const double rr = __ldg(P.nm.rtab + (w0[e] >> 8)), cc = __ldg(P.nm.ctab + (w1[e] >> 8));
-        out[e] = from_f64<SDR_BF16>(__dadd_rn(P.mean, __dmul_rn(P.stdv, __dmul_rn(rr, cc))));
-      }
-    }
+    for (int e = 0; e < NE; ++e)
+      if (badmask & (1u << e)) out[e] = normal_value<SDR_BF16>(P, L, w0[e], w1[e]);  // f64 path
   }
 }
 
@@ -651,7 +644,7 @@ __device__ __forceinline__ void fill_chunk(const FillArgs& A, const NormalLut* L
   else chunk_words<kV>(A.g, j0, w0, w1);
   T v[kV];
   if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
-    normal_chunk_bf16<kV>(A.d, w0, w1, v);
+    normal_chunk_bf16<kV>(A.d, L, w0, w1, v);
   } else if constexpr (DIST == SDR_NORMAL && DT != SDR_F64) {
     constexpr int NS = SDR_NORMAL_SPLIT;
 #pragma unroll
@@ -1032,7 +1025,10 @@ __global__ void k_normal_calibrate(const double* rtab, const double* ctab, const
   double er32;
   if (r32 == 0.0 || rn == 0.0) er32 = (r32 == rn) ? 0.0 : __longlong_as_double(0x7FF0000000000000ll);
   else er32 = fabs(r32 - rn) / r32;
-  const double ec32 = fabs(static_cast<double>(c32_fast(k)) - ctab[k]);
+  const float c32 = c32_fast(k);
+  // relative error of the float32 cos; c32 == 0 (k = 2^22, 3*2^22) always takes
+  // the exact path in the kernel, so it is excluded here
+  const double ec32 = (c32 == 0.0f) ? 0.0 : fabs(static_cast<double>(c32) - ctab[k]) / fabs(static_cast<double>(c32));
   unsigned long long b[4] = {static_cast<unsigned long long>(__double_as_longlong(er)),
                              static_cast<unsigned long long>(__double_as_longlong(ec)),
                              static_cast<unsigned long long>(__double_as_longlong(er32)),
@@ -1260,8 +1256,12 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
         P.nm.err_c32 = Ac32;
         P.nm.mean32 = static_cast<float>(P.mean);
         P.nm.std32 = static_cast<float>(P.stdv);
-        P.nm.b32_r = static_cast<float>(2.0 * fabs(P.stdv) * (Er32 * (1.0 + Ac32) + Ac32 + 0x1p-22) * 1.001);
-        P.nm.b32_c = static_cast<float>(2.0 * 0x1p-23 * fabs(P.mean) + 0x1p-140);
+        // |v32 - v_np| <= |std32 z32| (Er32 + Ec32 + 2^-23) + 2^-24 |v32| + 2^-24 |mean32|,
+        // x1.02 for second-order terms and the rounding of the bound itself
+        // (kernel adds |v| 2^-23 = 2 x the 2^-24 term).
+        P.nm.b32_r = static_cast<float>(1.02 * fabs(static_cast<double>(P.nm.std32)) *
+                                        (Er32 * (1.0 + Ac32) + Ac32 + 0x1p-23) + 0x1p-60);
+        P.nm.b32_c = static_cast<float>(1.02 * 0x1p-24 * fabs(P.mean) + 0x1p-140);
       }
       P.nm.fallbacks = g_nm[device].fallbacks;
       break;

@@ -269,6 +269,15 @@ def _fused_gather(mesh, md, items, ledger, mover):
         send_members.append(Member(loc, o, rows_local, inner, chunk))
         recv_members.append(Member(full, o, rows_full, inner, chunk))
         outs.append(full)
+    if len(items) == 1 and recv_members[0].outer <= 1 and recv_members[0].rows == P * recv_members[0].chunk:
+        # zero-copy: the shard IS the rank segment and the output IS the
+        # rank-major gathered buffer (outer == 1, even split)
+        loc = items[0][1][1].contiguous()
+        comm.all_gather_into(outs[0].view(-1), loc.view(-1), group, ledger, mesh.name, mesh.dim_names[md], P)
+        slot = items[0][1]
+        slot[0] = slot[0].with_placement(md, Replicate())
+        slot[1] = outs[0]
+        return
     seg = layout(send_members)
     for s, r in zip(send_members, recv_members):
         r.seg_off = s.seg_off
@@ -300,6 +309,15 @@ def _fused_reduce_scatter(mesh, md, items, ledger, mover):
         full_members.append(Member(loc, o, rows_full, inner, chunk))
         piece_members.append(Member(out, o, rows_mine, inner, chunk))
         outs.append(out)
+    if len(items) == 1 and full_members[0].outer <= 1 and full_members[0].rows == P * full_members[0].chunk:
+        # zero-copy: the full local tensor is already rank-major
+        inp = items[0][1][1].contiguous()
+        comm.reduce_scatter_into(outs[0].view(-1), inp.view(-1), group, ledger, mesh.name,
+                                 mesh.dim_names[md], P)
+        x, slot, dst_p = items[0]
+        slot[0] = slot[0].with_placement(md, dst_p)
+        slot[1] = outs[0]
+        return
     seg = layout(full_members, align=16)
     for f, pm in zip(full_members, piece_members):
         pm.seg_off = f.seg_off
