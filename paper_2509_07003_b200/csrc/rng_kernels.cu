@@ -260,10 +260,17 @@ struct NormalLut {
   double2 trig[2049];
 };
 
+// float32 copies for the bfloat16 fast path (20 KiB, staged in shared memory).
+struct NormalLut32 {
+  float2 logt[512];
+  float2 trig[2049];
+};
+
 struct NormalMirror {
   const double* rtab;   // NumPy r[k] = sqrt(-2*log1p(-k*2^-24))
   const double* ctab;   // NumPy c[k] = cos(2*pi*(k*2^-24))
   const NormalLut* lut; // device copy of the fast-path tables
+  const NormalLut32* lut32;
   double err_r;         // max |r_fast - r_np| / r_fast over all k (exhaustive)
   double err_c;         // max |c_fast - c_np| over all k (exhaustive)
   double bound_r;       // certification bound B = r*bound_r + |v|*2^-51 (+tiny)
@@ -404,54 +411,60 @@ __host__ __device__ __forceinline__ double c_fast(uint32_t k, const NormalLut* L
 
 // float32 fast functions for the bfloat16 path (errors calibrated exhaustively
 // against the NumPy tables like the float64 ones).
-__host__ __device__ __forceinline__ float r32_fast(uint32_t k) {
-  const float u = static_cast<float>(k) * 0x1p-24f;     // exact
-  const float L = -log1pf(-u);                          // ~1 ulp relative (accurate libm)
-  const float x = L + L;
-#ifdef __CUDA_ARCH__
+// float32 r: same reduction as r_fast with float tables; t = fma(M, mult, -1)
+// is rounded once (M 24 bits, mult 20 bits), log1p(t) to t^3.
+__device__ __forceinline__ float r32_fast(uint32_t k, const NormalLut32* L) {
+  const uint32_t n = (1u << 24) - k - (k == 0 ? 1u : 0u);
+  const uint32_t hw = __float_as_uint(__uint2float_rn(n));   // exact (n < 2^24)
+  const int b = static_cast<int>(hw >> 23) - 126;             // bit length of n
+  const int j = static_cast<int>((hw >> 14) & 511u);
+  const int e = b - 25 + (j >= 256 ? 1 : 0);
+  const float Mf = __uint_as_float((hw & 0x007FFFFFu) | (150u << 23));  // n in [2^23, 2^24)
+  const float2 tb = L->logt[j];
+  const float t = fmaf(Mf, tb.x, -1.0f);
+  const float lg = fmaf(t * t, fmaf(t, 1.0f / 3.0f, -0.5f), t);
+  const float Lw = fmaf(static_cast<float>(-e), 0.69314718f, tb.y - lg);
+  const float x = Lw + Lw;
   const float r = x * rsqrtf(x);
-#else
-  const float r = std::sqrt(x);
-#endif
   return k == 0 ? 0.0f : r;
 }
 
-__host__ __device__ __forceinline__ float c32_fast(uint32_t k) {
-  const float h = static_cast<float>(k) * 0x1p-23f;     // 2u, exact
-#ifdef __CUDA_ARCH__
-  return cospif(h);
-#else
-  return static_cast<float>(std::cos(3.141592653589793 * static_cast<double>(h)));
-#endif
+// float32 c: nearest point of the pi/1024 table + residual to d^2 / d^3.
+__device__ __forceinline__ float c32_fast(uint32_t k, const NormalLut32* L) {
+  const uint32_t i = (k + 4096u) >> 13;
+  const uint32_t dj4 = k + 4096u - (i << 13);                  // dj + 4096 in [0, 8191]
+  const float d = (__uint_as_float(0x4B000000u | dj4) - 8392704.0f) * 3.74507039e-7f;  // exact dj, *2pi/2^24
+  const float d2 = d * d;
+  const float cm = -0.5f * d2;
+  const float sd = d * fmaf(d2, -1.0f / 6.0f, 1.0f);
+  const float2 cs = L->trig[i];
+  return cs.x + fmaf(cs.x, cm, -cs.y * sd);
 }
 
-// bfloat16 normals of a chunk through float32, certified against the float64
-// NumPy value with a directed-rounding enclosure; the rare uncertified
-// elements recompute exactly from the tables.
 template <int DT>
 __device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, const NormalLut* L,
                                                            uint32_t w0, uint32_t w1);
 
 template <int NE>
-__device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLut* L, const uint32_t* w0,
-                                                  const uint32_t* w1, uint16_t* out) {
+__device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLut32* L32,
+                                                  const uint32_t* w0, const uint32_t* w1, uint16_t* out) {
   uint32_t badmask = 0;
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
-    const float r = r32_fast(w0[e] >> 8), c = c32_fast(w1[e] >> 8);
+    const float r = r32_fast(w0[e] >> 8, L32), c = c32_fast(w1[e] >> 8, L32);
     const float z = __fmul_rn(r, c);
     const float v = __fmaf_rn(P.nm.std32, z, P.nm.mean32);
-    // |v - v_numpy| <= |z|*b32_r + |v|*2^-23 + b32_c   (host: bound terms)
-    const float B = fmaf(fabsf(z), P.nm.b32_r, fmaf(fabsf(v), 0x1p-23f, P.nm.b32_c));
+    // |v - v_numpy| <= r*b32_r + |v|*2^-23 + b32_c   (host: bound terms)
+    const float B = fmaf(r, P.nm.b32_r, fmaf(fabsf(v), 0x1p-23f, P.nm.b32_c));
     const uint16_t lo = bf16_bits(__fsub_rd(v, B)), hi = bf16_bits(__fadd_ru(v, B));
     out[e] = lo;
-    // c == 0 only at u2 = 1/4, 3/4 where NumPy's cos(fl(pi/2)) != 0: exact path
-    badmask |= (lo == hi && c != 0.0f) ? 0u : (1u << e);
+    badmask |= (lo == hi) ? 0u : (1u << e);
   }
   if (__builtin_expect(badmask != 0, 0)) {
+    // float64 certified path (tables read through L1/L2), then the exact NumPy tables
 #pragma unroll
     for (int e = 0; e < NE; ++e)
-      if (badmask & (1u << e)) out[e] = normal_value<SDR_BF16>(P, L, w0[e], w1[e]);  // f64 path
+      if (badmask & (1u << e)) out[e] = normal_value<SDR_BF16>(P, P.nm.lut, w0[e], w1[e]);
   }
 }
 
@@ -521,10 +534,12 @@ __device__ __forceinline__ void normal_chunk(const DistP& P, const NormalLut* L,
 }
 
 // Stage the Normal tables in shared memory (whole CTA participates).
-__device__ __forceinline__ void stage_lut(NormalLut* dst, const NormalLut* src) {
-  const double2* s = reinterpret_cast<const double2*>(src);
-  double2* d = reinterpret_cast<double2*>(dst);
-  for (int i = threadIdx.x; i < static_cast<int>(sizeof(NormalLut) / 16); i += blockDim.x) d[i] = s[i];
+template <typename LUT>
+__device__ __forceinline__ void stage_lut(LUT* dst, const LUT* src) {
+  static_assert(sizeof(LUT) % 8 == 0, "LUT size");
+  const uint2* s = reinterpret_cast<const uint2*>(src);
+  uint2* d = reinterpret_cast<uint2*>(dst);
+  for (int i = threadIdx.x; i < static_cast<int>(sizeof(LUT) / 8); i += blockDim.x) d[i] = s[i];
   __syncthreads();
 }
 
@@ -644,7 +659,7 @@ __device__ __forceinline__ void fill_chunk(const FillArgs& A, const NormalLut* L
   else chunk_words<kV>(A.g, j0, w0, w1);
   T v[kV];
   if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
-    normal_chunk_bf16<kV>(A.d, L, w0, w1, v);
+    normal_chunk_bf16<kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v);
   } else if constexpr (DIST == SDR_NORMAL && DT != SDR_F64) {
     constexpr int NS = SDR_NORMAL_SPLIT;
 #pragma unroll
@@ -668,7 +683,11 @@ __device__ __forceinline__ void fill_elem(const FillArgs& A, const NormalLut* L,
 template <int DIST, int DT, bool ALIGNED>
 __global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_fast(const __grid_constant__ FillArgs A) {
   const NormalLut* L = nullptr;
-  if constexpr (DIST == SDR_NORMAL) {
+  if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
+    __shared__ NormalLut32 s_lut32;
+    stage_lut(&s_lut32, A.d.nm.lut32);
+    L = reinterpret_cast<const NormalLut*>(&s_lut32);
+  } else if constexpr (DIST == SDR_NORMAL) {
     __shared__ NormalLut s_lut;
     stage_lut(&s_lut, A.d.nm.lut);
     L = &s_lut;
@@ -707,7 +726,11 @@ __global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_batch(const FillArg
   __shared__ __align__(16) unsigned char smem[sizeof(FillArgs)];
   FillArgs& A = *reinterpret_cast<FillArgs*>(smem);
   const NormalLut* L = nullptr;
-  if constexpr (DIST == SDR_NORMAL) {
+  if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
+    __shared__ NormalLut32 s_lut32;
+    stage_lut(&s_lut32, descs[0].d.nm.lut32);
+    L = reinterpret_cast<const NormalLut*>(&s_lut32);
+  } else if constexpr (DIST == SDR_NORMAL) {
     __shared__ NormalLut s_lut;
     stage_lut(&s_lut, descs[0].d.nm.lut);
     L = &s_lut;
@@ -1010,10 +1033,10 @@ __global__ void k_philox_blocks(const uint64_t* tau, const uint64_t* beta, int64
 
 // Exhaustive calibration of the Normal fast path against the NumPy tables.
 __global__ void k_normal_calibrate(const double* rtab, const double* ctab, const NormalLut* lut,
-                                   unsigned long long* max_r_bits,
+                                   const NormalLut32* lut32, unsigned long long* max_r_bits,
                                    unsigned long long* max_c_bits) {
   __shared__ NormalLut s_lut;
-  stage_lut(&s_lut, lut);
+  stage_lut(&s_lut, lut);  // the float32 tables are read from global memory here
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= (1u << 24)) return;
   const double rg = r_fast(k, &s_lut), rn = rtab[k];
@@ -1021,14 +1044,11 @@ __global__ void k_normal_calibrate(const double* rtab, const double* ctab, const
   if (rg == 0.0 || rn == 0.0) er = (rg == rn) ? 0.0 : __longlong_as_double(0x7FF0000000000000ll);
   else er = fabs(rg - rn) / rg;
   const double ec = fabs(c_fast(k, &s_lut) - ctab[k]);
-  const double r32 = r32_fast(k);
+  const double r32 = r32_fast(k, lut32);
   double er32;
   if (r32 == 0.0 || rn == 0.0) er32 = (r32 == rn) ? 0.0 : __longlong_as_double(0x7FF0000000000000ll);
   else er32 = fabs(r32 - rn) / r32;
-  const float c32 = c32_fast(k);
-  // relative error of the float32 cos; c32 == 0 (k = 2^22, 3*2^22) always takes
-  // the exact path in the kernel, so it is excluded here
-  const double ec32 = (c32 == 0.0f) ? 0.0 : fabs(static_cast<double>(c32) - ctab[k]) / fabs(static_cast<double>(c32));
+  const double ec32 = fabs(static_cast<double>(c32_fast(k, lut32)) - ctab[k]);  // absolute
   unsigned long long b[4] = {static_cast<unsigned long long>(__double_as_longlong(er)),
                              static_cast<unsigned long long>(__double_as_longlong(ec)),
                              static_cast<unsigned long long>(__double_as_longlong(er32)),
@@ -1170,6 +1190,7 @@ struct NormalState {
   double* rtab = nullptr;
   double* ctab = nullptr;
   NormalLut* lut = nullptr;
+  NormalLut32* lut32 = nullptr;
   unsigned long long* fallbacks = nullptr;
   double err_r = 0, err_c = 0, err_r32 = 0, err_c32 = 0;
   bool loaded = false;
@@ -1244,6 +1265,7 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
       P.nm.rtab = g_nm[device].rtab;
       P.nm.ctab = g_nm[device].ctab;
       P.nm.lut = g_nm[device].lut;
+      P.nm.lut32 = g_nm[device].lut32;
       P.nm.err_r = g_nm[device].err_r;
       P.nm.err_c = g_nm[device].err_c;
       {
@@ -1470,17 +1492,24 @@ int normal_tables_load(int device, const double* r_host, const double* c_host, d
     if (e == cudaSuccess) e = cudaMalloc(&S.ctab, bytes);
     if (e == cudaSuccess) e = cudaMalloc(&S.fallbacks, 5 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMalloc(&S.lut, sizeof(NormalLut));
+    if (e == cudaSuccess) e = cudaMalloc(&S.lut32, sizeof(NormalLut32));
     if (e == cudaSuccess) {
       NormalLut h;
       build_normal_lut(h);
+      NormalLut32 h32;
+      for (int j = 0; j < 512; ++j) h32.logt[j] = make_float2(static_cast<float>(h.logt[j].x),
+                                                              static_cast<float>(h.logt[j].y));
+      for (int i = 0; i <= 2048; ++i) h32.trig[i] = make_float2(static_cast<float>(h.trig[i].x),
+                                                                static_cast<float>(h.trig[i].y));
       e = cudaMemcpy(S.lut, &h, sizeof(NormalLut), cudaMemcpyHostToDevice);
+      if (e == cudaSuccess) e = cudaMemcpy(S.lut32, &h32, sizeof(NormalLut32), cudaMemcpyHostToDevice);
     }
   }
   if (e == cudaSuccess) e = cudaMemcpy(S.rtab, r_host, bytes, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(S.ctab, c_host, bytes, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(S.fallbacks, 0, 5 * sizeof(unsigned long long));
   if (e == cudaSuccess) {
-    k_normal_calibrate<<<(1u << 24) / 256, 256>>>(S.rtab, S.ctab, S.lut, S.fallbacks + 1,
+    k_normal_calibrate<<<(1u << 24) / 256, 256>>>(S.rtab, S.ctab, S.lut, S.lut32, S.fallbacks + 1,
                                                   S.fallbacks + 2);
     e = cudaGetLastError();
   }
