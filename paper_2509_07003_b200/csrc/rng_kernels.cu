@@ -251,19 +251,27 @@ __device__ __forceinline__ typename St<DT>::T one_or_zero(bool b) {
 // Distribution parameters and the Normal mirror state.
 // ---------------------------------------------------------------------------
 // Device lookup tables of the Normal fast path (40 KiB, staged in shared
-// memory by every kernel that draws normals):
-//   logt[j] = (mult_j * 2^-23, ln(inv_j)) for the 512 mantissa intervals
-//             [1 + j/512, 1 + (j+1)/512) of the 24-bit integer 2^24 - k;
-//   trig[i] = (cos, sin)(i * pi/1024), i = 0..2048 (full circle).
+// memory by every kernel that draws normals).  With n = 2^24 - k the fast path
+// evaluates X = 2L = -2 ln(n 2^-24) as
+//   X = (-e) 2ln2 + 2 ln(inv_j) + g(s),  s = -2t = 2 - 2 m' inv_j  (exact),
+//   g(s) = -2 log1p(-s/2) = s + s^2/4 + s^3/12 + s^4/32 + s^5/80,
+// with n = 2^(e+24) m', m' in [0.75, 1.5) and j the top 9 fraction bits of n;
+// r = sqrt(X) is one Newton step on the MUFU.RSQ64H seed.  The cosine is
+//   c = cos(i pi/1024 + K d) = C_i (1 + cm(d)) - S_i sd(d),
+// i = round(k / 8192), d = k - 8192 i in [-4096, 4096), K = 2 pi / 2^24.
+//   logt[j] = (-2 mult_j 2^-23, 2 ln(inv_j))  (+2^-1000 at j = 0: X > 0 at k = 0)
+//   trig[i] = (cos, sin)(i pi/1024), i = 0..2047 (k near 2^24 wraps to i = 0)
+// Both are approximations to ~2^-45 whose exact error against the host's NumPy
+// is measured over all 2^24 inputs at load time (k_normal_calibrate).
 struct NormalLut {
   double2 logt[512];
-  double2 trig[2049];
+  double2 trig[2048];
 };
 
 // float32 copies for the bfloat16 fast path (20 KiB, staged in shared memory).
 struct NormalLut32 {
   float2 logt[512];
-  float2 trig[2049];
+  float2 trig[2048];
 };
 
 struct NormalMirror {
@@ -271,9 +279,8 @@ struct NormalMirror {
   const double* ctab;   // NumPy c[k] = cos(2*pi*(k*2^-24))
   const NormalLut* lut; // device copy of the fast-path tables
   const NormalLut32* lut32;
-  double err_r;         // max |r_fast - r_np| / r_fast over all k (exhaustive)
-  double err_c;         // max |c_fast - c_np| over all k (exhaustive)
-  double bound_r;       // certification bound B = r*bound_r + |v|*2^-51 (+tiny)
+  double nh, th;        // -0.5*std, 1.5*std: the Newton step of r_fast returns std*r
+  double kr, k0;        // certification bound B = (std r) kr + |v| 2^-51 + k0
   // float32 fast path (bfloat16 outputs): calibrated errors and bound terms
   double err_r32, err_c32;
   float mean32, std32, b32_r, b32_c;  // B32 = r*b32_r + |v|*2^-22 + b32_c
@@ -292,153 +299,129 @@ struct DistP {
   NormalMirror nm;
 };
 
-constexpr double kLn2Hi = 0x1.62e42fefa3800p-1;   // ln 2, low 16 bits zero: e*kLn2Hi exact
-constexpr double kLn2Lo = 0x1.ef35793c76730p-45;
-constexpr double kTwoPiOver2p24 = 0x1.921fb54442d18p-22;  // 2*pi / 2^24
+constexpr double kTwo52m1 = 4503599627370495.0;     // 2^52 - 1
+constexpr double kTwo52p1047 = 4503599627371543.0;  // 2^52 + 1047
+constexpr double kTwo52p4096 = 4503599627374592.0;  // 2^52 + 4096
+constexpr double kK1 = 0x1.921fb54442d18p-22;       // 2 pi / 2^24
 
 // Polynomial coefficients as constant-bank operands (no per-use materialisation).
-__constant__ double c_npoly[8] = {
-    -1.0 / 6.0, 1.0 / 5.0, -0.25, 1.0 / 3.0, -0.5,   // log1p Horner (with 1/7 folded below)
-    1.0 / 24.0, 1.0 / 120.0, -1.0 / 6.0};             // cos / sin residual
-
-#ifndef SDR_SQRT_NEWTON
-#define SDR_SQRT_NEWTON 1   // Newton steps on the MUFU.RSQ64H seed before the final correction
-#endif
+__constant__ double c_npoly[9] = {
+    1.0 / 80.0, 1.0 / 32.0, 1.0 / 12.0, 0.25,        // g(s) Horner
+    kK1 * kK1 * kK1 * kK1 / 24.0, -0.5 * kK1 * kK1,   // cos(K d) - 1 = d^2 (c4 d^2 + c2)
+    -kK1 * kK1 * kK1 / 6.0, kK1,                      // sin(K d) = d (s3 d^2 + K)
+    0x1.62e42fefa39efp0};                             // 2 ln 2
 #ifndef SDR_NORMAL_BF16_F32
 #define SDR_NORMAL_BF16_F32 1  // certified float32 Box-Muller for bfloat16 outputs
 #endif
 #ifndef SDR_NORMAL_SPLIT
 #define SDR_NORMAL_SPLIT 1  // float64 phases of a chunk in SPLIT passes (register pressure)
 #endif
+#ifndef SDR_R_NEWTON2
+#define SDR_R_NEWTON2 0   // second Newton step for r (fewer certification fallbacks)
+#endif
 #ifndef SDR_FILL_MINB
-#define SDR_FILL_MINB 2   // 2 CTAs/SM: <=128 regs so the 8 f64 chains of a chunk interleave
+#define SDR_FILL_MINB 2   // CTAs/SM the register budget of the fill kernels is sized for
 #endif
 
-// Branch-free sqrt for x in (0, 64): MUFU.RSQ64H seed + Newton steps.  Not
-// correctly rounded -- the exhaustive calibration covers its error.
-__host__ __device__ __forceinline__ double sqrt_nb(double x) {
+__host__ __device__ __forceinline__ double hilo(uint32_t hi, uint32_t lo) {
 #ifdef __CUDA_ARCH__
+  return __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
+#else
+  const uint64_t b = (static_cast<uint64_t>(hi) << 32) | lo;
+  double d;
+  memcpy(&d, &b, 8);
+  return d;
+#endif
+}
+__host__ __device__ __forceinline__ uint32_t dhi(double d) {
+#ifdef __CUDA_ARCH__
+  return static_cast<uint32_t>(__double2hiint(d));
+#else
+  uint64_t b;
+  memcpy(&b, &d, 8);
+  return static_cast<uint32_t>(b >> 32);
+#endif
+}
+__host__ __device__ __forceinline__ uint32_t dlo(double d) {
+#ifdef __CUDA_ARCH__
+  return static_cast<uint32_t>(__double2loint(d));
+#else
+  uint64_t b;
+  memcpy(&b, &d, 8);
+  return static_cast<uint32_t>(b);
+#endif
+}
+
+__device__ __forceinline__ double rsqrt_seed(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double hx = 0.5 * x;
-#if SDR_SQRT_NEWTON > 1
-  double e = fma(-hx * y, y, 0.5);
-  y = fma(y, e, y);
-#endif
-  const double e1 = fma(-hx * y, y, 0.5);
-  y = fma(y, e1, y);
-  double s = x * y;
-  const double d = fma(-s, s, x);
-  return fma(0.5 * y, d, s);
-#else
-  return sqrt(x);
-#endif
+  return y;
 }
 
-// r(k) = sqrt(-2*log1p(-k*2^-24)) from the exact integer n = 2^24 - k:
-// w = n*2^-24 = 2^e' * m', m' in [0.75, 1.5); ln m' = -ln(inv) + log1p(t) with
-// t = m'*inv - 1 EXACT (24-bit m' times a 20-bit inv); the two intervals next
-// to m' = 1 use inv = 1 so no cancellation occurs for small k.  Branch-free:
-// k = 0 (r = 0 exactly) is selected at the end.
-// Exact uint32 -> double without a conversion instruction: 2^52 + x has x in
-// its low mantissa bits, so one DADD removes the bias (fp64 pipe, not XU).
-__host__ __device__ __forceinline__ double u32_to_f64(uint32_t x) {
-#ifdef __CUDA_ARCH__
-  return __hiloint2double(0x43300000, static_cast<int>(x)) - 0x1p52;
-#else
-  return static_cast<double>(x);
-#endif
+template <typename T>
+__device__ __forceinline__ const T& lut_at(const T* base, uint32_t byte_off) {
+  return *reinterpret_cast<const T*>(reinterpret_cast<const char*>(base) + byte_off);
 }
 
-__host__ __device__ __forceinline__ double r_fast(uint32_t k, const NormalLut* L) {
-  const uint32_t n = (1u << 24) - k - (k == 0 ? 1u : 0u);  // 1 .. 2^24-1
-  const double nd = u32_to_f64(n);                // exact
-#ifdef __CUDA_ARCH__
-  const uint32_t hw = static_cast<uint32_t>(__double2hiint(nd));
-  const uint32_t lw = static_cast<uint32_t>(__double2loint(nd));
-#else
-  uint64_t nb;
-  memcpy(&nb, &nd, 8);
-  const uint32_t hw = static_cast<uint32_t>(nb >> 32), lw = static_cast<uint32_t>(nb);
-#endif
-  const int b = static_cast<int>(hw >> 20) - 1022;  // bit length of n, 1..24
-  const int j = static_cast<int>((hw >> 11) & 511u); // top 9 fraction bits: interval 0..511
-  const int e = b - 25 + (j >= 256 ? 1 : 0);      // e' of w = 2^e' m'
-  // M = n scaled into [2^23, 2^24): same mantissa, exponent of 2^23
-#ifdef __CUDA_ARCH__
-  const double Md = __hiloint2double(static_cast<int>((hw & 0x000FFFFFu) | 0x41600000u), static_cast<int>(lw));
-#else
-  const uint64_t mb = (static_cast<uint64_t>((hw & 0x000FFFFFu) | 0x41600000u) << 32) | lw;
-  double Md;
-  memcpy(&Md, &mb, 8);
-#endif
-  const double2 tb = L->logt[j];
-  const double t = fma(Md, tb.x, -1.0);           // exact
-#ifdef __CUDA_ARCH__
+// std * r(k), r(k) = sqrt(-2*log1p(-k*2^-24)), k = w0 >> 8, as described at
+// NormalLut; nh = -0.5*std, th = 1.5*std fold std into the Newton step.  No
+// select for k = 0: the 2^-1000 in logt[0] keeps X > 0 and r ~ 2^-499.5.
+__device__ __forceinline__ double r_fast(uint32_t w0, const NormalLut* L, double nh, double th) {
   const double* C = c_npoly;
-#else
-  static const double C[8] = {-1.0 / 6.0, 1.0 / 5.0, -0.25, 1.0 / 3.0, -0.5, 1.0 / 24.0, 1.0 / 120.0, -1.0 / 6.0};
+  const double nd = hilo(0x43300000u, (w0 >> 8) ^ 0xFFFFFFu) - kTwo52m1;  // n, exact
+  const uint32_t hw = dhi(nd), lw = dlo(nd);
+  const double2 tb = lut_at(L->logt, (hw >> 7) & 0x1FF0u);               // j = hw[19:11]
+  const double s = fma(hilo((hw & 0x000FFFFFu) | 0x41600000u, lw), tb.x, 2.0);  // -2t, exact
+  double p = fma(s, C[0], C[1]);
+  p = fma(s, p, C[2]);
+  p = fma(s, p, C[3]);
+  const double g = fma(s * s, p, s);                                     // -2 log1p(t)
+  const double ne = kTwo52p1047 - hilo(0x43300000u, (hw + 0x80000u) >> 20);  // -e, exact
+  const double X = fma(ne, C[8], tb.y + g);                              // -2 ln w
+  double h = rsqrt_seed(X);
+#if SDR_R_NEWTON2
+  h = h * fma(X * h, h * -0.5, 1.5);                                     // seed to ~2^-40
 #endif
-  // log1p(t), |t| <= 2^-9: Taylor to t^6 (|t|^7/7 < 2^-66)
-  double p = fma(t, C[0], C[1]);                   // 1/5 - t/6
-  p = fma(t, p, C[2]);
-  p = fma(t, p, C[3]);
-  p = fma(t, p, C[4]);
-  const double lg = fma(t * t, p, t);             // t + t^2*(-1/2 + ...)
-  const double ne = u32_to_f64(static_cast<uint32_t>(-e));   // 0..24, exact
-  const double Lw = fma(ne, kLn2Hi, fma(ne, kLn2Lo, tb.y - lg));  // -ln w
-  const double r = sqrt_nb(Lw + Lw);
-  return k == 0 ? 0.0 : r;
+  const double gx = X * h;
+  return gx * fma(gx * h, nh, th);                                       // std * sqrt(X)
 }
 
-// c(k) = cos(2*pi*k*2^-24): nearest point of a pi/1024 full-circle table + a
-// short Taylor residual (|d| <= 1.54e-3).
-__host__ __device__ __forceinline__ double c_fast(uint32_t k, const NormalLut* L) {
-  const uint32_t i = (k + 4096u) >> 13;            // 0..2048
-  const uint32_t dj4 = k + 4096u - (i << 13);     // dj + 4096 in [0, 8191]
-  const double d = (u32_to_f64(dj4) - 4096.0) * kTwoPiOver2p24;
+// cos(2*pi*k*2^-24), k = w1 >> 8: nearest pi/1024 table point + residual.
+__device__ __forceinline__ double c_fast(uint32_t w1, const NormalLut* L) {
+  const double* C = c_npoly;
+  const uint32_t u = w1 + 0x100000u;                                     // (k + 4096) << 8
+  const double2 cs = lut_at(L->trig, (u >> 17) & 0x7FF0u);               // i = u >> 21
+  const double d = hilo(0x43300000u, (u >> 8) & 0x1FFFu) - kTwo52p4096;  // k - 8192 i, exact
   const double d2 = d * d;
-#ifdef __CUDA_ARCH__
-  const double* C = c_npoly;
-#else
-  static const double C[8] = {-1.0 / 6.0, 1.0 / 5.0, -0.25, 1.0 / 3.0, -0.5, 1.0 / 24.0, 1.0 / 120.0, -1.0 / 6.0};
-#endif
-  const double cm = d2 * fma(d2, C[5], C[4]);                  // cos d - 1
-  const double sd = fma(d * d2, fma(d2, C[6], C[7]), d);        // sin d
-  const double2 cs = L->trig[i];
-  return cs.x + fma(cs.x, cm, -cs.y * sd);
+  const double cm = d2 * fma(d2, C[4], C[5]);                            // cos(K d) - 1
+  const double sd = d * fma(d2, C[6], C[7]);                             // sin(K d)
+  return fma(-cs.y, sd, fma(cs.x, cm, cs.x));
 }
 
-// float32 fast functions for the bfloat16 path (errors calibrated exhaustively
-// against the NumPy tables like the float64 ones).
-// float32 r: same reduction as r_fast with float tables; t = fma(M, mult, -1)
-// is rounded once (M 24 bits, mult 20 bits), log1p(t) to t^3.
-__device__ __forceinline__ float r32_fast(uint32_t k, const NormalLut32* L) {
-  const uint32_t n = (1u << 24) - k - (k == 0 ? 1u : 0u);
-  const uint32_t hw = __float_as_uint(__uint2float_rn(n));   // exact (n < 2^24)
-  const int b = static_cast<int>(hw >> 23) - 126;             // bit length of n
-  const int j = static_cast<int>((hw >> 14) & 511u);
-  const int e = b - 25 + (j >= 256 ? 1 : 0);
-  const float Mf = __uint_as_float((hw & 0x007FFFFFu) | (150u << 23));  // n in [2^23, 2^24)
-  const float2 tb = L->logt[j];
-  const float t = fmaf(Mf, tb.x, -1.0f);
-  const float lg = fmaf(t * t, fmaf(t, 1.0f / 3.0f, -0.5f), t);
-  const float Lw = fmaf(static_cast<float>(-e), 0.69314718f, tb.y - lg);
-  const float x = Lw + Lw;
-  const float r = x * rsqrtf(x);
-  return k == 0 ? 0.0f : r;
+// float32 fast functions for the bfloat16 path: the same reductions as
+// r_fast / c_fast in float32 arithmetic (~2^-21), calibrated exhaustively like
+// the float64 ones.  Tables (NormalLut32): logt[j] = (-2 mult_j 2^-23,
+// 2 ln(inv_j)) (+2^-100 at j = 0), trig[i] = (cos, sin)(i pi/1024).
+__device__ __forceinline__ float r32_fast(uint32_t w0, const NormalLut32* L) {
+  const uint32_t hw = __float_as_uint(__uint2float_rn(0x1000000u - (w0 >> 8)));  // n, exact
+  const float2 tb = lut_at(L->logt, (hw >> 11) & 0xFF8u);                         // j = hw[22:14]
+  const float s = fmaf(__uint_as_float((hw & 0x007FFFFFu) | 0x4B000000u), tb.x, 2.0f);  // -2t
+  const float g = fmaf(s * s, fmaf(s, 1.0f / 12.0f, 0.25f), s);                   // -2 log1p(t)
+  const float e = __uint_as_float(0x4B000000u | ((hw + 0x400000u) >> 23)) - 8388759.0f;  // e, exact
+  const float X = fmaf(e, -1.38629436f, tb.y + g);                                // -2 ln w
+  float h;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(h) : "f"(X));
+  return X * h;
 }
 
-// float32 c: nearest point of the pi/1024 table + residual to d^2 / d^3.
-__device__ __forceinline__ float c32_fast(uint32_t k, const NormalLut32* L) {
-  const uint32_t i = (k + 4096u) >> 13;
-  const uint32_t dj4 = k + 4096u - (i << 13);                  // dj + 4096 in [0, 8191]
-  const float d = (__uint_as_float(0x4B000000u | dj4) - 8392704.0f) * 3.74507039e-7f;  // exact dj, *2pi/2^24
-  const float d2 = d * d;
-  const float cm = -0.5f * d2;
-  const float sd = d * fmaf(d2, -1.0f / 6.0f, 1.0f);
-  const float2 cs = L->trig[i];
-  return cs.x + fmaf(cs.x, cm, -cs.y * sd);
+__device__ __forceinline__ float c32_fast(uint32_t w1, const NormalLut32* L) {
+  const uint32_t u = w1 + 0x100000u;
+  const float2 cs = lut_at(L->trig, (u >> 18) & 0x3FF8u);
+  const float d = __uint_as_float(((u >> 8) & 0x1FFFu) | 0x4B000000u) - 8392704.0f;  // exact
+  const float d2 = d * d;                                                         // exact
+  const float cm = d2 * static_cast<float>(-0.5 * kK1 * kK1);
+  const float sd = d * fmaf(d2, static_cast<float>(-kK1 * kK1 * kK1 / 6.0), static_cast<float>(kK1));
+  return fmaf(-cs.y, sd, fmaf(cs.x, cm, cs.x));
 }
 
 template <int DT>
@@ -451,14 +434,16 @@ __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLu
   uint32_t badmask = 0;
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
-    const float r = r32_fast(w0[e] >> 8, L32), c = c32_fast(w1[e] >> 8, L32);
-    const float z = __fmul_rn(r, c);
-    const float v = __fmaf_rn(P.nm.std32, z, P.nm.mean32);
-    // |v - v_numpy| <= r*b32_r + |v|*2^-23 + b32_c   (host: bound terms)
-    const float B = fmaf(r, P.nm.b32_r, fmaf(fabsf(v), 0x1p-23f, P.nm.b32_c));
-    const uint16_t lo = bf16_bits(__fsub_rd(v, B)), hi = bf16_bits(__fadd_ru(v, B));
-    out[e] = lo;
-    badmask |= (lo == hi) ? 0u : (1u << e);
+    const float r = r32_fast(w0[e], L32), c = c32_fast(w1[e], L32);
+    const float v = fmaf(P.nm.std32, r * c, P.nm.mean32);
+    // |v - v_numpy| <= r*b32_r + |v|*2^-22 + b32_c   (host: bound terms)
+    const float B = fmaf(r, P.nm.b32_r, fmaf(fabsf(v), 0x1p-22f, P.nm.b32_c));
+    // bf16(RN32(.)) is monotone: [v-B, v+B] rounds to one bfloat16 iff both ends do
+    const __nv_bfloat162 pk = __floats2bfloat162_rn(__fsub_rd(v, B), __fadd_ru(v, B));
+    uint32_t lh;
+    memcpy(&lh, &pk, 4);
+    out[e] = static_cast<uint16_t>(lh);
+    badmask |= ((lh ^ (lh >> 16)) & 0xFFFFu) ? (1u << e) : 0u;
   }
   if (__builtin_expect(badmask != 0, 0)) {
     // float64 certified path (tables read through L1/L2), then the exact NumPy tables
@@ -468,71 +453,71 @@ __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLu
   }
 }
 
+// Exact Normal (rng.py:150-156) from the NumPy tables: float64 Box-Muller with
+// the reference's own r[k1], c[k2], then one cast.
+template <int DT>
+__device__ __forceinline__ typename St<DT>::T normal_exact(const DistP& P, uint32_t w0, uint32_t w1) {
+  const double r = __ldg(P.nm.rtab + (w0 >> 8)), c = __ldg(P.nm.ctab + (w1 >> 8));
+  return from_f64<DT>(__dadd_rn(P.mean, __dmul_rn(P.stdv, __dmul_rn(r, c))));
+}
+
+// Certified fast value: v = fma(std r, c, mean) and |v_numpy - v| <= B; if the
+// monotone cast R to DT gives R(v - B) == R(v + B) that is the reference's
+// value, else ok = false.
+template <int DT>
+__device__ __forceinline__ typename St<DT>::T normal_certified(const DistP& P, double rs, double c,
+                                                               bool& ok) {
+  const double v = fma(rs, c, P.mean);
+  const double B = fma(rs, P.nm.kr, fma(fabs(v), 0x1p-51, P.nm.k0));
+  const auto lo = from_f64<DT>(v - B), hi = from_f64<DT>(v + B);
+  if constexpr (DT == SDR_F32) ok = __float_as_uint(lo) == __float_as_uint(hi);
+  else ok = lo == hi;
+  return lo;
+}
+
 // Normal (rng.py:150-156): float64 Box-Muller then one cast.  Fast path with
 // the table functions + a rigorous error bound; elements whose rounding to DT
 // the bound cannot certify recompute from the exact NumPy tables.
 template <int DT>
 __device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, const NormalLut* L,
                                                            uint32_t w0, uint32_t w1) {
-  const uint32_t k1 = w0 >> 8, k2 = w1 >> 8;
   if constexpr (DT != SDR_F64) {
-    const double r = r_fast(k1, L), c = c_fast(k2, L);
-    const double z = __dmul_rn(r, c);
-    const double s = __dmul_rn(P.stdv, z);
-    const double v = __dadd_rn(P.mean, s);
-    // |v_numpy - v| <= r*|std|*(Er + Ac(1+Er) + 5u) + 2u|v|, doubled (host: bound_r)
-    const double B = fma(r, P.nm.bound_r, fabs(v) * 0x1p-51) + 0x1p-1060;
-    const auto lo = from_f64<DT>(v - B), hi = from_f64<DT>(v + B);
     bool ok;
-    if constexpr (DT == SDR_F32) ok = __float_as_uint(lo) == __float_as_uint(hi);
-    else ok = lo == hi;
-    if (__builtin_expect(ok, 1)) return lo;
+    const auto v = normal_certified<DT>(P, r_fast(w0, L, P.nm.nh, P.nm.th), c_fast(w1, L), ok);
+    if (__builtin_expect(ok, 1)) return v;
     atomicAdd(P.nm.fallbacks, 1ull);
   }
-  const double r = __ldg(P.nm.rtab + k1), c = __ldg(P.nm.ctab + k2);
-  const double z = __dmul_rn(r, c);
-  const double v = __dadd_rn(P.mean, __dmul_rn(P.stdv, z));
-  return from_f64<DT>(v);
+  return normal_exact<DT>(P, w0, w1);
 }
 
 // A whole chunk of normals, phase by phase (all r, all c, then combine and
-// certify) so the 8 independent float64 chains interleave; one branch for the
+// certify) so the independent float64 chains interleave; one branch for the
 // rare uncertified elements.
 template <int DT, int NE>
 __device__ __forceinline__ void normal_chunk(const DistP& P, const NormalLut* L, const uint32_t* w0,
                                              const uint32_t* w1, typename St<DT>::T* out) {
-  double r[NE], c[NE];
+  double rs[NE], c[NE];
 #pragma unroll
-  for (int e = 0; e < NE; ++e) r[e] = r_fast(w0[e] >> 8, L);
+  for (int e = 0; e < NE; ++e) rs[e] = r_fast(w0[e], L, P.nm.nh, P.nm.th);
 #pragma unroll
-  for (int e = 0; e < NE; ++e) c[e] = c_fast(w1[e] >> 8, L);
-  bool bad = false;
+  for (int e = 0; e < NE; ++e) c[e] = c_fast(w1[e], L);
   uint32_t badmask = 0;
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
-    const double z = __dmul_rn(r[e], c[e]);
-    const double v = __dadd_rn(P.mean, __dmul_rn(P.stdv, z));
-    const double B = fma(r[e], P.nm.bound_r, fabs(v) * 0x1p-51) + 0x1p-1060;
-    const auto lo = from_f64<DT>(v - B), hi = from_f64<DT>(v + B);
     bool ok;
-    if constexpr (DT == SDR_F32) ok = __float_as_uint(lo) == __float_as_uint(hi);
-    else ok = lo == hi;
-    out[e] = lo;
+    out[e] = normal_certified<DT>(P, rs[e], c[e], ok);
     badmask |= ok ? 0u : (1u << e);
   }
-  bad = badmask != 0;
-  if (__builtin_expect(bad, 0)) {
+  if (__builtin_expect(badmask != 0, 0)) {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       if (badmask & (1u << e)) {
         atomicAdd(P.nm.fallbacks, 1ull);
-        const double rr = __ldg(P.nm.rtab + (w0[e] >> 8)), cc = __ldg(P.nm.ctab + (w1[e] >> 8));
-        out[e] = from_f64<DT>(__dadd_rn(P.mean, __dmul_rn(P.stdv, __dmul_rn(rr, cc))));
+        out[e] = normal_exact<DT>(P, w0[e], w1[e]);
       }
     }
   }
 }
-
 // Stage the Normal tables in shared memory (whole CTA participates).
 template <typename LUT>
 __device__ __forceinline__ void stage_lut(LUT* dst, const LUT* src) {
@@ -1031,7 +1016,9 @@ __global__ void k_philox_blocks(const uint64_t* tau, const uint64_t* beta, int64
   words[4 * i + 3] = x3;
 }
 
-// Exhaustive calibration of the Normal fast path against the NumPy tables.
+// Exhaustive calibration of the Normal fast path against the NumPy tables:
+// max relative error of r_fast (k >= 1; k = 0 must give r <= 2^-490), max
+// absolute error of c_fast, and the same for the float32 functions.
 __global__ void k_normal_calibrate(const double* rtab, const double* ctab, const NormalLut* lut,
                                    const NormalLut32* lut32, unsigned long long* max_r_bits,
                                    unsigned long long* max_c_bits) {
@@ -1039,21 +1026,22 @@ __global__ void k_normal_calibrate(const double* rtab, const double* ctab, const
   stage_lut(&s_lut, lut);  // the float32 tables are read from global memory here
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= (1u << 24)) return;
-  const double rg = r_fast(k, &s_lut), rn = rtab[k];
+  const double inf = __longlong_as_double(0x7FF0000000000000ll);
+  const double rg = r_fast(k << 8, &s_lut, -0.5, 1.5), rn = rtab[k];
   double er;
-  if (rg == 0.0 || rn == 0.0) er = (rg == rn) ? 0.0 : __longlong_as_double(0x7FF0000000000000ll);
-  else er = fabs(rg - rn) / rg;
-  const double ec = fabs(c_fast(k, &s_lut) - ctab[k]);
-  const double r32 = r32_fast(k, lut32);
+  if (k == 0) er = (rn == 0.0 && rg >= 0.0 && rg <= 0x1p-490) ? 0.0 : inf;
+  else er = (rg > 0.0 && rn > 0.0) ? fabs(rg - rn) / rg : inf;
+  const double ec = fabs(c_fast(k << 8, &s_lut) - ctab[k]);
+  const double r32 = r32_fast(k << 8, lut32);
   double er32;
-  if (r32 == 0.0 || rn == 0.0) er32 = (r32 == rn) ? 0.0 : __longlong_as_double(0x7FF0000000000000ll);
-  else er32 = fabs(r32 - rn) / r32;
-  const double ec32 = fabs(static_cast<double>(c32_fast(k, lut32)) - ctab[k]);  // absolute
+  if (k == 0) er32 = (r32 >= 0.0 && r32 <= 0x1p-49) ? 0.0 : inf;
+  else er32 = (r32 > 0.0 && rn > 0.0) ? fabs(r32 - rn) / r32 : inf;
+  const double ec32 = fabs(static_cast<double>(c32_fast(k << 8, lut32)) - ctab[k]);  // absolute
   unsigned long long b[4] = {static_cast<unsigned long long>(__double_as_longlong(er)),
                              static_cast<unsigned long long>(__double_as_longlong(ec)),
                              static_cast<unsigned long long>(__double_as_longlong(er32)),
                              static_cast<unsigned long long>(__double_as_longlong(ec32))};
-  // Non-negative doubles order like their bit patterns; reduce per warp first.
+  // Non-negative doubles order like their bit patterns (NaN above inf); reduce per warp first.
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     for (int o = 16; o > 0; o >>= 1) b[i] = max(b[i], __shfl_xor_sync(0xffffffffu, b[i], o));
@@ -1219,20 +1207,31 @@ static void build_normal_lut(NormalLut& L) {
       inv = round_sig(1.0L / mc, 20);
       mult = inv / 2.0L;
     }
-    L.logt[j].x = static_cast<double>(ldexpl(mult, -23));
-    L.logt[j].y = (inv == 1.0L) ? 0.0 : static_cast<double>(logl(inv));
+    L.logt[j].x = static_cast<double>(-2.0L * ldexpl(mult, -23));
+    L.logt[j].y = (inv == 1.0L) ? 0.0 : static_cast<double>(2.0L * logl(inv));
   }
+  L.logt[0].y = 0x1p-1000;
   const long double pi = 3.141592653589793238462643383279502884L;
-  for (int i = 0; i <= 2048; ++i) {
+  for (int i = 0; i < 2048; ++i) {
     const long double a = pi * i / 1024.0L;
     L.trig[i].x = static_cast<double>(cosl(a));
     L.trig[i].y = static_cast<double>(sinl(a));
   }
   // exact table points
-  L.trig[512].x = 0.0;
-  L.trig[1024].y = 0.0;
-  L.trig[1536].x = 0.0;
-  L.trig[2048].y = 0.0;
+  L.trig[0] = make_double2(1.0, 0.0);
+  L.trig[512] = make_double2(0.0, 1.0);
+  L.trig[1024] = make_double2(-1.0, 0.0);
+  L.trig[1536] = make_double2(0.0, -1.0);
+}
+
+// float32 tables of the bfloat16 path: the float64 layout rounded (the logt.x
+// entries are exact: 20-bit mult).
+static void build_normal_lut32(const NormalLut& h, NormalLut32& L) {
+  for (int j = 0; j < 512; ++j)
+    L.logt[j] = make_float2(static_cast<float>(h.logt[j].x), static_cast<float>(h.logt[j].y));
+  L.logt[0].y = 0x1p-100f;
+  for (int i = 0; i < 2048; ++i)
+    L.trig[i] = make_float2(static_cast<float>(h.trig[i].x), static_cast<float>(h.trig[i].y));
 }
 static NormalState g_nm[64];
 
@@ -1266,24 +1265,30 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
       P.nm.ctab = g_nm[device].ctab;
       P.nm.lut = g_nm[device].lut;
       P.nm.lut32 = g_nm[device].lut32;
-      P.nm.err_r = g_nm[device].err_r;
-      P.nm.err_c = g_nm[device].err_c;
       {
-        const double Er = P.nm.err_r, Ac = P.nm.err_c, u = 0x1p-53;
-        P.nm.bound_r = 2.0 * fabs(P.stdv) * (Er + Ac * (1.0 + Er) + 5.0 * u) * (1.0 + 0x1p-40);
-        // float32 path: |v32 - v_np| <= |std| r (Er32 + Ac32 + 2^-22) + 2^-23 |mean| + 2^-23 |v|,
-        // doubled (rounding of the bound itself, second-order terms).
+        // float64 fast path (see normal_certified): with Er, Ec the calibrated
+        // errors of r_fast / c_fast and u = 2^-53,
+        //   |v - v_np| <= 2.03u|v| + (std r)(Er' + Ec(1 + Er') + 2.01u)/(1 - Er'),
+        // Er' = Er/(1-Er) + 8u (std folded into the Newton step); doubled.
+        // k = 0 (r_np = 0, r_fast <= 2^-490) is covered by k0.
+        const double u = 0x1p-53, Er = g_nm[device].err_r, Ec = g_nm[device].err_c;
+        const double Erp = (Er / (1.0 - Er) + 8.0 * u) * (1.0 + 0x1p-30);
+        P.nm.nh = -0.5 * P.stdv;
+        P.nm.th = 1.5 * P.stdv;
+        P.nm.kr = 2.0 * (Erp + Ec * (1.0 + Erp) + 2.01 * u) / (1.0 - Erp) * (1.0 + 0x1p-30);
+        P.nm.k0 = 2.0 * fabs(P.stdv) * 0x1p-489 + 0x1p-1060;
+        if (!(Er < 0x1p-20) || !(Ec < 0x1p-20)) P.nm.kr = INFINITY;  // calibration failed: exact path
+        // float32 path (bfloat16 outputs): Er32, Ec32 the calibrated errors of
+        // r32_fast / c32_fast;  |v32 - v_np| <= |std| r (Er32 + Ec32(1+Er32) + 2^-23)
+        // + 2^-24 (|v32| + |mean|) + |std| 2^-49 (k = 0), doubled.
         const double Er32 = g_nm[device].err_r32, Ac32 = g_nm[device].err_c32;
         P.nm.err_r32 = Er32;
         P.nm.err_c32 = Ac32;
         P.nm.mean32 = static_cast<float>(P.mean);
         P.nm.std32 = static_cast<float>(P.stdv);
-        // |v32 - v_np| <= |std32 z32| (Er32 + Ec32 + 2^-23) + 2^-24 |v32| + 2^-24 |mean32|,
-        // x1.02 for second-order terms and the rounding of the bound itself
-        // (kernel adds |v| 2^-23 = 2 x the 2^-24 term).
-        P.nm.b32_r = static_cast<float>(1.02 * fabs(static_cast<double>(P.nm.std32)) *
-                                        (Er32 * (1.0 + Ac32) + Ac32 + 0x1p-23) + 0x1p-60);
-        P.nm.b32_c = static_cast<float>(1.02 * 0x1p-24 * fabs(P.mean) + 0x1p-140);
+        P.nm.b32_r = static_cast<float>(2.04 * fabs(P.stdv) * (Er32 + Ac32 * (1.0 + Er32) + 0x1p-23) + 0x1p-60);
+        P.nm.b32_c = static_cast<float>(2.04 * 0x1p-24 * fabs(P.mean) + 2.0 * fabs(P.stdv) * 0x1p-48 + 0x1p-140);
+        if (!(Er32 < 0x1p-12) || !(Ac32 < 0x1p-12)) P.nm.b32_r = INFINITY;  // calibration failed
       }
       P.nm.fallbacks = g_nm[device].fallbacks;
       break;
@@ -1497,10 +1502,7 @@ int normal_tables_load(int device, const double* r_host, const double* c_host, d
       NormalLut h;
       build_normal_lut(h);
       NormalLut32 h32;
-      for (int j = 0; j < 512; ++j) h32.logt[j] = make_float2(static_cast<float>(h.logt[j].x),
-                                                              static_cast<float>(h.logt[j].y));
-      for (int i = 0; i <= 2048; ++i) h32.trig[i] = make_float2(static_cast<float>(h.trig[i].x),
-                                                                static_cast<float>(h.trig[i].y));
+      build_normal_lut32(h, h32);
       e = cudaMemcpy(S.lut, &h, sizeof(NormalLut), cudaMemcpyHostToDevice);
       if (e == cudaSuccess) e = cudaMemcpy(S.lut32, &h32, sizeof(NormalLut32), cudaMemcpyHostToDevice);
     }
@@ -1529,18 +1531,6 @@ int normal_tables_load(int device, const double* r_host, const double* c_host, d
   if (er) *er = S.err_r;
   if (ec) *ec = S.err_c;
   return SDR_OK;
-}
-
-// Host evaluation of the fast functions (accuracy harness in tools/).
-void normal_fast_host(uint32_t k, double* r, double* c) {
-  static NormalLut L;
-  static bool built = false;
-  if (!built) {
-    build_normal_lut(L);
-    built = true;
-  }
-  *r = r_fast(k, &L);
-  *c = c_fast(k, &L);
 }
 
 int normal_tables_loaded(int device) {
