@@ -211,42 +211,42 @@ def run_ours(a):
             xb = torch.randn((SHAPE[1], SHAPE[2]), generator=gen, device=dev, dtype=torch.bfloat16)
             x[b].copy_(xb[s0:s0 + n])
             del xb
-    y = torch.empty_like(x)
     n_local = x.numel()
     local_bytes = n_local * BYTES_PER_ELEM
+    # Rotate over enough (x, y) buffer pairs that the footprint exceeds 3x L2:
+    # every step reads an x that is not L2-resident (no flush kernel needed),
+    # and the K steps run back to back between one pair of events.
     l2_bytes = 126 * 1024 * 1024
-    need_flush = x.numel() * 2 < 2 * l2_bytes
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev) if need_flush else None
+    nbuf = max(1, math.ceil(3 * l2_bytes / local_bytes))  # local_bytes = x + y bytes
+    xs = [x] + [x.clone() for _ in range(nbuf - 1)]
+    ys = [torch.empty_like(x) for _ in range(nbuf)]
     stream = torch.cuda.current_stream(dev)
     state = R.RngState(SEED, 0, 65536)
 
-    def step():
-        ops.dropout_apply(x, P_DROP, state, view, out=y)
+    def step(i):
+        ops.dropout_apply(xs[i % nbuf], P_DROP, state, view, out=ys[i % nbuf])
         state.advance(math.prod(SHAPE))  # every rank, no communication (rng.py:95-98)
 
-    for _ in range(a.warmup):
-        step()
+    for i in range(a.warmup):
+        step(i)
     torch.cuda.synchronize(dev)
 
     # --- timed region: K steps, barrier + synchronize on both sides ---------
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     with ClockSampler(local) as clk:
+        t0.record(stream)
         for i in range(a.steps):
-            if flush is not None:
-                flush.fill_(i & 0xFF)  # evict x / y from L2 between timed steps (untimed)
-            starts[i].record(stream)
-            step()
-            ends[i].record(stream)
+            step(i)
+        t1.record(stream)
         torch.cuda.synchronize(dev)
         if ws > 1:
             dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    ms_local = sum(step_ms) / len(step_ms)
+    ms_local = t0.elapsed_time(t1) / a.steps
     clocks = clk.summary()
+    y = ys[0]
 
     # --- e2e through the public API with host buffers -------------------------
     xh = x.cpu().pin_memory()
@@ -327,8 +327,9 @@ def run_ours(a):
             "config": {"workload": "cfg2: dropout p=0.1 on bf16 [8,4096,4096], Shard(1) sequence-parallel",
                        "global_shape": list(SHAPE), "p": P_DROP, "placement": "S(1)",
                        "parallelism": f"sp{ws}", "per_gpu_elements": n_local,
-                       "l2": "flushed between timed steps (256 MiB write)" if need_flush
-                             else "input 268 MB > 126 MB L2 (no flush needed)",
+                       "l2": f"{nbuf} rotating x/y buffer pair(s), {nbuf * local_bytes // 2**20} MiB "
+                             f"footprint > 3x the 126 MB L2 (no step reads an L2-resident x)",
+                       "timing": "one CUDA-event pair around the K back-to-back steps on the launch stream",
                        "per_gpu_gbs": round(gbs / ws, 3),
                        "elements_per_s": round(total_elems / (ms * 1e-3), 1)},
             "roofline": {
@@ -346,7 +347,7 @@ def run_ours(a):
             "e2e": {"value": round(e2e_gbs, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": xh.numel() * xh.element_size(),
                     "d2h_bytes_per_step": yh.numel() * yh.element_size(),
-                    "how": "paper_2509_07003_b200.ops.dropout_host: pinned host x -> H2D | fused kernel | D2H y, 8-block 3-stream pipeline"},
+                    "how": "paper_2509_07003_b200.ops.dropout_host: pinned host x -> H2D | fused kernel | D2H y, tapered 16-block 3-stream pipeline"},
             "gpu_launches": a.steps,
             "clocks": clocks,
         }

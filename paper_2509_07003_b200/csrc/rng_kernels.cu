@@ -319,6 +319,12 @@ __constant__ double c_npoly[9] = {
 #ifndef SDR_R_NEWTON2
 #define SDR_R_NEWTON2 0   // second Newton step for r (fewer certification fallbacks)
 #endif
+#ifndef SDR_R32_NEWTON
+#define SDR_R32_NEWTON 0  // Newton step on the float32 rsqrt seed (fewer float64 fallbacks)
+#endif
+#ifndef SDR_COUNT_F32_MISS
+#define SDR_COUNT_F32_MISS 0  // A/B diagnostics: count float32-path misses as fallbacks
+#endif
 #ifndef SDR_FILL_MINB
 #define SDR_FILL_MINB 2   // CTAs/SM the register budget of the fill kernels is sized for
 #endif
@@ -411,7 +417,12 @@ __device__ __forceinline__ float r32_fast(uint32_t w0, const NormalLut32* L) {
   const float X = fmaf(e, -1.38629436f, tb.y + g);                                // -2 ln w
   float h;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(h) : "f"(X));
+#if SDR_R32_NEWTON
+  const float gx = X * h;
+  return gx * fmaf(gx * h, -0.5f, 1.5f);
+#else
   return X * h;
+#endif
 }
 
 __device__ __forceinline__ float c32_fast(uint32_t w1, const NormalLut32* L) {
@@ -446,6 +457,9 @@ __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLu
     badmask |= ((lh ^ (lh >> 16)) & 0xFFFFu) ? (1u << e) : 0u;
   }
   if (__builtin_expect(badmask != 0, 0)) {
+#if SDR_COUNT_F32_MISS
+    atomicAdd(P.nm.fallbacks, static_cast<unsigned long long>(__popc(badmask)));
+#endif
     // float64 certified path (tables read through L1/L2), then the exact NumPy tables
 #pragma unroll
     for (int e = 0; e < NE; ++e)
@@ -604,6 +618,25 @@ __device__ __forceinline__ void load_chunk(const T* p, T (&v)[N]) {
   }
 }
 
+// Global flat index of chunk q (CH elements inside one row of the canonical
+// view, nd >= 1): row/column by the launch-constant chunks-per-row divisor, the
+// inner outer-dims by their sizes; the outermost digit needs no division (the
+// row index is below its extent).
+__device__ __forceinline__ uint64_t outer_base(const ViewIndexer& ix, const FastDiv64& div_cpr,
+                                               uint64_t q, int CH) {
+  uint64_t row, cq;
+  div_cpr.divmod(q, row, cq);
+  const CanonView& cv = ix.cv;
+  uint64_t j = static_cast<uint64_t>(cv.base) + cq * CH;
+  for (int k = cv.nd - 1; k >= 1; --k) {
+    uint64_t qq, r;
+    ix.div_o[k].divmod(row, qq, r);
+    j += r * static_cast<uint64_t>(cv.ostride[k]);
+    row = qq;
+  }
+  return j + row * static_cast<uint64_t>(cv.ostride[0]);
+}
+
 // ---------------------------------------------------------------------------
 // Fill kernels.
 // ---------------------------------------------------------------------------
@@ -622,17 +655,7 @@ struct __align__(16) FillArgs {
 // Global flat index of the first element of chunk q (fast path).
 __device__ __forceinline__ uint64_t chunk_base(const FillArgs& A, uint64_t q) {
   if (A.ix.cv.nd == 0) return static_cast<uint64_t>(A.ix.cv.base) + q * kV;  // one contiguous run
-  uint64_t row, cq;
-  A.div_cpr.divmod(q, row, cq);
-  uint64_t j = static_cast<uint64_t>(A.ix.cv.base) + cq * kV;
-  const CanonView& cv = A.ix.cv;
-  for (int k = cv.nd - 1; k >= 0; --k) {
-    uint64_t qq, r;
-    A.ix.div_o[k].divmod(row, qq, r);
-    j += r * static_cast<uint64_t>(cv.ostride[k]);
-    row = qq;
-  }
-  return j;
+  return outer_base(A.ix, A.div_cpr, q, kV);
 }
 
 template <int DIST, int DT, bool ALIGNED>
@@ -844,16 +867,7 @@ constexpr int kDropCh = SDR_DROP_CH;
 __device__ __forceinline__ uint64_t drop_chunk_base(const DropArgs& A, uint64_t q) {
   const CanonView& cv = A.ix.cv;
   if (cv.nd == 0) return static_cast<uint64_t>(cv.base) + q * kDropCh;  // one contiguous run
-  uint64_t row, cq;
-  A.div_cpr.divmod(q, row, cq);
-  uint64_t j = static_cast<uint64_t>(cv.base) + cq * kDropCh;
-  for (int k = cv.nd - 1; k >= 0; --k) {
-    uint64_t qq, r;
-    A.ix.div_o[k].divmod(row, qq, r);
-    j += r * static_cast<uint64_t>(cv.ostride[k]);
-    row = qq;
-  }
-  return j;
+  return outer_base(A.ix, A.div_cpr, q, kDropCh);
 }
 
 

@@ -190,6 +190,7 @@ def dtensor_dropout(x, p: float, state: RngState | None = None, ledger=None, *, 
 # Host-buffer dropout: pipelined H2D -> fused kernel -> D2H.
 # ---------------------------------------------------------------------------
 _PIPE: dict = {}
+_PIPE_NBUF = 3  # device staging buffers per direction in dropout_host
 
 
 def _pipe_state(device, nbytes_in, nbytes_out, dtype_in, dtype_out, nbuf):
@@ -205,17 +206,71 @@ def _pipe_state(device, nbytes_in, nbytes_out, dtype_in, dtype_out, nbuf):
     return st
 
 
+def _host_blocks(shape, view: ShardView, chunks: int):
+    """Cut a window into contiguous product sub-windows for the host pipeline.
+    The window is walked as R "rows" (dim-0 indices, or dim-0 x dim-1 indices
+    when dim 1 is a plain range); blocks grow from R/chunks rows by doubling to
+    R/8 and shrink the same way at the end, so the pipeline fill (first H2D)
+    and drain (last D2H) are short while the middle needs few copies.  A block
+    never straddles a dim-0 index unless it spans whole dim-0 rows.  Yields
+    (index tuple, sub-view)."""
+    from .placement import DimWindow
+    wins = tuple(view.windows)
+    if not shape or shape[0] == 0 or wins[0].groups != 1 or math.prod(shape) == 0:
+        yield (slice(None),), view
+        return
+    L = shape[1] if len(shape) >= 2 and wins[1].groups == 1 and shape[1] >= 2 else 1
+    R = shape[0] * L
+    unit = max(1, R // max(1, chunks))
+    big = max(unit, R // 8)
+    head = []
+    s = unit
+    while sum(head) + s <= R // 2 and s < big:
+        head.append(s)
+        s *= 2
+    H = sum(head)
+    step = max(L, big // L * L) if L > 1 else big
+    pts = {0, R}
+    acc = 0
+    for n in head:
+        acc += n
+        pts.update((acc, R - acc))
+    pts.update(range(-(-H // step) * step, R - H, step))
+    pts = sorted(p for p in pts if 0 <= p <= R)
+    cuts = []
+    for a, b in zip(pts, pts[1:]):
+        while a < b:  # split at dim-0 boundaries unless spanning whole dim-0 rows
+            if L > 1 and (a % L or b - a < L):
+                e = min(b, (a // L + 1) * L)
+            elif L > 1:
+                e = b - b % L
+            else:
+                e = b
+            cuts.append((a, e))
+            a = e
+    for a, b in cuts:
+        if L == 1 or (a % L == 0 and b % L == 0):
+            r0, r1 = a // L, b // L
+            yield (slice(r0, r1),), ShardView(view.global_shape,
+                                              windows=(DimWindow(wins[0].start + r0, r1 - r0),) + wins[1:])
+        else:
+            r, c0, c1 = a // L, a % L, b - (a // L) * L
+            yield (slice(r, r + 1), slice(c0, c1)), ShardView(
+                view.global_shape, windows=(DimWindow(wins[0].start + r, 1),
+                                            DimWindow(wins[1].start + c0, c1 - c0)) + wins[2:])
+
+
 def dropout_host(x_host: torch.Tensor, p: float, state: RngState, view: ShardView | None = None, *,
                  out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None,
-                 device=None, chunks: int = 8) -> torch.Tensor:
+                 device=None, chunks: int = 16) -> torch.Tensor:
     """dropout_apply for a tensor in (pinned) HOST memory, result in host
-    memory.  The window is cut into `chunks` row blocks along its first dim;
-    block i's H2D copy, block i-1's fused kernel and block i-2's D2H copy run
-    concurrently on three streams (PCIe is full duplex), so the end-to-end
-    time approaches max(H2D, D2H) instead of their sum.  Values are identical
-    to dropout_apply (each block is a sub-window of the same global draw).
-    Does NOT advance `state`.  Blocks the host until the result is ready."""
-    from .placement import DimWindow
+    memory.  The window is cut into contiguous blocks of 1/chunks .. 1/8 of it
+    (_host_blocks, tapered at both ends); block i's H2D copy, block i-1's fused kernel and block
+    i-2's D2H copy run concurrently on three streams (PCIe is full duplex), so
+    the end-to-end time approaches max(H2D, D2H) instead of their sum.  Values
+    are identical to dropout_apply (each block is a sub-window of the same
+    global draw).  Does NOT advance `state`.  Blocks the host until the result
+    is ready."""
     if x_host.is_cuda:
         raise ValueError("dropout_host expects a host tensor; use dropout_apply for device tensors")
     view = full_view(tuple(x_host.shape)) if view is None else view
@@ -226,44 +281,39 @@ def dropout_host(x_host: torch.Tensor, p: float, state: RngState, view: ShardVie
     if out is None:
         out = torch.empty(x_host.shape, dtype=yd, pin_memory=True)
     x_host = x_host.contiguous()
-    rows = x_host.shape[0] if x_host.dim() else 1
-    w0 = view.windows[0] if view.windows else None
-    if x_host.dim() == 0 or rows == 0 or w0.groups != 1:
-        chunks = 1
-    chunks = max(1, min(chunks, rows))
-    per = -(-rows // chunks)
-    row_in = x_host[0].numel() * x_host.element_size() if x_host.dim() else x_host.element_size()
-    row_out = row_in // x_host.element_size() * torch.empty((), dtype=yd).element_size()
-    nbuf = 3
-    S = _pipe_state(dev, per * row_in, per * row_out, x_host.dtype, yd, nbuf)
+    if x_host.dim() == 0:
+        blocks = [((), view)]
+    else:
+        blocks = list(_host_blocks(tuple(x_host.shape), view, max(1, chunks)))
+    cap = max(int(x_host[ix].numel()) for ix, _ in blocks) if x_host.dim() else 1
+    nbuf = _PIPE_NBUF
+    S = _pipe_state(dev, cap * x_host.element_size(), cap * torch.empty((), dtype=yd).element_size(),
+                    x_host.dtype, yd, nbuf)
     cur = torch.cuda.current_stream(dev)
-    h2d_done = [torch.cuda.Event() for _ in range(chunks)]
-    comp_done = [torch.cuda.Event() for _ in range(chunks)]
     d2h_done = [None] * nbuf
     for s in (S["h2d"], S["comp"], S["d2h"]):
         s.wait_stream(cur)
-    for i in range(chunks):
-        r0, r1 = i * per, min(rows, (i + 1) * per)
-        if r0 >= r1:
-            break
+    for i, (ix, sub) in enumerate(blocks):
         b = i % nbuf
-        n_in, n_out = (r1 - r0) * row_in, (r1 - r0) * row_out
-        xin = S["xin"][b][:n_in].view(x_host.dtype).view((r1 - r0,) + tuple(x_host.shape[1:]))
-        yout = S["yout"][b][:n_out].view(yd).view(xin.shape)
+        xs = x_host[ix]
+        n = xs.numel()
+        if n == 0:
+            continue
+        xin = S["xin"][b][:n * x_host.element_size()].view(x_host.dtype).view(xs.shape)
+        yout = S["yout"][b][:n * out.element_size()].view(yd).view(xs.shape)
+        h2d_done, comp_done = torch.cuda.Event(), torch.cuda.Event()
         with torch.cuda.stream(S["h2d"]):
             if d2h_done[b] is not None:
                 S["h2d"].wait_event(d2h_done[b])  # buffer b free again
-            xin.copy_(x_host[r0:r1], non_blocking=True)
-            h2d_done[i].record(S["h2d"])
-        sub = ShardView(view.global_shape,
-                        windows=(DimWindow(w0.start + r0, r1 - r0),) + tuple(view.windows[1:]))
+            xin.copy_(xs, non_blocking=True)
+            h2d_done.record(S["h2d"])
         with torch.cuda.stream(S["comp"]):
-            S["comp"].wait_event(h2d_done[i])
+            S["comp"].wait_event(h2d_done)
             dropout_apply(xin, p, state, sub, out=yout, out_dtype=yd)
-            comp_done[i].record(S["comp"])
+            comp_done.record(S["comp"])
         with torch.cuda.stream(S["d2h"]):
-            S["d2h"].wait_event(comp_done[i])
-            out[r0:r1].copy_(yout, non_blocking=True)
+            S["d2h"].wait_event(comp_done)
+            out[ix].copy_(yout, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(S["d2h"])
             d2h_done[b] = ev

@@ -155,3 +155,9 @@ def test_dropout_host_pipeline_matches_device(dt, out_dtype):
         yh = ops.dropout_host(x, 0.3, st, v, out_dtype=out_dtype, chunks=chunks)
         yd = ops.dropout_apply(x.cuda(), 0.3, st, v, out_dtype=out_dtype)
         assert not yh.is_cuda and torch.equal(bits(yh), bits(yd.cpu())), chunks
+    # Shard(1) window (sequence parallel), blocks split along dim 1
+    v1 = local_shape_and_offset(ShardSpec(mesh, parse_placements("S(1)")), (6, 111, 64), (2,))
+    for chunks in (3, 32):
+        yh = ops.dropout_host(x, 0.3, st, v1, out_dtype=out_dtype, chunks=chunks)
+        yd = ops.dropout_apply(x.cuda(), 0.3, st, v1, out_dtype=out_dtype)
+        assert torch.equal(bits(yh), bits(yd.cpu())), chunks

@@ -174,3 +174,24 @@ def test_distribute_merge_roundtrip(pl, sizes):
         bad[k] = bad[k] + 1
         with pytest.raises(PlacementError):
             merge_local_tensors(spec, (8, 6), bad)
+
+
+def test_host_pipeline_blocks_tile_the_window():
+    """ops._host_blocks: every local element in exactly one block, each block a
+    sub-window at the right global offset."""
+    import numpy as np
+    from paper_2509_07003_b200 import ops
+    mesh = create_mesh([("sp", 3)])
+    for gshape, pl, chunks in [((18, 37, 64), "S(0)", 4), ((18, 37, 64), "S(0)", 100),
+                               ((6, 111, 64), "S(1)", 32), ((8, 512, 64), "S(1)", 32), ((5,), "S(0)", 3)]:
+        v = local_shape_and_offset(ShardSpec(mesh, parse_placements(pl)), gshape, (1,))
+        seen = np.zeros(v.local_shape, dtype=np.int32)
+        for ix, sub in ops._host_blocks(v.local_shape, v, chunks):
+            seen[ix] += 1
+            blk = seen[ix]
+            assert blk.shape == sub.local_shape
+            for d, w in enumerate(sub.windows):
+                s = ix[d] if d < len(ix) else slice(None)
+                start = (s.start or 0) if isinstance(s, slice) else s
+                assert w.start == v.windows[d].start + start
+        assert (seen == 1).all(), (gshape, pl, chunks)
