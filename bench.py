@@ -188,10 +188,18 @@ def run_ours(a):
     ws, rank, local = dist_env()
     if ws != a.gpus:
         raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={ws}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # Test hook: SDR_BENCH_SHARE_GPU=1 runs every rank on cuda:0 with gloo for the
+    # barriers / max-over-ranks (exercises the N-rank path on a 1-GPU box; the
+    # numbers are then not scaling numbers).
+    share = os.environ.get("SDR_BENCH_SHARE_GPU") == "1"
+    gpu = 0 if share else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     from paper_2509_07003_b200 import _lib, create_mesh, ops, rng as R
     from paper_2509_07003_b200.placement import ShardSpec, local_shape_and_offset, parse_placements
@@ -236,7 +244,7 @@ def run_ours(a):
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
+    with ClockSampler(gpu) as clk:
         t0.record(stream)
         for i in range(a.steps):
             step(i)
@@ -273,7 +281,7 @@ def run_ours(a):
     e2e_ms_local = sum(s.elapsed_time(e) for s, e in zip(e_starts, e_ends)) / a.steps
 
     # --- max over ranks -------------------------------------------------------
-    t = torch.tensor([ms_local, e2e_ms_local], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms_local, e2e_ms_local], dtype=torch.float64, device="cpu" if share else dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, e2e_ms = t.tolist()
@@ -292,7 +300,7 @@ def run_ours(a):
     hbm_src = "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback B200_PROFILING.md"
     import ctypes as C
     imad, lop3, phx = C.c_double(), C.c_double(), C.c_double()
-    _lib.check(_lib.LIB.sdr_probe_int32(local, C.byref(imad), C.byref(lop3), C.byref(phx)),
+    _lib.check(_lib.LIB.sdr_probe_int32(gpu, C.byref(imad), C.byref(lop3), C.byref(phx)),
                "sdr_probe_int32")
     # INT32 peak in Philox proportion: a memory-free Philox4x32-10 with every
     # counter word per-thread varying and all four words consumed (nothing to
