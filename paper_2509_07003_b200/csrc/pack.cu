@@ -10,8 +10,8 @@
 // rows in the packed buffer so NCCL sees equal-size rank segments.  For fixed
 // `outer` index both the tensor piece and its slot are one contiguous byte
 // span, so each (member, rank) pair is a batched 2-D copy ("job").  All jobs of
-// a call run in one launch: CTAs walk a global tile list (binary search on the
-// job prefix) and move 16 B vectors when the job is 16 B aligned.
+// a call run in one launch with one CTA per tile (binary search on the job
+// prefix), moving 16 B vectors when every job is 16 B aligned.
 #include <cstring>
 #include <vector>
 
@@ -26,47 +26,66 @@ struct CopyJob {
   int64_t span_bytes;   // bytes per span
   int64_t src_stride;   // bytes between spans in src
   int64_t dst_stride;   // bytes between spans in dst
-  int64_t tiles;        // tiles of kTileBytes covering nspans*span_bytes
+  int64_t tiles;        // tiles covering the job (see tile_geometry)
+  int64_t spt;          // spans per tile (>= 1; > 1 only when a span is < kTileBytes)
+  int64_t parts;        // tiles per span (>= 1; > 1 only when spt == 1)
   int32_t vec;          // 16, 8, 4 or 1: widest aligned access
   int32_t pad_;
 };
 
-constexpr int64_t kTileBytes = 32768;
+// A tile is <= kTileBytes of one job: `spt` whole spans when spans are short
+// (e.g. the 4 KiB half-rows of a Shard(1) bf16 [4096, 4096] weight), or one
+// kTileBytes part of a long span.  One CTA per tile: 256 threads x U vectors,
+// all loads issued before the stores; the CTA scheduler keeps a moving front
+// of tiles in flight (measured: 8 KiB tiles beat persistent, 32 KiB and TMA
+// bulk-copy variants on B200).
+constexpr int64_t kTileBytes = 8192;
 
-// Tiles never cross a span: tile t of a job is part (t % tiles_per_span) of
-// span (t / tiles_per_span), so the inner loop is a plain strided vector copy.
 template <typename V>
-__device__ __forceinline__ void copy_part(const unsigned char* __restrict__ src,
-                                          unsigned char* __restrict__ dst, int64_t nbytes) {
-  const int64_t n = nbytes / static_cast<int64_t>(sizeof(V));
-  const V* s = reinterpret_cast<const V*>(src);
-  V* d = reinterpret_cast<V*>(dst);
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) d[i] = s[i];
-}
-
-__global__ void __launch_bounds__(256) k_copy_jobs(const CopyJob* __restrict__ jobs,
-                                                   const int64_t* __restrict__ prefix, int n,
-                                                   int64_t ntiles) {
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    int lo = 0, hi = n - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (prefix[mid] <= t) lo = mid;
-      else hi = mid - 1;
+__global__ void __launch_bounds__(256) k_copy_tiles(const CopyJob* __restrict__ jobs,
+                                                    const int64_t* __restrict__ prefix, int n) {
+  constexpr int U = static_cast<int>(kTileBytes / (sizeof(V) * 256));
+  const int64_t t = blockIdx.x;
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (prefix[mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const CopyJob& J = jobs[lo];
+  const int64_t lt = t - prefix[lo];
+  int64_t s0, off, len;
+  int cnt;
+  if (J.spt > 1) {
+    s0 = lt * J.spt;
+    cnt = static_cast<int>(min(J.spt, J.nspans - s0));
+    off = 0;
+    len = J.span_bytes;
+  } else {
+    s0 = lt / J.parts;
+    cnt = 1;
+    off = (lt - s0 * J.parts) * kTileBytes;
+    len = min(kTileBytes, J.span_bytes - off);
+  }
+  const int lv = static_cast<int>(len / static_cast<int64_t>(sizeof(V)));
+  const int total = cnt * lv;
+  const unsigned char* src = J.src + s0 * J.src_stride + off;
+  unsigned char* dst = J.dst + s0 * J.dst_stride + off;
+  V v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int i = threadIdx.x + u * 256;
+    if (i < total) {
+      const int r = i / lv, c = i - r * lv;
+      v[u] = *reinterpret_cast<const V*>(src + r * J.src_stride + c * static_cast<int64_t>(sizeof(V)));
     }
-    const CopyJob& J = jobs[lo];
-    const int64_t tps = (J.span_bytes + kTileBytes - 1) / kTileBytes;  // tiles per span
-    const int64_t lt = t - prefix[lo];
-    const int64_t span = lt / tps, part = lt - span * tps;
-    const int64_t off = part * kTileBytes;
-    const int64_t len = min(kTileBytes, J.span_bytes - off);
-    const unsigned char* src = J.src + span * J.src_stride + off;
-    unsigned char* dst = J.dst + span * J.dst_stride + off;
-    switch (J.vec) {
-      case 16: copy_part<uint4>(src, dst, len); break;
-      case 8: copy_part<uint2>(src, dst, len); break;
-      case 4: copy_part<uint32_t>(src, dst, len); break;
-      default: copy_part<unsigned char>(src, dst, len); break;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int i = threadIdx.x + u * 256;
+    if (i < total) {
+      const int r = i / lv, c = i - r * lv;
+      *reinterpret_cast<V*>(dst + r * J.dst_stride + c * static_cast<int64_t>(sizeof(V))) = v[u];
     }
   }
 }
@@ -91,7 +110,15 @@ static void add_job(std::vector<CopyJob>& jobs, const void* src, void* dst, int6
   J.span_bytes = span_bytes;
   J.src_stride = src_stride;
   J.dst_stride = dst_stride;
-  J.tiles = nspans * ((span_bytes + kTileBytes - 1) / kTileBytes);
+  if (span_bytes < kTileBytes) {
+    J.spt = kTileBytes / span_bytes;
+    J.parts = 1;
+    J.tiles = (nspans + J.spt - 1) / J.spt;
+  } else {
+    J.spt = 1;
+    J.parts = (span_bytes + kTileBytes - 1) / kTileBytes;
+    J.tiles = nspans * J.parts;
+  }
   J.vec = widest({static_cast<int64_t>(reinterpret_cast<uintptr_t>(src)),
                   static_cast<int64_t>(reinterpret_cast<uintptr_t>(dst)), span_bytes, src_stride,
                   dst_stride});
@@ -117,12 +144,16 @@ static int run_jobs(const std::vector<CopyJob>& jobs, cudaStream_t s) {
     set_cuda_error(e);
     return SDR_E_CUDA;
   }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t cap = static_cast<int64_t>(sms) * 8;
-  const int grid = static_cast<int>(tiles < cap ? tiles : cap);
-  k_copy_jobs<<<grid, 256, 0, s>>>(d_jobs, d_prefix, n, tiles);
+  // vector width of the whole call: the narrowest job's (jobs are few and large)
+  int vec = 16;
+  for (const CopyJob& J : jobs) vec = J.vec < vec ? J.vec : vec;
+  const unsigned grid = static_cast<unsigned>(tiles);
+  switch (vec) {
+    case 16: k_copy_tiles<uint4><<<grid, 256, 0, s>>>(d_jobs, d_prefix, n); break;
+    case 8: k_copy_tiles<uint2><<<grid, 256, 0, s>>>(d_jobs, d_prefix, n); break;
+    case 4: k_copy_tiles<uint32_t><<<grid, 256, 0, s>>>(d_jobs, d_prefix, n); break;
+    default: k_copy_tiles<unsigned char><<<grid, 256, 0, s>>>(d_jobs, d_prefix, n); break;
+  }
   const int st = check_launch();
   cudaFreeAsync(d_jobs, s);
   cudaFreeAsync(d_prefix, s);
