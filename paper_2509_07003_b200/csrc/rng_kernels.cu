@@ -15,6 +15,7 @@
 // per element instead of 20 (the last round's M0 product is dead for every
 // distribution, which uses words 0-1 only).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -1326,6 +1327,12 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
         P.nm.b32_r = static_cast<float>(2.04 * fabs(P.stdv) * (Er32 + Ac32 * (1.0 + Er32) + 0x1p-23) + 0x1p-60);
         P.nm.b32_c = static_cast<float>(2.04 * 0x1p-24 * fabs(P.mean) + 2.0 * fabs(P.stdv) * 0x1p-48 + 0x1p-140);
         if (!(Er32 < 0x1p-12) || !(Ac32 < 0x1p-12)) P.nm.b32_r = INFINITY;  // calibration failed
+        // Test hook: SDR_NORMAL_PATH=exact sends every element through the NumPy
+        // tables, =f64 skips the float32 path (results must be identical).
+        if (const char* path = getenv("SDR_NORMAL_PATH")) {
+          if (strcmp(path, "exact") == 0) P.nm.kr = P.nm.b32_r = INFINITY;
+          if (strcmp(path, "f64") == 0) P.nm.b32_r = INFINITY;
+        }
       }
       P.nm.fallbacks = g_nm[device].fallbacks;
       break;
