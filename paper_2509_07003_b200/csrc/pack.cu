@@ -37,9 +37,12 @@ struct CopyJob {
 // (e.g. the 4 KiB half-rows of a Shard(1) bf16 [4096, 4096] weight), or one
 // kTileBytes part of a long span.  One CTA per tile: 256 threads x U vectors,
 // all loads issued before the stores; the CTA scheduler keeps a moving front
-// of tiles in flight (measured: 8 KiB tiles beat persistent, 32 KiB and TMA
-// bulk-copy variants on B200).
-constexpr int64_t kTileBytes = 8192;
+// of tiles in flight (measured: per-CTA tiles beat persistent grids and TMA
+// bulk-copy variants on B200; 16 KiB tiles reach the torch-copy rate, 6.3 TB/s).
+#ifndef SDR_COPY_TILE
+#define SDR_COPY_TILE 16384
+#endif
+constexpr int64_t kTileBytes = SDR_COPY_TILE;
 
 template <typename V>
 __global__ void __launch_bounds__(256) k_copy_tiles(const CopyJob* __restrict__ jobs,
@@ -69,25 +72,38 @@ __global__ void __launch_bounds__(256) k_copy_tiles(const CopyJob* __restrict__ 
   }
   const int lv = static_cast<int>(len / static_cast<int64_t>(sizeof(V)));
   const int total = cnt * lv;
-  const unsigned char* src = J.src + s0 * J.src_stride + off;
-  unsigned char* dst = J.dst + s0 * J.dst_stride + off;
+  // Thread element i = tid + 256u -> (span r, vector c), stepped incrementally:
+  // one division per thread, then +256 = (dr spans, dc vectors) with a carry.
+  const int dr = 256 / lv, dc = 256 - dr * lv;
+  int r = threadIdx.x / lv, c = threadIdx.x - r * lv;
+  const unsigned char* sp = J.src + (s0 + r) * J.src_stride + off + c * static_cast<int64_t>(sizeof(V));
+  unsigned char* dp = J.dst + (s0 + r) * J.dst_stride + off + c * static_cast<int64_t>(sizeof(V));
+  const int64_t s_step = dr * J.src_stride + dc * static_cast<int64_t>(sizeof(V));
+  const int64_t d_step = dr * J.dst_stride + dc * static_cast<int64_t>(sizeof(V));
+  const int64_t s_wrap = J.src_stride - lv * static_cast<int64_t>(sizeof(V));
+  const int64_t d_wrap = J.dst_stride - lv * static_cast<int64_t>(sizeof(V));
+  const V* sv[U];
+  V* dv[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    sv[u] = reinterpret_cast<const V*>(sp);
+    dv[u] = reinterpret_cast<V*>(dp);
+    sp += s_step;
+    dp += d_step;
+    c += dc;
+    if (c >= lv) {
+      c -= lv;
+      sp += s_wrap;
+      dp += d_wrap;
+    }
+  }
   V v[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int i = threadIdx.x + u * 256;
-    if (i < total) {
-      const int r = i / lv, c = i - r * lv;
-      v[u] = *reinterpret_cast<const V*>(src + r * J.src_stride + c * static_cast<int64_t>(sizeof(V)));
-    }
-  }
+  for (int u = 0; u < U; ++u)
+    if (static_cast<int>(threadIdx.x) + u * 256 < total) v[u] = *sv[u];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int i = threadIdx.x + u * 256;
-    if (i < total) {
-      const int r = i / lv, c = i - r * lv;
-      *reinterpret_cast<V*>(dst + r * J.dst_stride + c * static_cast<int64_t>(sizeof(V))) = v[u];
-    }
-  }
+  for (int u = 0; u < U; ++u)
+    if (static_cast<int>(threadIdx.x) + u * 256 < total) *dv[u] = v[u];
 }
 
 static int widest(std::initializer_list<int64_t> vals) {
