@@ -254,6 +254,11 @@ def redistribute_many(xs: list[DTensor], dsts: list[ShardSpec],
 def _fused_gather(mesh, md, items, ledger, mover):
     """items: (x, [spec, local]) with a shard-like placement on md -> Replicate."""
     P = mesh.sizes[md]
+    if P == 1:  # a one-rank fiber: the shard is the whole tensor (one copy, no collective)
+        for _, slot in items:
+            slot[0] = slot[0].with_placement(md, Replicate())
+            slot[1] = slot[1].clone()
+        return
     group, fiber = comm.fiber_group(mesh, (md,))
     send_members, recv_members = [], []
     outs = []
@@ -295,6 +300,11 @@ def _fused_gather(mesh, md, items, ledger, mover):
 def _fused_reduce_scatter(mesh, md, items, ledger, mover):
     """items: (x, [spec, local], dst_placement) with Partial on md."""
     P = mesh.sizes[md]
+    if P == 1:  # a one-rank fiber: the sum over one rank is the tensor itself
+        for _, slot, dst_p in items:
+            slot[0] = slot[0].with_placement(md, dst_p)
+            slot[1] = slot[1].clone()
+        return
     group, fiber = comm.fiber_group(mesh, (md,))
     k = fiber.index(comm.my_rank())
     full_members, piece_members, outs = [], [], []
@@ -324,7 +334,8 @@ def _fused_reduce_scatter(mesh, md, items, ledger, mover):
     dt = items[0][1][1].dtype
     es = items[0][1][1].element_size()
     dev = items[0][1][1].device
-    packed = torch.zeros(seg * P // es, dtype=dt, device=dev)
+    # pad rows / alignment gaps are summed but never read back: no memset needed
+    packed = torch.empty(seg * P // es, dtype=dt, device=dev)
     mover.pack_scatter(full_members, packed.view(torch.uint8), seg, P)
     piece_buf = torch.empty(seg // es, dtype=dt, device=dev)
     comm.reduce_scatter_into(piece_buf, packed, group, ledger, mesh.name, mesh.dim_names[md], P)
@@ -351,12 +362,16 @@ def _fused_all_reduce(mesh, dims, items, ledger, mover):
     back to back.  Replaces each slot's local with a new reduced tensor (the
     inputs are never modified)."""
     P = math.prod(mesh.sizes[d] for d in dims)
+    if P == 1:
+        for _, slot in items:
+            slot[1] = slot[1].clone()
+        return
     group, _ = comm.fiber_group(mesh, tuple(dims))
     members = [Member(slot[1].contiguous(), 1, 1, slot[1].numel(), 1) for _, slot in items]
     seg = layout(members, align=16)
     dt = items[0][1][1].dtype
     es = items[0][1][1].element_size()
-    buf = torch.zeros(seg // es, dtype=dt, device=items[0][1][1].device)
+    buf = torch.empty(seg // es, dtype=dt, device=items[0][1][1].device)  # gaps never read
     mover.pack_local(members, buf.view(torch.uint8))
     comm.all_reduce_into(buf, group, ledger, mesh.name, "+".join(mesh.dim_names[d] for d in dims), P)
     outs = [Member(torch.empty_like(m.tensor), 1, 1, m.inner, 1, m.seg_off) for m in members]

@@ -112,8 +112,13 @@ def run(a):
         ms_ag = _time(lambda: redistribute_many(xs, dsts), a.steps, a.warmup, dev, ws)
         ms_rs = _time(lambda: redistribute_many(grads, gdst), a.steps, a.warmup, dev, ws)
         S = sum(math.prod(x.shape) // tp for x in xs) * 2  # gathered bytes per DP fiber
-        busbw = lambda ms: S / ms / 1e6 * (dp - 1) / dp if dp > 1 else 0.0
-        line.update(metric="fused redistribute busBW (cfg5)", value=round(busbw(ms_ag), 3), unit="GB/s",
+        if dp > 1:
+            busbw = lambda ms: S / ms / 1e6 * (dp - 1) / dp
+            metric = "fused redistribute busBW (cfg5)"
+        else:  # one-rank DP fiber: no exchange; report the local data movement (read + write)
+            busbw = lambda ms: 2 * S / ms / 1e6
+            metric = "fused redistribute local copy GB/s (cfg5 at dp=1: no exchange)"
+        line.update(metric=metric, value=round(busbw(ms_ag), 3), unit="GB/s",
                     ms_per_step=round(ms_ag, 4), scaling="weak", dtype="bf16",
                     config={"workload": "cfg5: one LLaMA-3-8B layer, fused AG (S->R over dp) + RS (P->S)",
                             "parallelism": f"dp{dp}xtp{tp}", "ms_allgather": round(ms_ag, 4),
