@@ -139,3 +139,52 @@ def test_materialize_torch_module_on_meta_device():
         assert p.is_cuda and torch.equal(bits(p.data), bits(want)), name
     assert st.offset == ref_st.offset
     assert model[0].weight.shape == (24, 64) and model[2].weight.shape == (32, 24)
+
+
+@pytest.mark.parametrize("kind", ["normal", "uniform"])
+def test_cfg4_llama3_8b_tp8_shards_equal_tp1(kind):
+    """BASELINE config 4 at full size: the whole LLaMA-3-8B init (291 params,
+    8.03 G bf16 elements, one launch) on 1 GPU, then every TP=8 rank's shards
+    (one launch per rank) equal the corresponding slices bit for bit, the
+    RngState offsets agree, and oracle spot checks pin absolute values."""
+    b = 3 ** 0.5 * 0.02
+    fac = (lambda n, s: R.Normal(0.0, 0.02)) if kind == "normal" else (lambda n, s: R.Uniform(-b, b))
+    full = I.llama3_8b_params(fac, "bfloat16")
+    st1 = R.RngState(1234)
+    out1 = I.materialize(full, st1)
+    mesh = S.create_mesh([("tp", 8)])
+    specs = I.llama3_tp_specs(full, mesh)
+    for rank in (0, 3, 7):
+        params = I.llama3_8b_params(fac, "bfloat16")
+        st8 = R.RngState(1234)
+        out8 = I.materialize(params, st8, specs, (rank,))
+        assert st8.offset == st1.offset
+        for name, p in params.items():
+            v = local_shape_and_offset(specs[name], p.shape, (rank,))
+            sl = tuple(slice(o, o + n) for o, n in zip(v.local_offset, v.local_shape))
+            assert torch.equal(bits(out8[name]), bits(out1[name][sl])), (name, rank)
+        del out8, params
+    # absolute values: oracle windows of three parameters (first, middle, last)
+    offs = np.cumsum([0] + [int(np.prod(p.shape)) // 65536 + (int(np.prod(p.shape)) % 65536 > 0)
+                            for p in full.values()])
+    names = list(full)
+    params = (("normal", (0.0, 0.02)) if kind == "normal" else ("uniform", (-b, b)))
+    for idx in (0, 150, 290):
+        name, shape = names[idx], full[names[idx]].shape
+        rows = np.array([0, 1, shape[0] - 1]) if len(shape) == 2 else None
+        win = [rows, np.arange(0, 64)] if rows is not None else [np.arange(shape[0] - 64, shape[0])]
+        ref = O.fill_window(shape, win, 1234, int(offs[idx]), 65536, params[0], params[1], _bf16())
+        t = out1[name]
+        if rows is not None:
+            got = t[torch.as_tensor(rows, device=t.device)][:, :64]
+        else:
+            got = t[shape[0] - 64:]
+        got = got.contiguous().cpu().view(torch.int16).numpy().view(np.uint16)
+        assert got.tobytes() == np.ascontiguousarray(ref).view(np.uint16).tobytes(), name
+    del out1
+    torch.cuda.empty_cache()
+
+
+def _bf16():
+    import ml_dtypes
+    return ml_dtypes.bfloat16
