@@ -661,6 +661,44 @@ __device__ __forceinline__ uint64_t outer_base(const ViewIndexer& ix, const Fast
   return j + row * static_cast<uint64_t>(cv.ostride[0]);
 }
 
+// Incremental chunk walk of a grid-stride loop over a view with at most one
+// outer dim (nd <= 1): after one division for the first chunk, each step of
+// S = gridDim*blockDim chunks adds dj to the global index and dcq to the
+// column, with one conditional wrap to the next row.  Set per launch
+// (set_walk) because S depends on the grid.
+struct ChunkWalk {
+  uint64_t dj, dcq, wrap;
+  uint32_t on;  // nd <= 1
+};
+
+inline void set_walk(ChunkWalk& w, const CanonView& cv, uint64_t cpr, uint64_t S, int ch) {
+  w.on = cv.nd <= 1 && cpr > 0;
+  if (!w.on) return;
+  const uint64_t os0 = cv.nd == 1 ? static_cast<uint64_t>(cv.ostride[0]) : cpr * ch;
+  w.dcq = S % cpr;
+  w.dj = (S / cpr) * os0 + w.dcq * ch;
+  w.wrap = os0 - cpr * ch;
+}
+
+// First chunk of this thread: global index and column (one division).
+__device__ __forceinline__ uint64_t walk_start(const ViewIndexer& ix, const FastDiv64& div_cpr,
+                                               uint64_t q, int ch, uint64_t& cq) {
+  uint64_t row;
+  div_cpr.divmod(q, row, cq);
+  uint64_t j = static_cast<uint64_t>(ix.cv.base) + cq * ch;
+  if (ix.cv.nd == 1) j += row * static_cast<uint64_t>(ix.cv.ostride[0]);
+  return j;
+}
+
+__device__ __forceinline__ void walk_next(const ChunkWalk& w, uint64_t cpr, uint64_t& j, uint64_t& cq) {
+  cq += w.dcq;
+  j += w.dj;
+  if (cq >= cpr) {
+    cq -= cpr;
+    j += w.wrap;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Fill kernels.
 // ---------------------------------------------------------------------------
@@ -674,6 +712,7 @@ struct __align__(16) FillArgs {
   uint64_t nchunks;
   uint64_t chunks_per_row;
   FastDiv64 div_cpr;
+  ChunkWalk walk;
 };
 
 // Global flat index of the first element of chunk q (fast path).
@@ -683,9 +722,19 @@ __device__ __forceinline__ uint64_t chunk_base(const FillArgs& A, uint64_t q) {
 }
 
 template <int DIST, int DT, bool ALIGNED>
+__device__ __forceinline__ void fill_chunk_at(const FillArgs& A, const NormalLut* L, uint64_t q,
+                                              uint64_t j0);
+
+template <int DIST, int DT, bool ALIGNED>
 __device__ __forceinline__ void fill_chunk(const FillArgs& A, const NormalLut* L, uint64_t q) {
+  fill_chunk_at<DIST, DT, ALIGNED>(A, L, q, chunk_base(A, q));
+}
+
+// Chunk q whose first element has global index j0.
+template <int DIST, int DT, bool ALIGNED>
+__device__ __forceinline__ void fill_chunk_at(const FillArgs& A, const NormalLut* L, uint64_t q,
+                                              uint64_t j0) {
   using T = typename St<DT>::T;
-  const uint64_t j0 = chunk_base(A, q);
   uint32_t w0[kV], w1[kV];
   if constexpr (ALIGNED) chunk_words_aligned<kV>(A.g, j0, w0, w1);
   else chunk_words<kV>(A.g, j0, w0, w1);
@@ -725,9 +774,17 @@ __global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_fast(const __grid_c
     L = &s_lut;
   }
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < A.nchunks;
-       q += stride)
-    fill_chunk<DIST, DT, ALIGNED>(A, L, q);
+  uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (A.walk.on) {
+    uint64_t cq;
+    uint64_t j = walk_start(A.ix, A.div_cpr, q, kV, cq);
+    for (; q < A.nchunks; q += stride) {
+      fill_chunk_at<DIST, DT, ALIGNED>(A, L, q, j);
+      walk_next(A.walk, A.chunks_per_row, j, cq);
+    }
+  } else {
+    for (; q < A.nchunks; q += stride) fill_chunk<DIST, DT, ALIGNED>(A, L, q);
+  }
 }
 
 template <int DIST, int DT>
@@ -953,7 +1010,7 @@ __global__ void __launch_bounds__(256, SDR_DROP_MINB) k_dropout_fast(const __gri
        q += stride) {
     XTy xv[CH];
     load_chunk(x + q * CH, xv);
-    const uint64_t j0 = drop_chunk_base(A, q);
+    const uint64_t j0 = drop_chunk_base(A, q);  // (an incremental walk measured slower here)
     YTy yv[CH];
     bool keep[CH], anynan = false, nan[CH];
 #pragma unroll
@@ -1384,11 +1441,16 @@ static void setup_chunks(const CanonView& cv, bool fast, uint64_t& nchunks, uint
 }
 
 template <int DIST, int DT>
-static void launch_fill(const FillArgs& A, bool fast, cudaStream_t s) {
+static void launch_fill(const FillArgs& A0, bool fast, cudaStream_t s) {
+  FillArgs A = A0;
   if (fast && A.aligned) {
-    k_fill_fast<DIST, DT, true><<<grid_for(k_fill_fast<DIST, DT, true>, A.nchunks, 256), 256, 0, s>>>(A);
+    const int grid = grid_for(k_fill_fast<DIST, DT, true>, A.nchunks, 256);
+    set_walk(A.walk, A.ix.cv, A.chunks_per_row, static_cast<uint64_t>(grid) * 256, kV);
+    k_fill_fast<DIST, DT, true><<<grid, 256, 0, s>>>(A);
   } else if (fast) {
-    k_fill_fast<DIST, DT, false><<<grid_for(k_fill_fast<DIST, DT, false>, A.nchunks, 256), 256, 0, s>>>(A);
+    const int grid = grid_for(k_fill_fast<DIST, DT, false>, A.nchunks, 256);
+    set_walk(A.walk, A.ix.cv, A.chunks_per_row, static_cast<uint64_t>(grid) * 256, kV);
+    k_fill_fast<DIST, DT, false><<<grid, 256, 0, s>>>(A);
   } else {
     k_fill_generic<DIST, DT><<<grid_for(k_fill_generic<DIST, DT>, A.ix.cv.numel, 256), 256, 0, s>>>(A);
   }
