@@ -269,10 +269,13 @@ struct NormalLut {
   double2 trig[2048];
 };
 
-// float32 copies for the bfloat16 fast path (20 KiB, staged in shared memory).
+// float32 tables of the bfloat16 fast path, staged in (dynamic) shared memory:
+// the log table plus a two-level cosine table, cos(2 pi k / 2^24) =
+// C_hi C_lo - S_hi S_lo with k = 4096 hi + lo (68 KiB).
 struct NormalLut32 {
   float2 logt[512];
-  float2 trig[2048];
+  float2 trig_hi[4096];  // (cos, sin)(2 pi hi / 4096)
+  float2 trig_lo[4096];  // (cos, sin)(2 pi lo / 2^24)
 };
 
 struct NormalMirror {
@@ -427,13 +430,9 @@ __device__ __forceinline__ float r32_fast(uint32_t w0, const NormalLut32* L) {
 }
 
 __device__ __forceinline__ float c32_fast(uint32_t w1, const NormalLut32* L) {
-  const uint32_t u = w1 + 0x100000u;
-  const float2 cs = lut_at(L->trig, (u >> 18) & 0x3FF8u);
-  const float d = __uint_as_float(((u >> 8) & 0x1FFFu) | 0x4B000000u) - 8392704.0f;  // exact
-  const float d2 = d * d;                                                         // exact
-  const float cm = d2 * static_cast<float>(-0.5 * kK1 * kK1);
-  const float sd = d * fmaf(d2, static_cast<float>(-kK1 * kK1 * kK1 / 6.0), static_cast<float>(kK1));
-  return fmaf(-cs.y, sd, fmaf(cs.x, cm, cs.x));
+  const float2 a = lut_at(L->trig_hi, (w1 >> 17) & 0x7FF8u);  // hi = k >> 12
+  const float2 b = lut_at(L->trig_lo, (w1 >> 5) & 0x7FF8u);   // lo = k & 4095
+  return fmaf(a.x, b.x, -a.y * b.y);
 }
 
 template <int DT>
@@ -765,9 +764,10 @@ template <int DIST, int DT, bool ALIGNED>
 __global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_fast(const __grid_constant__ FillArgs A) {
   const NormalLut* L = nullptr;
   if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
-    __shared__ __align__(16) NormalLut32 s_lut32;
-    stage_lut(&s_lut32, A.d.nm.lut32);
-    L = reinterpret_cast<const NormalLut*>(&s_lut32);
+    extern __shared__ __align__(16) unsigned char s_dyn[];  // sizeof(NormalLut32), set at launch
+    NormalLut32* s_lut32 = reinterpret_cast<NormalLut32*>(s_dyn);
+    stage_lut(s_lut32, A.d.nm.lut32);
+    L = reinterpret_cast<const NormalLut*>(s_lut32);
   } else if constexpr (DIST == SDR_NORMAL) {
     __shared__ __align__(16) NormalLut s_lut;
     stage_lut(&s_lut, A.d.nm.lut);
@@ -816,9 +816,10 @@ __global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_batch(const FillArg
   FillArgs& A = *reinterpret_cast<FillArgs*>(smem);
   const NormalLut* L = nullptr;
   if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
-    __shared__ __align__(16) NormalLut32 s_lut32;
-    stage_lut(&s_lut32, descs[0].d.nm.lut32);
-    L = reinterpret_cast<const NormalLut*>(&s_lut32);
+    extern __shared__ __align__(16) unsigned char s_dyn[];  // sizeof(NormalLut32), set at launch
+    NormalLut32* s_lut32 = reinterpret_cast<NormalLut32*>(s_dyn);
+    stage_lut(s_lut32, descs[0].d.nm.lut32);
+    L = reinterpret_cast<const NormalLut*>(s_lut32);
   } else if constexpr (DIST == SDR_NORMAL) {
     __shared__ __align__(16) NormalLut s_lut;
     stage_lut(&s_lut, descs[0].d.nm.lut);
@@ -1252,9 +1253,9 @@ static int device_sms() {
 // Persistent grid: one wave of resident CTAs (SMs x occupancy), or fewer
 // blocks when the work is small.  Grid-stride loops cover the rest.
 template <typename K>
-static int grid_for(K kernel, uint64_t work, int threads) {
+static int grid_for(K kernel, uint64_t work, int threads, size_t dyn_smem = 0) {
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, dyn_smem) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
   const uint64_t cap = static_cast<uint64_t>(device_sms()) * per_sm;
@@ -1319,14 +1320,22 @@ static void build_normal_lut(NormalLut& L) {
   L.trig[1536] = make_double2(0.0, -1.0);
 }
 
-// float32 tables of the bfloat16 path: the float64 layout rounded (the logt.x
-// entries are exact: 20-bit mult).
+// float32 tables of the bfloat16 path: the float64 log table rounded (the
+// logt.x entries are exact: 20-bit mult) and the two-level cosine table.
 static void build_normal_lut32(const NormalLut& h, NormalLut32& L) {
   for (int j = 0; j < 512; ++j)
     L.logt[j] = make_float2(static_cast<float>(h.logt[j].x), static_cast<float>(h.logt[j].y));
   L.logt[0].y = 0x1p-100f;
-  for (int i = 0; i < 2048; ++i)
-    L.trig[i] = make_float2(static_cast<float>(h.trig[i].x), static_cast<float>(h.trig[i].y));
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int i = 0; i < 4096; ++i) {
+    const long double a = 2.0L * pi * i / 4096.0L, b = 2.0L * pi * i / 16777216.0L;
+    L.trig_hi[i] = make_float2(static_cast<float>(cosl(a)), static_cast<float>(sinl(a)));
+    L.trig_lo[i] = make_float2(static_cast<float>(cosl(b)), static_cast<float>(sinl(b)));
+  }
+  L.trig_hi[0] = make_float2(1.0f, 0.0f);
+  L.trig_hi[1024] = make_float2(0.0f, 1.0f);
+  L.trig_hi[2048] = make_float2(-1.0f, 0.0f);
+  L.trig_hi[3072] = make_float2(0.0f, -1.0f);
 }
 static NormalState g_nm[64];
 
@@ -1440,17 +1449,31 @@ static void setup_chunks(const CanonView& cv, bool fast, uint64_t& nchunks, uint
   div_cpr = FastDiv64(cpr > 0 ? cpr : 1);
 }
 
+// Dynamic shared memory of the fill kernels (the float32 Normal tables exceed
+// the 48 KiB static limit), with the opt-in attribute set before each launch.
+template <int DIST, int DT>
+static constexpr size_t fill_dyn_smem() {
+  return (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) ? sizeof(NormalLut32) : 0;
+}
+template <typename K>
+static void allow_dyn_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+}
+
 template <int DIST, int DT>
 static void launch_fill(const FillArgs& A0, bool fast, cudaStream_t s) {
   FillArgs A = A0;
+  constexpr size_t dsm = fill_dyn_smem<DIST, DT>();
   if (fast && A.aligned) {
-    const int grid = grid_for(k_fill_fast<DIST, DT, true>, A.nchunks, 256);
+    allow_dyn_smem(k_fill_fast<DIST, DT, true>, dsm);
+    const int grid = grid_for(k_fill_fast<DIST, DT, true>, A.nchunks, 256, dsm);
     set_walk(A.walk, A.ix.cv, A.chunks_per_row, static_cast<uint64_t>(grid) * 256, kV);
-    k_fill_fast<DIST, DT, true><<<grid, 256, 0, s>>>(A);
+    k_fill_fast<DIST, DT, true><<<grid, 256, dsm, s>>>(A);
   } else if (fast) {
-    const int grid = grid_for(k_fill_fast<DIST, DT, false>, A.nchunks, 256);
+    allow_dyn_smem(k_fill_fast<DIST, DT, false>, dsm);
+    const int grid = grid_for(k_fill_fast<DIST, DT, false>, A.nchunks, 256, dsm);
     set_walk(A.walk, A.ix.cv, A.chunks_per_row, static_cast<uint64_t>(grid) * 256, kV);
-    k_fill_fast<DIST, DT, false><<<grid, 256, 0, s>>>(A);
+    k_fill_fast<DIST, DT, false><<<grid, 256, dsm, s>>>(A);
   } else {
     k_fill_generic<DIST, DT><<<grid_for(k_fill_generic<DIST, DT>, A.ix.cv.numel, 256), 256, 0, s>>>(A);
   }
@@ -1660,7 +1683,9 @@ int normal_fallback_count(int device, uint64_t* count) {
 template <int DIST, int DT>
 static void launch_batch(const FillArgs* d_descs, const uint64_t* d_prefix, int n, uint64_t ntiles,
                          cudaStream_t s) {
-  k_fill_batch<DIST, DT><<<launch_grid(ntiles * 256, 256), 256, 0, s>>>(d_descs, d_prefix, n, ntiles);
+  constexpr size_t dsm = fill_dyn_smem<DIST, DT>();
+  allow_dyn_smem(k_fill_batch<DIST, DT>, dsm);
+  k_fill_batch<DIST, DT><<<launch_grid(ntiles * 256, 256), 256, dsm, s>>>(d_descs, d_prefix, n, ntiles);
 }
 
 template <int DIST>
