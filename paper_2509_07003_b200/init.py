@@ -16,6 +16,7 @@ The result is bit-identical to calling `generate_distributed` /
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import math
 from dataclasses import dataclass, field
 
@@ -43,6 +44,13 @@ class Parameter:
     @property
     def materialized(self) -> bool:
         return self.value is not None
+
+
+@functools.lru_cache(maxsize=4096)
+def _window(spec: ShardSpec, shape: tuple, coord: tuple):
+    """local_shape_and_offset, memoised: a model re-initialised (or many models
+    with the same layout) recomputes no windows (ShardSpec is frozen/hashable)."""
+    return local_shape_and_offset(spec, shape, coord)
 
 
 def materialize(params, state: RngState, init_specs: dict | None = None, coord=None, *,
@@ -78,7 +86,7 @@ def materialize(params, state: RngState, init_specs: dict | None = None, coord=N
                 import torch.distributed as dist_mod
                 rank = dist_mod.get_rank() if dist_mod.is_initialized() else 0
                 c = spec.mesh.coords_of_rank(rank)
-            view = local_shape_and_offset(spec, p.shape, tuple(c))
+            view = _window(spec, tuple(p.shape), tuple(c))
         code = p.dist.out_code(dtype_code(p.dtype))
         t = torch.empty(view.local_shape, dtype=_TORCH_OF_CODE[code], device=dev)
         result[name] = t
