@@ -284,10 +284,10 @@ struct NormalMirror {
   const NormalLut* lut; // device copy of the fast-path tables
   const NormalLut32* lut32;
   double nh, th;        // -0.5*std, 1.5*std: the Newton step of r_fast returns std*r
-  double kr, k0;        // certification bound B = (std r) kr + |v| 2^-51 + k0
+  double kr, k0;        // certification bound B = (std r) kr + k0
   // float32 fast path (bfloat16 outputs): calibrated errors and bound terms
   double err_r32, err_c32;
-  float mean32, std32, b32_r, b32_c;  // B32 = r*b32_r + |v|*2^-22 + b32_c
+  float mean32, std32, b32_r, b32_c;  // B32 = r*b32_r + b32_c
   unsigned long long* fallbacks;
 };
 
@@ -447,8 +447,8 @@ __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLu
   for (int e = 0; e < NE; ++e) {
     const float r = r32_fast(w0[e], L32), c = c32_fast(w1[e], L32);
     const float v = fmaf(P.nm.std32, r * c, P.nm.mean32);
-    // |v - v_numpy| <= r*b32_r + |v|*2^-22 + b32_c   (host: bound terms)
-    const float B = fmaf(r, P.nm.b32_r, fmaf(fabsf(v), 0x1p-22f, P.nm.b32_c));
+    // |v - v_numpy| <= r*b32_r + b32_c   (host: bound terms)
+    const float B = fmaf(r, P.nm.b32_r, P.nm.b32_c);  // |v| term folded (host)
     // bf16(RN32(.)) is monotone: [v-B, v+B] rounds to one bfloat16 iff both ends do
     const __nv_bfloat162 pk = __floats2bfloat162_rn(__fsub_rd(v, B), __fadd_ru(v, B));
     uint32_t lh;
@@ -482,7 +482,7 @@ template <int DT>
 __device__ __forceinline__ typename St<DT>::T normal_certified(const DistP& P, double rs, double c,
                                                                bool& ok) {
   const double v = fma(rs, c, P.mean);
-  const double B = fma(rs, P.nm.kr, fma(fabs(v), 0x1p-51, P.nm.k0));
+  const double B = fma(rs, P.nm.kr, P.nm.k0);  // |v| 2^-51 folded: |v| <= |mean| + rs (host)
   const auto lo = from_f64<DT>(v - B), hi = from_f64<DT>(v + B);
   if constexpr (DT == SDR_F32) ok = __float_as_uint(lo) == __float_as_uint(hi);
   else ok = lo == hi;
@@ -1381,6 +1381,9 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
         P.nm.th = 1.5 * P.stdv;
         P.nm.kr = 2.0 * (Erp + Ec * (1.0 + Erp) + 2.01 * u) / (1.0 - Erp) * (1.0 + 0x1p-30);
         P.nm.k0 = 2.0 * fabs(P.stdv) * 0x1p-489 + 0x1p-1060;
+        // the kernel's B = rs kr + k0 also covers |v| 2^-51 <= (|mean| + rs (1 + 2^-48)) 2^-51
+        P.nm.kr += 0x1p-51 * (1.0 + 0x1p-40);
+        P.nm.k0 += fabs(P.mean) * 0x1p-51 * (1.0 + 0x1p-40);
         if (!(Er < 0x1p-20) || !(Ec < 0x1p-20)) P.nm.kr = INFINITY;  // calibration failed: exact path
         // float32 path (bfloat16 outputs): Er32, Ec32 the calibrated errors of
         // r32_fast / c32_fast;  |v32 - v_np| <= |std| r (Er32 + Ec32(1+Er32) + 2^-23)
@@ -1392,6 +1395,9 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
         P.nm.std32 = static_cast<float>(P.stdv);
         P.nm.b32_r = static_cast<float>(2.04 * fabs(P.stdv) * (Er32 + Ac32 * (1.0 + Er32) + 0x1p-23) + 0x1p-60);
         P.nm.b32_c = static_cast<float>(2.04 * 0x1p-24 * fabs(P.mean) + 2.0 * fabs(P.stdv) * 0x1p-48 + 0x1p-140);
+        // B32 = r b32_r + b32_c also covers |v| 2^-22 <= (|mean32| + std32 r (1 + 2^-21)) 2^-22
+        P.nm.b32_r = static_cast<float>(P.nm.b32_r + fabs(static_cast<double>(P.nm.std32)) * 0x1p-22 * (1.0 + 0x1p-20));
+        P.nm.b32_c = static_cast<float>(P.nm.b32_c + fabs(static_cast<double>(P.nm.mean32)) * 0x1p-22 * (1.0 + 0x1p-20));
         if (!(Er32 < 0x1p-12) || !(Ac32 < 0x1p-12)) P.nm.b32_r = INFINITY;  // calibration failed
         // Test hook: SDR_NORMAL_PATH=exact sends every element through the NumPy
         // tables, =f64 skips the float32 path (results must be identical).
