@@ -671,7 +671,7 @@ struct ChunkWalk {
 };
 
 inline void set_walk(ChunkWalk& w, const CanonView& cv, uint64_t cpr, uint64_t S, int ch) {
-  w.on = cv.nd <= 1 && cpr > 0;
+  w.on = cv.nd <= 1 && cpr > 0 && cv.inner % ch == 0;  // (ragged rows take fill_chunk_ragged)
   if (!w.on) return;
   const uint64_t os0 = cv.nd == 1 ? static_cast<uint64_t>(cv.ostride[0]) : cpr * ch;
   w.dcq = S % cpr;
@@ -708,6 +708,7 @@ struct __align__(16) FillArgs {
   void* out;
   // Fast-path chunk walk: chunk q covers local [8q, 8q+8) inside one row.
   uint32_t aligned;  // THETA pow2 >= 8 and chunk starts 8-aligned (no straddle)
+  uint32_t ragged;   // inner extent not a multiple of kV: per-element stores (fill_chunk_ragged)
   uint64_t nchunks;
   uint64_t chunks_per_row;
   FastDiv64 div_cpr;
@@ -729,15 +730,13 @@ __device__ __forceinline__ void fill_chunk(const FillArgs& A, const NormalLut* L
   fill_chunk_at<DIST, DT, ALIGNED>(A, L, q, chunk_base(A, q));
 }
 
-// Chunk q whose first element has global index j0.
+// Values of the kV elements with global indices j0 .. j0+kV-1.
 template <int DIST, int DT, bool ALIGNED>
-__device__ __forceinline__ void fill_chunk_at(const FillArgs& A, const NormalLut* L, uint64_t q,
-                                              uint64_t j0) {
-  using T = typename St<DT>::T;
+__device__ __forceinline__ void chunk_values(const FillArgs& A, const NormalLut* L, uint64_t j0,
+                                             typename St<DT>::T (&v)[kV]) {
   uint32_t w0[kV], w1[kV];
   if constexpr (ALIGNED) chunk_words_aligned<kV>(A.g, j0, w0, w1);
   else chunk_words<kV>(A.g, j0, w0, w1);
-  T v[kV];
   if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
     normal_chunk_bf16<kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v);
   } else if constexpr (DIST == SDR_NORMAL && DT != SDR_F64) {
@@ -749,7 +748,45 @@ __device__ __forceinline__ void fill_chunk_at(const FillArgs& A, const NormalLut
 #pragma unroll
     for (int e = 0; e < kV; ++e) v[e] = dist_value<DIST, DT>(A.d, L, w0[e], w1[e]);
   }
+}
+
+// Chunk q whose first element has global index j0.
+template <int DIST, int DT, bool ALIGNED>
+__device__ __forceinline__ void fill_chunk_at(const FillArgs& A, const NormalLut* L, uint64_t q,
+                                              uint64_t j0) {
+  using T = typename St<DT>::T;
+  T v[kV];
+  chunk_values<DIST, DT, ALIGNED>(A, L, j0, v);
   store_chunk(static_cast<T*>(A.out) + q * kV, v);
+}
+
+// Ragged rows (inner extent not a multiple of kV): chunk q = (row, cq) covers
+// columns [kV cq, min(kV cq + kV, inner)) of its row; the Philox words are
+// still computed kV at a time on consecutive global indices, the stores are
+// per element (row starts are not 16 B aligned).
+template <int DIST, int DT, bool ALIGNED>
+__device__ __forceinline__ void fill_chunk_ragged(const FillArgs& A, const NormalLut* L, uint64_t q) {
+  using T = typename St<DT>::T;
+  const CanonView& cv = A.ix.cv;
+  uint64_t row, cq;
+  A.div_cpr.divmod(q, row, cq);
+  uint64_t j0 = static_cast<uint64_t>(cv.base) + cq * kV, r = row;
+  for (int k = cv.nd - 1; k >= 1; --k) {
+    uint64_t qq, rem;
+    A.ix.div_o[k].divmod(r, qq, rem);
+    j0 += rem * static_cast<uint64_t>(cv.ostride[k]);
+    r = qq;
+  }
+  if (cv.nd >= 1) j0 += r * static_cast<uint64_t>(cv.ostride[0]);
+  const uint64_t inner = static_cast<uint64_t>(cv.inner);
+  const uint64_t lq = row * inner + cq * kV;
+  const int nvalid = static_cast<int>(min(static_cast<uint64_t>(kV), inner - cq * kV));
+  T v[kV];
+  chunk_values<DIST, DT, ALIGNED>(A, L, j0, v);
+  T* out = static_cast<T*>(A.out) + lq;
+#pragma unroll
+  for (int e = 0; e < kV; ++e)
+    if (e < nvalid) out[e] = v[e];
 }
 
 template <int DIST, int DT>
@@ -782,6 +819,8 @@ __global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_fast(const __grid_c
       fill_chunk_at<DIST, DT, ALIGNED>(A, L, q, j);
       walk_next(A.walk, A.chunks_per_row, j, cq);
     }
+  } else if (A.ragged) {
+    for (; q < A.nchunks; q += stride) fill_chunk_ragged<DIST, DT, ALIGNED>(A, L, q);
   } else {
     for (; q < A.nchunks; q += stride) fill_chunk<DIST, DT, ALIGNED>(A, L, q);
   }
@@ -1540,9 +1579,17 @@ int fill(void* out, int dt, const sdr_dist& dist, const sdr_rng& rng, const sdr_
   A.g = make_gen(rng);
   A.ix = make_indexer(cv);
   A.out = out;
-  const bool fast = cv.istride == 1 && cv.inner % kV == 0 && aligned16(out);
+  bool fast = cv.istride == 1 && cv.inner % kV == 0 && aligned16(out);
   setup_chunks(cv, fast, A.nchunks, A.chunks_per_row, A.div_cpr);
   A.aligned = fast && chunks_aligned(cv, rng.theta, kV);
+  if (!fast && cv.istride == 1 && cv.inner >= kV) {  // ragged rows: chunked, per-element stores
+    fast = true;
+    A.ragged = 1;
+    A.chunks_per_row = (static_cast<uint64_t>(cv.inner) + kV - 1) / kV;
+    A.nchunks = static_cast<uint64_t>(cv.numel / cv.inner) * A.chunks_per_row;
+    A.div_cpr = FastDiv64(A.chunks_per_row);
+    A.aligned = chunks_aligned(cv, rng.theta, kV);
+  }
   switch (dist.kind) {
     case SDR_UNIFORM01: return dispatch_fill_dt<SDR_UNIFORM01>(dt, A, fast, s);
     case SDR_UNIFORM: return dispatch_fill_dt<SDR_UNIFORM>(dt, A, fast, s);
