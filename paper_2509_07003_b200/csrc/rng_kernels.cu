@@ -914,6 +914,7 @@ struct DropArgs {
   float scale32;
   double scale64;
   uint16_t scale16;  // f16 bits of the scale
+  uint32_t ragged;   // inner extent not a multiple of the chunk: k_dropout_ragged
   uint64_t nchunks;
   uint64_t chunks_per_row;
   FastDiv64 div_cpr;
@@ -1108,6 +1109,54 @@ __global__ void __launch_bounds__(256, SDR_DROP_MINB) k_dropout_fast(const __gri
 #pragma unroll
         for (int e = 0; e < CH; ++e) mv[e] = one_or_zero<MT>(keep[e]);
         store_chunk(static_cast<MTy*>(A.mask) + q * CH, mv);
+      }
+    }
+  }
+}
+
+// Ragged rows (inner extent not a multiple of the chunk): chunk q = (row, cq)
+// covers columns [CH cq, min(CH cq + CH, inner)) of its row.  Philox is
+// computed CH-wide on consecutive global indices (hoisted rounds 1-2), x / y /
+// mask move per element (row starts are not 16 B aligned).
+template <int XT, int YT, int MT>
+__global__ void __launch_bounds__(256) k_dropout_ragged(const __grid_constant__ DropArgs A) {
+  using XTy = typename St<XT>::T;
+  using YTy = typename St<YT>::T;
+  constexpr int CH = kDropCh;
+  const XTy* x = static_cast<const XTy*>(A.x);
+  YTy* y = static_cast<YTy*>(A.y);
+  const CanonView& cv = A.ix.cv;
+  const uint64_t inner = static_cast<uint64_t>(cv.inner);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < A.nchunks;
+       q += stride) {
+    uint64_t row, cq;
+    A.div_cpr.divmod(q, row, cq);
+    uint64_t j0 = static_cast<uint64_t>(cv.base) + cq * CH, r = row;
+    for (int k = cv.nd - 1; k >= 1; --k) {
+      uint64_t qq, rem;
+      A.ix.div_o[k].divmod(r, qq, rem);
+      j0 += rem * static_cast<uint64_t>(cv.ostride[k]);
+      r = qq;
+    }
+    if (cv.nd >= 1) j0 += r * static_cast<uint64_t>(cv.ostride[0]);
+    const uint64_t lq = row * inner + cq * CH;
+    const int nvalid = static_cast<int>(min(static_cast<uint64_t>(CH), inner - cq * CH));
+    uint32_t w0[CH], w1[CH];
+    chunk_words<CH>(A.g, j0, w0, w1);
+#pragma unroll
+    for (int e = 0; e < CH; ++e) {
+      if (e < nvalid) {
+        const uint64_t i = lq + e;
+        const bool keep = ((static_cast<uint64_t>(w1[e]) << 32) | w0[e]) <= A.keep_le;
+        bool nan;
+        const XTy xe = x[i];
+        const YTy v = drop_apply<XT, YT>(A, xe, keep, nan);
+        y[i] = nan ? drop_nan_fix<XT, YT>(xe) : v;
+        if constexpr (MT >= 0) {
+          using MTy = typename St<MT>::T;
+          if (A.mask != nullptr) static_cast<MTy*>(A.mask)[i] = one_or_zero<MT>(keep);
+        }
       }
     }
   }
@@ -1602,7 +1651,9 @@ int fill(void* out, int dt, const sdr_dist& dist, const sdr_rng& rng, const sdr_
 
 template <int XT, int YT, int MT>
 static int launch_drop(const DropArgs& A, bool fast, cudaStream_t s) {
-  if (fast && A.aligned)
+  if (A.ragged)
+    k_dropout_ragged<XT, YT, MT><<<grid_for(k_dropout_ragged<XT, YT, MT>, A.nchunks, 256), 256, 0, s>>>(A);
+  else if (fast && A.aligned)
     k_dropout_fast<XT, YT, MT, true><<<grid_for(k_dropout_fast<XT, YT, MT, true>, A.nchunks, 256), 256, 0, s>>>(A);
   else if (fast)
     k_dropout_fast<XT, YT, MT, false><<<grid_for(k_dropout_fast<XT, YT, MT, false>, A.nchunks, 256), 256, 0, s>>>(A);
@@ -1647,6 +1698,12 @@ int dropout(const void* x, int xt, void* y, int yt, void* mask, int mt, double p
               (mask == nullptr || (reinterpret_cast<uintptr_t>(mask) & 7u) == 0);
   setup_chunks(cv, fast, A.nchunks, A.chunks_per_row, A.div_cpr, kDropCh);
   A.aligned = fast && chunks_aligned(cv, rng.theta, kDropCh);
+  if (!fast && cv.istride == 1 && cv.inner >= kDropCh) {  // ragged rows: chunked Philox, per-element I/O
+    A.ragged = 1;
+    A.chunks_per_row = (static_cast<uint64_t>(cv.inner) + kDropCh - 1) / kDropCh;
+    A.nchunks = static_cast<uint64_t>(cv.numel / cv.inner) * A.chunks_per_row;
+    A.div_cpr = FastDiv64(A.chunks_per_row);
+  }
   if (xt == SDR_F32 && yt == SDR_F32) return dispatch_drop_mask<SDR_F32, SDR_F32>(mt, A, fast, s);
   if (xt == SDR_F64 && yt == SDR_F64) return dispatch_drop_mask<SDR_F64, SDR_F64>(mt, A, fast, s);
   if (xt == SDR_BF16 && yt == SDR_BF16) return dispatch_drop_mask<SDR_BF16, SDR_BF16>(mt, A, fast, s);

@@ -161,3 +161,26 @@ def test_dropout_host_pipeline_matches_device(dt, out_dtype):
         yh = ops.dropout_host(x, 0.3, st, v1, out_dtype=out_dtype, chunks=chunks)
         yd = ops.dropout_apply(x.cuda(), 0.3, st, v1, out_dtype=out_dtype)
         assert torch.equal(bits(yh), bits(yd.cpu())), chunks
+
+
+@pytest.mark.parametrize("mask_dt", [torch.uint8, torch.bfloat16])
+def test_ragged_rows_with_mask(mask_dt):
+    """Windows whose rows are not a multiple of the 8-element chunk (chunked
+    Philox, per-element I/O), with the mask output, vs the oracle."""
+    import ml_dtypes
+    shape, p, seed, off = (7, 101), 0.3, 123, 5
+    x = torch.randn(shape, generator=torch.Generator().manual_seed(1)).to(torch.bfloat16).cuda()
+    xn = x.cpu().view(torch.int16).numpy().view(np.uint16).view(ml_dtypes.bfloat16)
+    m = O.keep_mask(shape, [np.arange(n) for n in shape], seed, off, 65536, p, ml_dtypes.bfloat16)
+    yref = O.dropout_apply(xn, m, p)
+    mesh = S.create_mesh([("tp", 3)])
+    spec = ShardSpec(mesh, parse_placements("S(1)"))
+    for coord in mesh.iter_coords():
+        v = local_shape_and_offset(spec, shape, coord)  # 34 / 34 / 33 columns
+        sl = tuple(slice(o, o + n) for o, n in zip(v.local_offset, v.local_shape))
+        mask = torch.empty(v.local_shape, dtype=mask_dt, device="cuda")
+        y = ops.dropout_apply(x[sl].contiguous(), p, R.RngState(seed, off), v, out_dtype=torch.float32,
+                              mask=mask)
+        assert torch.equal(bits(y.cpu()), bits(torch.from_numpy(np.ascontiguousarray(yref[sl])))), coord
+        want = torch.from_numpy(np.ascontiguousarray(m[sl]).astype(np.float32))
+        assert torch.equal(mask.float().cpu(), want), coord
