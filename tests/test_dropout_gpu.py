@@ -184,3 +184,38 @@ def test_ragged_rows_with_mask(mask_dt):
         assert torch.equal(bits(y.cpu()), bits(torch.from_numpy(np.ascontiguousarray(yref[sl])))), coord
         want = torch.from_numpy(np.ascontiguousarray(m[sl]).astype(np.float32))
         assert torch.equal(mask.float().cpu(), want), coord
+
+
+def test_cuda_graph_capture_and_replay():
+    """The fused kernels are stream-capturable: K dropout steps (each with its
+    own RngState offset baked into its launch) and a Normal fill captured in
+    one CUDA graph replay to exactly the eager results."""
+    shape, p = (4, 256, 512), 0.1
+    x = torch.randn(shape, device="cuda", dtype=torch.bfloat16)
+    st = R.RngState(77)
+    R.ensure_normal_tables()
+    view = S.placement.full_view(shape)
+    ys = [torch.empty_like(x) for _ in range(3)]
+    w = torch.empty((300, 64), device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        ops.dropout_apply(x, p, st, view, out=ys[0])  # warm-up outside capture
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            cap = R.RngState(77)
+            for y in ys:
+                ops.dropout_apply(x, p, cap, view, out=y)
+                cap.advance(x.numel())
+            R.fill_random(S.placement.full_view((300, 64)), cap, R.Normal(0.0, 0.02), np.float32, out=w)
+    for y in ys:
+        y.zero_()
+    w.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    ref = R.RngState(77)
+    for y in ys:
+        assert torch.equal(bits(y), bits(ops.dropout_apply(x, p, ref, view)))
+        ref.advance(x.numel())
+    assert torch.equal(w, R.fill_random(S.placement.full_view((300, 64)), ref, R.Normal(0.0, 0.02), np.float32))
