@@ -8,12 +8,19 @@
 //
 // Layout of the work: a thread owns chunks of kV = 8 consecutive local elements
 // (one 16 B bf16 vector / two 16 B f32 vectors), grid-stride over the window.
-// Fast path (inner run % 8 == 0, unit inner stride, 16 B aligned buffers): the
-// chunk's 8 global indices are consecutive, so when they share beta the round-1
-// product M0*beta_lo and the round-2 product M1*y2 are computed once per chunk
-// and the round-1 products M1*(tau+e) are formed by 64-bit adds -- 16 IMAD.WIDE
-// per element instead of 20 (the last round's M0 product is dead for every
-// distribution, which uses words 0-1 only).
+// Fast path (unit inner stride; inner run % 8 == 0 with 16 B aligned buffers,
+// or ragged rows with per-element I/O): the chunk's 8 global indices are
+// consecutive, so when they share beta the round-1 product M0*beta_lo and the
+// round-2 product M1*y2 are computed once per chunk and the round-1 products
+// M1*(tau+e) are formed by 64-bit adds; the last round's M0 product is dead
+// (every distribution uses words 0-1 only) -- about 14 IMAD.WIDE per element
+// instead of 20.  Dropout needs only w1 (rounds 9-10 trimmed further).
+//
+// Normal (rng.py:141-156) is a certified fast path over NumPy's own float64
+// transcendentals: a ~2^-40 table + polynomial evaluation of r and c whose
+// error is measured exhaustively at load, a rigorous bound, and the exact
+// NumPy tables for the few elements the bound cannot certify.
+// The SDR_* macros below are A/B knobs; their defaults are the measured best.
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
