@@ -10,6 +10,8 @@ bus-bandwidth convention used by bench.py.
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass, field
 from fractions import Fraction
 
@@ -57,11 +59,22 @@ def fiber_group(mesh, dims: tuple):
     return _GROUPS[key]
 
 
+def _host_staged(t) -> bool:
+    """Test hook (SDR_COMM_CPU_STAGING=1): CUDA buffers cross a gloo group via
+    host copies, so several processes sharing one GPU can run the CUDA movers
+    end to end.  Never set in production (NCCL moves device buffers)."""
+    return t.is_cuda and os.environ.get("SDR_COMM_CPU_STAGING") == "1"
+
+
 def all_gather_into(recv, send, group, ledger=None, mesh="", dims="", P=1):
     """recv[P*len(send)] <- every fiber member's `send`, in fiber order."""
     import torch.distributed as dist
     if P == 1 or group is None:
         recv.copy_(send)
+    elif _host_staged(recv):
+        r = recv.cpu()
+        dist.all_gather_into_tensor(r, send.cpu(), group=group)
+        recv.copy_(r)
     else:
         dist.all_gather_into_tensor(recv, send, group=group)
     if ledger is not None:
@@ -73,6 +86,10 @@ def reduce_scatter_into(out, inp, group, ledger=None, mesh="", dims="", P=1):
     import torch.distributed as dist
     if P == 1 or group is None:
         out.copy_(inp)
+    elif _host_staged(out):
+        o = out.cpu()
+        dist.reduce_scatter_tensor(o, inp.cpu(), op=dist.ReduceOp.SUM, group=group)
+        out.copy_(o)
     else:
         dist.reduce_scatter_tensor(out, inp, op=dist.ReduceOp.SUM, group=group)
     if ledger is not None:
@@ -81,7 +98,11 @@ def reduce_scatter_into(out, inp, group, ledger=None, mesh="", dims="", P=1):
 
 def all_reduce_into(buf, group, ledger=None, mesh="", dims="", P=1):
     import torch.distributed as dist
-    if P > 1 and group is not None:
+    if P > 1 and group is not None and _host_staged(buf):
+        b = buf.cpu()
+        dist.all_reduce(b, op=dist.ReduceOp.SUM, group=group)
+        buf.copy_(b)
+    elif P > 1 and group is not None:
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
     if ledger is not None:
         ledger.record("all_reduce", buf.numel() * buf.element_size(), P, mesh, dims)

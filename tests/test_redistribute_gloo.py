@@ -90,12 +90,18 @@ def test_redistribute_matches_reference_golden(mesh_sizes):
     _spawn(_worker_golden, int(np.prod(mesh_sizes)), mesh_sizes)
 
 
-def _worker_fused_grads(rank, ws):
+def _worker_fused_grads(rank, ws, cuda=False):
     from cpu_mover import TorchCpuMover
     from paper_2509_07003_b200 import comm, create_mesh
     from paper_2509_07003_b200.dtensor import from_local
     from paper_2509_07003_b200.placement import ShardSpec, parse_placements
-    mover = TorchCpuMover()
+    if cuda:  # CUDA pack/unpack kernels, host-staged gloo collectives (see _worker_golden_cuda)
+        os.environ["SDR_COMM_CPU_STAGING"] = "1"
+        torch.cuda.set_device(0)
+        from paper_2509_07003_b200.movers import CudaMover
+        mover = CudaMover()
+    else:
+        mover = TorchCpuMover()
     mesh = create_mesh([("dp", 2), ("tp", 2)])
     coord = mesh.coords_of_rank(rank)
     specs = ["P,P", "P,S(0)", "P,P", "R,P", "S(1),R"]
@@ -107,11 +113,11 @@ def _worker_fused_grads(rank, ws):
         v = local_shape_and_offset(spec, shp, coord)
         g = torch.Generator().manual_seed(100 * i + rank)
         loc = torch.randint(-4, 5, v.local_shape, generator=g).double()
-        grads.append(from_local(loc, spec, shp, coord))
+        grads.append(from_local(loc.cuda() if cuda else loc, spec, shp, coord))
     # expected: sum over the Partial fibers, computed with gathered locals
     expect = []
     for gr in grads:
-        t = gr.local.clone()
+        t = gr.local.cpu().clone()
         pd = gr.meta.spec.partial_mesh_dims()
         if pd:
             grp, _ = comm.fiber_group(mesh, pd)
@@ -121,7 +127,7 @@ def _worker_fused_grads(rank, ws):
     out_b, rep_b = comm.bucketed_grad_reduce(grads, bucket_bytes=64, ledger=l1, mover=mover)
     out_f, rep_f = comm.fused_nd_grad_reduce(grads, bucket_bytes=1 << 20, ledger=l2, mover=mover)
     for e, b, f, g in zip(expect, out_b, out_f, grads):
-        assert torch.equal(e, b.local) and torch.equal(e, f.local)
+        assert torch.equal(e, b.local.cpu()) and torch.equal(e, f.local.cpu())
         assert b.meta.spec == f.meta.spec
         assert not b.meta.spec.partial_mesh_dims()
     assert len(rep_b["skipped"]) == 1 and len(rep_f["skipped"]) == 1
@@ -158,3 +164,49 @@ def _worker_many_mixed(rank, ws):
 
 def test_redistribute_many_mixed_dtypes_gloo():
     _spawn(_worker_many_mixed, 3)
+
+
+def _worker_golden_cuda(rank, ws, mesh_sizes):
+    """The same golden cases with device tensors and the CUDA pack/unpack
+    kernels; every process shares cuda:0 and gloo carries the (host-staged)
+    collectives (SDR_COMM_CPU_STAGING=1)."""
+    os.environ["SDR_COMM_CPU_STAGING"] = "1"
+    torch.cuda.set_device(0)
+    from paper_2509_07003_b200 import comm, create_mesh
+    from paper_2509_07003_b200.dtensor import from_local, redistribute, redistribute_many
+    from paper_2509_07003_b200.movers import CudaMover
+    from paper_2509_07003_b200.placement import ShardSpec, parse_placements
+    man, arr = _golden()
+    mover = CudaMover()
+    mesh = create_mesh([(f"m{j}", s) for j, s in enumerate(mesh_sizes)])
+    coord = mesh.coords_of_rank(rank)
+    tag = "_".join(map(str, coord))
+    cases = [c for c in man["redistribute"] if tuple(c["mesh"]) == tuple(mesh_sizes)]
+    xs, dsts, wants = [], [], []
+    for c in cases:
+        src = ShardSpec(mesh, parse_placements(c["src"]))
+        dst = ShardSpec(mesh, parse_placements(c["dst"]))
+        loc = torch.from_numpy(np.ascontiguousarray(arr[c["key"] + "_in_" + tag])).cuda()
+        x = from_local(loc, src, tuple(c["shape"]), coord)
+        y = redistribute(x, dst, comm.CollectiveLedger(), mover=mover)
+        want = arr[c["key"] + "_out_" + tag]
+        assert y.local.is_cuda
+        assert y.local.cpu().numpy().tobytes() == np.ascontiguousarray(want).tobytes(), (c, coord)
+        xs.append(x)
+        dsts.append(dst)
+        wants.append(want)
+    ys = redistribute_many(xs, dsts, comm.CollectiveLedger(), mover=mover)
+    for y, want, c in zip(ys, wants, cases):
+        assert y.local.cpu().numpy().tobytes() == np.ascontiguousarray(want).tobytes(), ("many", c)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mesh_sizes", [(4,), (2, 4)])
+def test_redistribute_golden_cuda_movers_multiprocess(mesh_sizes):
+    _spawn(_worker_golden_cuda, int(np.prod(mesh_sizes)), mesh_sizes)
+
+
+@pytest.mark.gpu
+def test_bucketed_and_fused_grad_reduce_cuda_movers_multiprocess():
+    _spawn(_worker_fused_grads, 4, True)
+
