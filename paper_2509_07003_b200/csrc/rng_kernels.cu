@@ -553,8 +553,11 @@ __device__ __forceinline__ void mbar_wait_parity0(uint32_t bar) {
   } while (!done);
 }
 
+// Issue the bulk copy (thread 0) and make the barrier visible to the CTA;
+// returns the barrier to pass to stage_lut_wait.  Work that does not read the
+// tables (e.g. the first chunk's Philox) can run between the two.
 template <typename LUT>
-__device__ __forceinline__ void stage_lut(LUT* dst, const LUT* src) {
+__device__ __forceinline__ uint32_t stage_lut_begin(LUT* dst, const LUT* src) {
   static_assert(sizeof(LUT) % 16 == 0 && sizeof(LUT) < (1u << 20), "LUT size");
   __shared__ __align__(8) uint64_t s_bar;
   const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&s_bar));
@@ -569,7 +572,14 @@ __device__ __forceinline__ void stage_lut(LUT* dst, const LUT* src) {
            "r"(static_cast<uint32_t>(sizeof(LUT))), "r"(bar) : "memory");
   }
   __syncthreads();  // barrier initialised before anyone polls it
-  mbar_wait_parity0(bar);
+  return bar;
+}
+
+__device__ __forceinline__ void stage_lut_wait(uint32_t bar) { mbar_wait_parity0(bar); }
+
+template <typename LUT>
+__device__ __forceinline__ void stage_lut(LUT* dst, const LUT* src) {
+  stage_lut_wait(stage_lut_begin(dst, src));
 }
 
 template <int DIST, int DT>
@@ -738,12 +748,30 @@ __device__ __forceinline__ void fill_chunk(const FillArgs& A, const NormalLut* L
 }
 
 // Values of the kV elements with global indices j0 .. j0+kV-1.
+template <int DIST, int DT>
+__device__ __forceinline__ void values_from_words(const FillArgs& A, const NormalLut* L,
+                                                  const uint32_t (&w0)[kV], const uint32_t (&w1)[kV],
+                                                  typename St<DT>::T (&v)[kV]);
+
+template <bool ALIGNED>
+__device__ __forceinline__ void fill_words(const FillArgs& A, uint64_t j0, uint32_t (&w0)[kV],
+                                           uint32_t (&w1)[kV]) {
+  if constexpr (ALIGNED) chunk_words_aligned<kV>(A.g, j0, w0, w1);
+  else chunk_words<kV>(A.g, j0, w0, w1);
+}
+
 template <int DIST, int DT, bool ALIGNED>
 __device__ __forceinline__ void chunk_values(const FillArgs& A, const NormalLut* L, uint64_t j0,
                                              typename St<DT>::T (&v)[kV]) {
   uint32_t w0[kV], w1[kV];
-  if constexpr (ALIGNED) chunk_words_aligned<kV>(A.g, j0, w0, w1);
-  else chunk_words<kV>(A.g, j0, w0, w1);
+  fill_words<ALIGNED>(A, j0, w0, w1);
+  values_from_words<DIST, DT>(A, L, w0, w1, v);
+}
+
+template <int DIST, int DT>
+__device__ __forceinline__ void values_from_words(const FillArgs& A, const NormalLut* L,
+                                                  const uint32_t (&w0)[kV], const uint32_t (&w1)[kV],
+                                                  typename St<DT>::T (&v)[kV]) {
   if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
     normal_chunk_bf16<kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v);
   } else if constexpr (DIST == SDR_NORMAL && DT != SDR_F64) {
@@ -807,14 +835,15 @@ __device__ __forceinline__ void fill_elem(const FillArgs& A, const NormalLut* L,
 template <int DIST, int DT, bool ALIGNED>
 __global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_fast(const __grid_constant__ FillArgs A) {
   const NormalLut* L = nullptr;
+  uint32_t bar = 0;  // Normal: tables arriving by TMA (waited on before first use)
   if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
     extern __shared__ __align__(16) unsigned char s_dyn[];  // sizeof(NormalLut32), set at launch
     NormalLut32* s_lut32 = reinterpret_cast<NormalLut32*>(s_dyn);
-    stage_lut(s_lut32, A.d.nm.lut32);
+    bar = stage_lut_begin(s_lut32, A.d.nm.lut32);
     L = reinterpret_cast<const NormalLut*>(s_lut32);
   } else if constexpr (DIST == SDR_NORMAL) {
     __shared__ __align__(16) NormalLut s_lut;
-    stage_lut(&s_lut, A.d.nm.lut);
+    bar = stage_lut_begin(&s_lut, A.d.nm.lut);
     L = &s_lut;
   }
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -822,13 +851,31 @@ __global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_fast(const __grid_c
   if (A.walk.on) {
     uint64_t cq;
     uint64_t j = walk_start(A.ix, A.div_cpr, q, kV, cq);
+    if constexpr (DIST == SDR_NORMAL) {
+      // first chunk peeled: its Philox words overlap the table transfer
+      if (q < A.nchunks) {
+        using T = typename St<DT>::T;
+        uint32_t w0[kV], w1[kV];
+        fill_words<ALIGNED>(A, j, w0, w1);
+        stage_lut_wait(bar);
+        T v[kV];
+        values_from_words<DIST, DT>(A, L, w0, w1, v);
+        store_chunk(static_cast<T*>(A.out) + q * kV, v);
+        walk_next(A.walk, A.chunks_per_row, j, cq);
+        q += stride;
+      } else {
+        stage_lut_wait(bar);
+      }
+    }
     for (; q < A.nchunks; q += stride) {
       fill_chunk_at<DIST, DT, ALIGNED>(A, L, q, j);
       walk_next(A.walk, A.chunks_per_row, j, cq);
     }
   } else if (A.ragged) {
+    if constexpr (DIST == SDR_NORMAL) stage_lut_wait(bar);
     for (; q < A.nchunks; q += stride) fill_chunk_ragged<DIST, DT, ALIGNED>(A, L, q);
   } else {
+    if constexpr (DIST == SDR_NORMAL) stage_lut_wait(bar);
     for (; q < A.nchunks; q += stride) fill_chunk<DIST, DT, ALIGNED>(A, L, q);
   }
 }
