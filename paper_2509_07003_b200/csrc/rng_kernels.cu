@@ -899,7 +899,10 @@ __global__ void __launch_bounds__(256) k_fill_generic(const __grid_constant__ Fi
 // cut into tiles of kTileElems elements; CTAs walk the global tile list, stage
 // the member's descriptor in shared memory once per tile and fill it.  One
 // launch initialises every parameter of a model (model.py:121-132).
-constexpr uint64_t kTileElems = 16384;
+#ifndef SDR_TILE_ELEMS
+#define SDR_TILE_ELEMS 131072  // elements per tile of the batched fill (measured: 16K..256K, 128K best overall)
+#endif
+constexpr uint64_t kTileElems = SDR_TILE_ELEMS;
 
 template <int DIST, int DT>
 __global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_batch(const FillArgs* __restrict__ descs,
