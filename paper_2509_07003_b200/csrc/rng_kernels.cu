@@ -1032,6 +1032,9 @@ __device__ __noinline__ typename St<YT>::T drop_nan_fix(typename St<XT>::T x) {
   }
 }
 
+#ifndef SDR_PDL
+#define SDR_PDL 1  // programmatic dependent launch for the dropout kernel
+#endif
 #ifndef SDR_DROP_MINB
 #define SDR_DROP_MINB 4
 #endif
@@ -1103,6 +1106,13 @@ __global__ void __launch_bounds__(256, SDR_DROP_MINB) k_dropout_fast(const __gri
   YTy* y = static_cast<YTy*>(A.y);
   constexpr int CH = kDropCh;
   constexpr int NE = CH / SDR_DROP_SPLIT;
+#if SDR_PDL
+  // Programmatic dependent launch: let the next kernel on the stream start its
+  // CTAs as ours drain, and wait here until the previous grid's memory is
+  // visible (a no-op when launched without the attribute).
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < A.nchunks;
        q += stride) {
@@ -1706,14 +1716,34 @@ int fill(void* out, int dt, const sdr_dist& dist, const sdr_rng& rng, const sdr_
   }
 }
 
+// 256-thread launch with programmatic stream serialization (PDL) when SDR_PDL.
+template <typename K, typename Args>
+static void launch_pdl(K kernel, int grid, cudaStream_t s, const Args& A) {
+#if SDR_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, A);
+#else
+  kernel<<<grid, 256, 0, s>>>(A);
+#endif
+}
+
 template <int XT, int YT, int MT>
 static int launch_drop(const DropArgs& A, bool fast, cudaStream_t s) {
   if (A.ragged)
     k_dropout_ragged<XT, YT, MT><<<grid_for(k_dropout_ragged<XT, YT, MT>, A.nchunks, 256), 256, 0, s>>>(A);
   else if (fast && A.aligned)
-    k_dropout_fast<XT, YT, MT, true><<<grid_for(k_dropout_fast<XT, YT, MT, true>, A.nchunks, 256), 256, 0, s>>>(A);
+    launch_pdl(k_dropout_fast<XT, YT, MT, true>, grid_for(k_dropout_fast<XT, YT, MT, true>, A.nchunks, 256), s, A);
   else if (fast)
-    k_dropout_fast<XT, YT, MT, false><<<grid_for(k_dropout_fast<XT, YT, MT, false>, A.nchunks, 256), 256, 0, s>>>(A);
+    launch_pdl(k_dropout_fast<XT, YT, MT, false>, grid_for(k_dropout_fast<XT, YT, MT, false>, A.nchunks, 256), s, A);
   else
     k_dropout_generic<XT, YT, MT><<<grid_for(k_dropout_generic<XT, YT, MT>, A.ix.cv.numel, 256), 256, 0, s>>>(A);
   return check_launch();
