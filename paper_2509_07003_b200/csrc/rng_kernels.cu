@@ -321,6 +321,12 @@ __constant__ double c_npoly[9] = {
     kK1 * kK1 * kK1 * kK1 / 24.0, -0.5 * kK1 * kK1,   // cos(K d) - 1 = d^2 (c4 d^2 + c2)
     -kK1 * kK1 * kK1 / 6.0, kK1,                      // sin(K d) = d (s3 d^2 + K)
     0x1.62e42fefa39efp0};                             // 2 ln 2
+#ifndef SDR_PDL
+// Programmatic dependent launch for the dropout and fill fast kernels.  Every
+// PDL-launched kernel executes griddepcontrol.wait before touching memory the
+// previous grid may use, so early launch never reorders data accesses.
+#define SDR_PDL 1
+#endif
 #ifndef SDR_NORMAL_BF16_F32
 #define SDR_NORMAL_BF16_F32 1  // certified float32 Box-Muller for bfloat16 outputs
 #endif
@@ -834,6 +840,9 @@ __device__ __forceinline__ void fill_elem(const FillArgs& A, const NormalLut* L,
 
 template <int DIST, int DT, bool ALIGNED>
 __global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_fast(const __grid_constant__ FillArgs A) {
+#if SDR_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   const NormalLut* L = nullptr;
   uint32_t bar = 0;  // Normal: tables arriving by TMA (waited on before first use)
   if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
@@ -846,6 +855,11 @@ __global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_fast(const __grid_c
     bar = stage_lut_begin(&s_lut, A.d.nm.lut);
     L = &s_lut;
   }
+#if SDR_PDL
+  // previous grid's memory visible before any store (the constant tables may
+  // already be in flight: they are never written by a kernel)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (A.walk.on) {
@@ -1032,9 +1046,6 @@ __device__ __noinline__ typename St<YT>::T drop_nan_fix(typename St<XT>::T x) {
   }
 }
 
-#ifndef SDR_PDL
-#define SDR_PDL 1  // programmatic dependent launch for the dropout kernel
-#endif
 #ifndef SDR_DROP_MINB
 #define SDR_DROP_MINB 4
 #endif
@@ -1610,6 +1621,26 @@ static void setup_chunks(const CanonView& cv, bool fast, uint64_t& nchunks, uint
   div_cpr = FastDiv64(cpr > 0 ? cpr : 1);
 }
 
+// 256-thread launch with programmatic stream serialization (PDL) when SDR_PDL.
+template <typename K, typename Args>
+static void launch_pdl(K kernel, int grid, cudaStream_t s, const Args& A, size_t dyn_smem = 0) {
+#if SDR_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = dyn_smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, A);
+#else
+  kernel<<<grid, 256, dyn_smem, s>>>(A);
+#endif
+}
+
 // Dynamic shared memory of the fill kernels (the float32 Normal tables exceed
 // the 48 KiB static limit), with the opt-in attribute set before each launch.
 template <int DIST, int DT>
@@ -1629,12 +1660,12 @@ static void launch_fill(const FillArgs& A0, bool fast, cudaStream_t s) {
     allow_dyn_smem(k_fill_fast<DIST, DT, true>, dsm);
     const int grid = grid_for(k_fill_fast<DIST, DT, true>, A.nchunks, 256, dsm);
     set_walk(A.walk, A.ix.cv, A.chunks_per_row, static_cast<uint64_t>(grid) * 256, kV);
-    k_fill_fast<DIST, DT, true><<<grid, 256, dsm, s>>>(A);
+    launch_pdl(k_fill_fast<DIST, DT, true>, grid, s, A, dsm);
   } else if (fast) {
     allow_dyn_smem(k_fill_fast<DIST, DT, false>, dsm);
     const int grid = grid_for(k_fill_fast<DIST, DT, false>, A.nchunks, 256, dsm);
     set_walk(A.walk, A.ix.cv, A.chunks_per_row, static_cast<uint64_t>(grid) * 256, kV);
-    k_fill_fast<DIST, DT, false><<<grid, 256, dsm, s>>>(A);
+    launch_pdl(k_fill_fast<DIST, DT, false>, grid, s, A, dsm);
   } else {
     k_fill_generic<DIST, DT><<<grid_for(k_fill_generic<DIST, DT>, A.ix.cv.numel, 256), 256, 0, s>>>(A);
   }
@@ -1714,26 +1745,6 @@ int fill(void* out, int dt, const sdr_dist& dist, const sdr_rng& rng, const sdr_
     case SDR_BERNOULLI: return dispatch_fill_dt<SDR_BERNOULLI>(dt, A, fast, s);
     default: return SDR_E_DIST;
   }
-}
-
-// 256-thread launch with programmatic stream serialization (PDL) when SDR_PDL.
-template <typename K, typename Args>
-static void launch_pdl(K kernel, int grid, cudaStream_t s, const Args& A) {
-#if SDR_PDL
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kernel, A);
-#else
-  kernel<<<grid, 256, 0, s>>>(A);
-#endif
 }
 
 template <int XT, int YT, int MT>
