@@ -45,8 +45,8 @@ struct CopyJob {
 constexpr int64_t kTileBytes = SDR_COPY_TILE;
 
 template <typename V>
-__global__ void __launch_bounds__(256) k_copy_tiles(const CopyJob* __restrict__ jobs,
-                                                    const int64_t* __restrict__ prefix, int n) {
+__device__ __forceinline__ void copy_tile(const CopyJob* __restrict__ jobs,
+                                          const int64_t* __restrict__ prefix, int n) {
   constexpr int U = static_cast<int>(kTileBytes / (sizeof(V) * 256));
   const int64_t t = blockIdx.x;
   int lo = 0, hi = n - 1;
@@ -106,6 +106,29 @@ __global__ void __launch_bounds__(256) k_copy_tiles(const CopyJob* __restrict__ 
     if (static_cast<int>(threadIdx.x) + u * 256 < total) *dv[u] = v[u];
 }
 
+// Job table in device memory (large calls).
+template <typename V>
+__global__ void __launch_bounds__(256) k_copy_tiles(const CopyJob* __restrict__ jobs,
+                                                    const int64_t* __restrict__ prefix, int n) {
+  copy_tile<V>(jobs, prefix, n);
+}
+
+// Small calls (the common case: a layer's members x ranks): the job table is a
+// kernel parameter -- no allocation or H2D copy per call, and the launch is
+// stream-capturable into a CUDA graph.
+constexpr int kParamJobs = 96;
+struct JobTable {
+  int32_t n;
+  int32_t pad_;
+  int64_t prefix[kParamJobs];
+  CopyJob jobs[kParamJobs];
+};
+
+template <typename V>
+__global__ void __launch_bounds__(256) k_copy_tiles_p(const __grid_constant__ JobTable T) {
+  copy_tile<V>(T.jobs, T.prefix, T.n);
+}
+
 static int widest(std::initializer_list<int64_t> vals) {
   int64_t acc = 0;
   for (int64_t v : vals) acc |= v;
@@ -150,6 +173,26 @@ static int run_jobs(const std::vector<CopyJob>& jobs, cudaStream_t s) {
     prefix[i] = tiles;
     tiles += jobs[i].tiles;
   }
+  // vector width of the whole call: the narrowest job's (jobs are few and large)
+  int vec = 16;
+  for (const CopyJob& J : jobs) vec = J.vec < vec ? J.vec : vec;
+  const unsigned grid = static_cast<unsigned>(tiles);
+  if (n <= kParamJobs) {
+    JobTable T;
+    memset(static_cast<void*>(&T), 0, sizeof(T));
+    T.n = n;
+    for (int i = 0; i < n; ++i) {
+      T.prefix[i] = prefix[i];
+      T.jobs[i] = jobs[i];
+    }
+    switch (vec) {
+      case 16: k_copy_tiles_p<uint4><<<grid, 256, 0, s>>>(T); break;
+      case 8: k_copy_tiles_p<uint2><<<grid, 256, 0, s>>>(T); break;
+      case 4: k_copy_tiles_p<uint32_t><<<grid, 256, 0, s>>>(T); break;
+      default: k_copy_tiles_p<unsigned char><<<grid, 256, 0, s>>>(T); break;
+    }
+    return check_launch();
+  }
   CopyJob* d_jobs = nullptr;
   int64_t* d_prefix = nullptr;
   cudaError_t e = cudaMallocAsync(&d_jobs, sizeof(CopyJob) * n, s);
@@ -160,10 +203,6 @@ static int run_jobs(const std::vector<CopyJob>& jobs, cudaStream_t s) {
     set_cuda_error(e);
     return SDR_E_CUDA;
   }
-  // vector width of the whole call: the narrowest job's (jobs are few and large)
-  int vec = 16;
-  for (const CopyJob& J : jobs) vec = J.vec < vec ? J.vec : vec;
-  const unsigned grid = static_cast<unsigned>(tiles);
   switch (vec) {
     case 16: k_copy_tiles<uint4><<<grid, 256, 0, s>>>(d_jobs, d_prefix, n); break;
     case 8: k_copy_tiles<uint2><<<grid, 256, 0, s>>>(d_jobs, d_prefix, n); break;

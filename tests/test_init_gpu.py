@@ -188,3 +188,30 @@ def test_cfg4_llama3_8b_tp8_shards_equal_tp1(kind):
 def _bf16():
     import ml_dtypes
     return ml_dtypes.bfloat16
+
+
+def test_pack_kernels_capture_in_cuda_graph():
+    """Small calls pass the job table as a kernel parameter: pack/unpack of a
+    layer's members is stream-capturable and replays to the eager result."""
+    P = 2
+    shapes = [((64, 48), 1), ((33, 16), 0), ((16,), 0)]
+    full_m, outs = [], []
+    for shp, dim in shapes:
+        f = torch.randn(shp, device="cuda", dtype=torch.bfloat16)
+        outer, inner, rows = int(np.prod(shp[:dim])), int(np.prod(shp[dim + 1:])), shp[dim]
+        full_m.append(Member(f, outer, rows, inner, -(-rows // P)))
+    seg = layout(full_m)
+    mv = CudaMover()
+    eager = torch.zeros(seg * P, dtype=torch.uint8, device="cuda")  # pad rows stay 0 in both
+    mv.pack_scatter(full_m, eager, seg, P)
+    packed = torch.zeros(seg * P, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            mv.pack_scatter(full_m, packed, seg, P)
+    packed.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(packed, eager)
