@@ -1,7 +1,10 @@
-"""Secondary bench workloads (BASELINE configs 1, 4, 5), same JSON shape as
-bench.py's main line.  `python bench.py --workload randn|init|redistribute`.
+"""Secondary bench workloads (BASELINE configs 1, 3, 4, 5), same JSON shape as
+bench.py's main line.  `python bench.py --workload randn|embed|init|redistribute`.
 
 randn        cfg1: Normal(0,1) f32 [4096,4096] Shard(0) over N ranks (strong)
+embed        cfg3: [50257,4096] embedding on a DP x TP mesh, Shard(0),Shard(1)
+             (uneven rows): Normal(0,0.02) and the std-matched Uniform, f32 and
+             bf16 (strong; value = normal f32)
 init         cfg4: all 291 LLaMA-3-8B params, Normal(0,0.02) bf16, TP=N (strong)
 redistribute cfg5: one LLaMA-3-8B layer's params on DP x TP: fused all-gather over
              DP (S->R) then reduce-scatter of same-shaped grads (P->S); at N=1
@@ -38,7 +41,8 @@ def _time(fn, steps, warmup, dev, ws):
     torch.cuda.synchronize(dev)
     if ws > 1:
         dist.barrier()
-    t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64, device=dev)
+    share = os.environ.get("SDR_BENCH_SHARE_GPU") == "1"
+    t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64, device="cpu" if share else dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.item()
@@ -48,10 +52,15 @@ def run(a):
     from paper_2509_07003_b200 import create_mesh, init as I, rng as R
     from paper_2509_07003_b200.placement import ShardSpec, local_shape_and_offset, parse_placements
     ws, rank, local = _env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    share = os.environ.get("SDR_BENCH_SHARE_GPU") == "1"  # test hook, as in bench.py
+    gpu = 0 if share else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     line = {"n_gpus": ws, "steps": a.steps, "warmup": a.warmup, "higher_is_better": True,
             "vs_baseline": None, "data": "synthetic", "gpu_launches": a.steps}
     if a.workload == "randn":
@@ -68,6 +77,31 @@ def run(a):
                     ms_per_step=round(ms, 4), scaling="strong", dtype="f32",
                     config={"workload": "cfg1: randn f32 [4096,4096] Shard(0)", "parallelism": f"dp{ws}",
                             "elements_per_s": round(n / ms * 1e3, 1)})
+    elif a.workload == "embed":
+        shape = (50257, 4096)
+        dp = 2 if ws % 2 == 0 else 1
+        tp = ws // dp
+        mesh = create_mesh([("dp", dp), ("tp", tp)])
+        spec = ShardSpec(mesh, parse_placements("S(0),S(1)"))
+        v = local_shape_and_offset(spec, shape, mesh.coords_of_rank(rank))
+        R.ensure_normal_tables(dev)
+        b = math.sqrt(3) * 0.02
+        n = math.prod(shape)
+        rates = {}
+        for dname, dist_ in (("normal", R.Normal(0.0, 0.02)), ("uniform", R.Uniform(-b, b))):
+            for dt, tdt, nm in ((np.float32, torch.float32, "f32"), ("bfloat16", torch.bfloat16, "bf16")):
+                out = torch.empty(v.local_shape, dtype=tdt, device=dev)
+                st = R.RngState(1234)
+                ms_ = _time(lambda: R.fill_random(v, st, dist_, dt, out=out), a.steps, a.warmup, dev, ws)
+                rates[f"{dname}_{nm}"] = (ms_, n * out.element_size() / ms_ / 1e6)
+        ms, gbs = rates["normal_f32"]
+        line.update(metric="2-D mesh embedding init GB/s (cfg3)", value=round(gbs, 3), unit="GB/s",
+                    ms_per_step=round(ms, 4), scaling="strong", dtype="f32",
+                    config={"workload": "cfg3: [50257,4096] S(0),S(1) on dp x tp, normal(0,0.02) f32 "
+                                        "(uniform and bf16 variants in `variants`)",
+                            "parallelism": f"dp{dp}xtp{tp}", "local_shape": list(v.local_shape),
+                            "elements_per_s": round(n / ms * 1e3, 1),
+                            "variants": {k: {"ms": round(m_, 4), "GB/s": round(g_, 1)} for k, (m_, g_) in rates.items()}})
     elif a.workload == "init":
         params = I.llama3_8b_params(lambda nm, s: R.Normal(0.0, 0.02), "bfloat16")
         mesh = create_mesh([("tp", ws)])

@@ -14,7 +14,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv 
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1
 rm -f gpurun_out/bench_extra.log
-for w in randn init redistribute; do timeout 600 python bench.py --workload $w --steps 5 --warmup 3 >> gpurun_out/bench_extra.log 2>&1; done
+for w in randn embed init redistribute; do timeout 600 python bench.py --workload $w --steps 5 --warmup 3 >> gpurun_out/bench_extra.log 2>&1; done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_dropout_fast -s 4 -c 1 -o gpurun_out/prof_dropout -f python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
 else
