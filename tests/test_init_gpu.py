@@ -215,3 +215,37 @@ def test_pack_kernels_capture_in_cuda_graph():
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(packed, eager)
+
+
+@pytest.mark.parametrize("P", [2, 8])
+def test_cfg5_full_layer_pack_round_trip(P):
+    """BASELINE config 5 at full size: one LLaMA-3-8B layer's 9 bf16 tensors
+    (q,k,v,gate,up split on dim 1; o,down on dim 0; the norms) packed
+    rank-major for a reduce-scatter and unpacked after a gather reproduce the
+    tensors bit for bit, and rank k's local segment equals its rank segment."""
+    d, ff, kv = 4096, 14336, 1024
+    shapes = [((d, d), 1), ((kv, d), 1), ((kv, d), 1), ((d, d), 0), ((ff, d), 1), ((ff, d), 1),
+              ((d, ff), 0), ((d,), 0), ((d,), 0)]
+    mv = CudaMover()
+    full_m, fulls = [], []
+    for shp, dim in shapes:
+        f = torch.randint(-30000, 30000, shp, device="cuda", dtype=torch.int16).view(torch.bfloat16)
+        outer, inner, rows = int(np.prod(shp[:dim])), int(np.prod(shp[dim + 1:])), shp[dim]
+        full_m.append(Member(f, outer, rows, inner, -(-rows // P)))
+        fulls.append(f)
+    seg = layout(full_m)
+    packed = torch.zeros(seg * P, dtype=torch.uint8, device="cuda")
+    mv.pack_scatter(full_m, packed, seg, P)
+    outs = [Member(torch.empty_like(m.tensor), m.outer, m.rows, m.inner, m.chunk, m.seg_off) for m in full_m]
+    mv.unpack_gathered(outs, packed, seg, P)
+    for o, f in zip(outs, fulls):
+        assert torch.equal(o.tensor.view(torch.int16), f.view(torch.int16))
+    k = P - 1
+    locs = []
+    for (shp, dim), m in zip(shapes, full_m):
+        lo = min(m.rows, k * m.chunk)
+        n = min(m.rows, lo + m.chunk) - lo
+        locs.append(Member(m.tensor.narrow(dim, lo, n).contiguous(), m.outer, n, m.inner, m.chunk, m.seg_off))
+    segbuf = torch.zeros(seg, dtype=torch.uint8, device="cuda")
+    mv.pack_local(locs, segbuf)
+    assert torch.equal(segbuf, packed[k * seg:(k + 1) * seg])
