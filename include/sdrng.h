@@ -13,6 +13,12 @@
  *  - The caller owns every buffer.  Device buffers are plain device pointers.
  *  - The library holds no RNG state: (seed, offset, theta) are passed by value
  *    and advanced by the caller exactly as rng.py:95-98.
+ *  - The fill and dropout fast kernels use programmatic dependent launch: a
+ *    following PDL launch may start its CTAs while ours drain, and every one of
+ *    our kernels executes griddepcontrol.wait before touching memory a previous
+ *    grid may use, so stream order is preserved for all data.  Launches are
+ *    CUDA-graph capturable (the pack/unpack job table of calls with <= 96 jobs
+ *    is a kernel parameter; larger calls stage it with cudaMallocAsync).
  *  - A window ("view") of a row-major global tensor of rank `ndim` is given per
  *    tensor dim d by global_shape[d], local_start[d], local_len[d], and for
  *    InterleavedShard dims groups[d] (m) and group_stride[d] (global distance
