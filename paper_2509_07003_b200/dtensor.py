@@ -251,6 +251,76 @@ def redistribute_many(xs: list[DTensor], dsts: list[ShardSpec],
     return out
 
 
+# Coalesced collectives are cut into buckets of about this many send bytes
+# (whole members; a larger member is a bucket of its own) and pipelined: the
+# pack of bucket b+1 and the unpack of bucket b-1 run on the current stream
+# while bucket b's collective runs on a side stream, so the HBM copies overlap
+# the wire instead of adding to it.  One bucket = the plain pack/collective/
+# unpack sequence.
+PIPELINE_BUCKET_BYTES = 64 << 20
+
+
+def _buckets(sizes: list[int], cap: int | None = None) -> list[list[int]]:
+    cap = PIPELINE_BUCKET_BYTES if cap is None else cap
+    out, used = [[]], 0
+    for i, n in enumerate(sizes):
+        if out[-1] and used + n > cap:
+            out.append([])
+            used = 0
+        out[-1].append(i)
+        used += n
+    return out
+
+
+class _Pipeline:
+    """pack (current stream) -> collective (side stream) -> unpack (current
+    stream, one bucket behind), with events between the streams and the
+    caching allocator told about the side-stream use of each buffer."""
+
+    def __init__(self, dev):
+        self.cuda = dev.type == "cuda"
+        self.cur = torch.cuda.current_stream(dev) if self.cuda else None
+        self.side = _side_stream(dev) if self.cuda else None
+        self.pending = []
+
+    def collective(self, run, buffers, unpack):
+        if not self.cuda:
+            run()
+            unpack()
+            return
+        ready = torch.cuda.Event()
+        ready.record(self.cur)
+        with torch.cuda.stream(self.side):
+            self.side.wait_event(ready)
+            run()
+            done = torch.cuda.Event()
+            done.record(self.side)
+        for b in buffers:
+            b.record_stream(self.side)
+        self.pending.append((done, unpack))
+        if len(self.pending) > 1:  # unpack the previous bucket behind this one's collective
+            self._unpack_oldest()
+
+    def _unpack_oldest(self):
+        done, unpack = self.pending.pop(0)
+        self.cur.wait_event(done)
+        unpack()
+
+    def drain(self):
+        while self.pending:
+            self._unpack_oldest()
+
+
+_SIDE_STREAMS: dict = {}
+
+
+def _side_stream(dev):
+    s = _SIDE_STREAMS.get(dev)
+    if s is None:
+        s = _SIDE_STREAMS[dev] = torch.cuda.Stream(dev)
+    return s
+
+
 def _fused_gather(mesh, md, items, ledger, mover):
     """items: (x, [spec, local]) with a shard-like placement on md -> Replicate."""
     P = mesh.sizes[md]
@@ -283,15 +353,23 @@ def _fused_gather(mesh, md, items, ledger, mover):
         slot[0] = slot[0].with_placement(md, Replicate())
         slot[1] = outs[0]
         return
-    seg = layout(send_members)
-    for s, r in zip(send_members, recv_members):
-        r.seg_off = s.seg_off
     dev = items[0][1][1].device
-    send = torch.empty(seg, dtype=torch.uint8, device=dev)
-    recv = torch.empty(seg * P, dtype=torch.uint8, device=dev)
-    mover.pack_local(send_members, send)
-    comm.all_gather_into(recv, send, group, ledger, mesh.name, mesh.dim_names[md], P)
-    mover.unpack_gathered(recv_members, recv, seg, P)
+    pipe = _Pipeline(dev)
+    # bucket by the PADDED rank-segment bytes: identical on every rank of the
+    # fiber (local shard sizes differ for uneven splits), so all ranks issue the
+    # same sequence of collectives
+    for idx in _buckets([m.outer * m.chunk * m.inner * m.tensor.element_size() for m in send_members]):
+        sm, rm = [send_members[i] for i in idx], [recv_members[i] for i in idx]
+        seg = layout(sm)
+        for a, b in zip(sm, rm):
+            b.seg_off = a.seg_off
+        send = torch.empty(seg, dtype=torch.uint8, device=dev)
+        recv = torch.empty(seg * P, dtype=torch.uint8, device=dev)
+        mover.pack_local(sm, send)
+        pipe.collective(lambda r=recv, s_=send: comm.all_gather_into(
+            r, s_, group, ledger, mesh.name, mesh.dim_names[md], P), (send, recv),
+            lambda r=recv, rm_=rm, sg=seg: mover.unpack_gathered(rm_, r, sg, P))
+    pipe.drain()
     for (x, slot), full in zip(items, outs):
         slot[0] = slot[0].with_placement(md, Replicate())
         slot[1] = full
@@ -328,18 +406,23 @@ def _fused_reduce_scatter(mesh, md, items, ledger, mover):
         slot[0] = slot[0].with_placement(md, dst_p)
         slot[1] = outs[0]
         return
-    seg = layout(full_members, align=16)
-    for f, pm in zip(full_members, piece_members):
-        pm.seg_off = f.seg_off
     dt = items[0][1][1].dtype
     es = items[0][1][1].element_size()
     dev = items[0][1][1].device
-    # pad rows / alignment gaps are summed but never read back: no memset needed
-    packed = torch.empty(seg * P // es, dtype=dt, device=dev)
-    mover.pack_scatter(full_members, packed.view(torch.uint8), seg, P)
-    piece_buf = torch.empty(seg // es, dtype=dt, device=dev)
-    comm.reduce_scatter_into(piece_buf, packed, group, ledger, mesh.name, mesh.dim_names[md], P)
-    mover.unpack_local(piece_members, piece_buf.view(torch.uint8))
+    pipe = _Pipeline(dev)
+    for idx in _buckets([m.outer * m.chunk * m.inner * m.tensor.element_size() for m in full_members]):
+        fm, pm = [full_members[i] for i in idx], [piece_members[i] for i in idx]
+        seg = layout(fm, align=16)
+        for f, q in zip(fm, pm):
+            q.seg_off = f.seg_off
+        # pad rows / alignment gaps are summed but never read back: no memset needed
+        packed = torch.empty(seg * P // es, dtype=dt, device=dev)
+        mover.pack_scatter(fm, packed.view(torch.uint8), seg, P)
+        piece_buf = torch.empty(seg // es, dtype=dt, device=dev)
+        pipe.collective(lambda o=piece_buf, i=packed: comm.reduce_scatter_into(
+            o, i, group, ledger, mesh.name, mesh.dim_names[md], P), (packed, piece_buf),
+            lambda pb=piece_buf, pm_=pm: mover.unpack_local(pm_, pb.view(torch.uint8)))
+    pipe.drain()
     for (x, slot, dst_p), out in zip(items, outs):
         slot[0] = slot[0].with_placement(md, dst_p)
         slot[1] = out

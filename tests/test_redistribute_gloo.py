@@ -50,8 +50,11 @@ def _golden():
     return man, np.load(os.path.join(HERE, "golden", "golden.npz"))
 
 
-def _worker_golden(rank, ws, mesh_sizes):
+def _worker_golden(rank, ws, mesh_sizes, bucket_bytes=None):
     from cpu_mover import TorchCpuMover
+    from paper_2509_07003_b200 import dtensor as DT
+    if bucket_bytes is not None:
+        DT.PIPELINE_BUCKET_BYTES = bucket_bytes
     from paper_2509_07003_b200 import comm, create_mesh
     from paper_2509_07003_b200.dtensor import from_local, redistribute, redistribute_many
     from paper_2509_07003_b200.placement import ShardSpec, parse_placements
@@ -82,12 +85,20 @@ def _worker_golden(rank, ws, mesh_sizes):
     for y, want, c in zip(ys, wants, cases):
         assert y.local.numpy().tobytes() == np.ascontiguousarray(want).tobytes(), ("many", c)
     per_dim_kinds = len(ledger.entries)
-    assert per_dim_kinds <= 3 * len(mesh_sizes), ledger.entries
+    if bucket_bytes is None:  # one coalesced collective per (dim, kind)
+        assert per_dim_kinds <= 3 * len(mesh_sizes), ledger.entries
+    elif bucket_bytes == 1:  # one collective per member
+        assert per_dim_kinds >= len(cases), ledger.entries
 
 
 @pytest.mark.parametrize("mesh_sizes", [(4,), (2,), (2, 4)])
 def test_redistribute_matches_reference_golden(mesh_sizes):
     _spawn(_worker_golden, int(np.prod(mesh_sizes)), mesh_sizes)
+
+
+def test_redistribute_many_bucketed_pipeline_golden():
+    """One member per bucket (the pipelined path) still reproduces the reference."""
+    _spawn(_worker_golden, 8, (2, 4), 1)
 
 
 def _worker_fused_grads(rank, ws, cuda=False):
@@ -166,12 +177,16 @@ def test_redistribute_many_mixed_dtypes_gloo():
     _spawn(_worker_many_mixed, 3)
 
 
-def _worker_golden_cuda(rank, ws, mesh_sizes):
+def _worker_golden_cuda(rank, ws, mesh_sizes, bucket_bytes=None):
     """The same golden cases with device tensors and the CUDA pack/unpack
     kernels; every process shares cuda:0 and gloo carries the (host-staged)
-    collectives (SDR_COMM_CPU_STAGING=1)."""
+    collectives (SDR_COMM_CPU_STAGING=1).  bucket_bytes forces the pipelined
+    multi-bucket path (pack / side-stream collective / unpack)."""
     os.environ["SDR_COMM_CPU_STAGING"] = "1"
     torch.cuda.set_device(0)
+    from paper_2509_07003_b200 import dtensor as DT
+    if bucket_bytes is not None:
+        DT.PIPELINE_BUCKET_BYTES = bucket_bytes
     from paper_2509_07003_b200 import comm, create_mesh
     from paper_2509_07003_b200.dtensor import from_local, redistribute, redistribute_many
     from paper_2509_07003_b200.movers import CudaMover
@@ -201,12 +216,18 @@ def _worker_golden_cuda(rank, ws, mesh_sizes):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mesh_sizes", [(4,), (2, 4)])
-def test_redistribute_golden_cuda_movers_multiprocess(mesh_sizes):
-    _spawn(_worker_golden_cuda, int(np.prod(mesh_sizes)), mesh_sizes)
+@pytest.mark.parametrize("mesh_sizes,bucket", [((4,), None), ((2, 4), None), ((4,), 64), ((2, 4), 1)])
+def test_redistribute_golden_cuda_movers_multiprocess(mesh_sizes, bucket):
+    _spawn(_worker_golden_cuda, int(np.prod(mesh_sizes)), mesh_sizes, bucket)
 
 
 @pytest.mark.gpu
 def test_bucketed_and_fused_grad_reduce_cuda_movers_multiprocess():
     _spawn(_worker_fused_grads, 4, True)
 
+
+
+def test_redistribute_many_bucketed_uneven_golden():
+    """Bucket boundaries must not depend on a rank's (uneven) shard size:
+    64-byte buckets over the golden cases, whose shards are uneven."""
+    _spawn(_worker_golden, 4, (4,), 64)
