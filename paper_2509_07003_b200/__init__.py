@@ -35,6 +35,7 @@ from .rng import (
     generate_local,
 )
 from .ops import dropout
+from .dtensor import DTensor, DTensorMeta, distribute, from_local, redistribute, redistribute_many, to_global
 
 __all__ = [
     "DeviceMesh", "MeshError", "create_mesh",
@@ -43,4 +44,7 @@ __all__ = [
     "RngState", "Uniform01", "Uniform", "Normal", "RandInt", "Bernoulli",
     "fill_random", "generate_global", "generate_distributed", "generate_local",
     "dropout_mask_local", "dropout",
+    # reference top-level exports (spmdsim/__init__.py:3-32)
+    "DTensor", "DTensorMeta", "distribute", "redistribute", "to_global",
+    "from_local", "redistribute_many",
 ]

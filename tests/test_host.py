@@ -195,3 +195,14 @@ def test_host_pipeline_blocks_tile_the_window():
                 start = (s.start or 0) if isinstance(s, slice) else s
                 assert w.start == v.windows[d].start + start
         assert (seen == 1).all(), (gshape, pl, chunks)
+
+
+def test_reference_top_level_exports_present():
+    """Every name the reference package exports at top level
+    (spmdsim/__init__.py:3-32) is importable from this package."""
+    import paper_2509_07003_b200 as S
+    ref = ["DeviceMesh", "create_mesh", "Placement", "Shard", "Replicate", "Partial", "InterleavedShard",
+           "ShardSpec", "ShardView", "DTensor", "DTensorMeta", "distribute", "redistribute", "to_global",
+           "RngState"]
+    assert [n for n in ref if not hasattr(S, n)] == []
+    assert set(ref) <= set(S.__all__)
