@@ -111,6 +111,56 @@ def all_reduce_into(buf, group, ledger=None, mesh="", dims="", P=1):
 # ---------------------------------------------------------------------------
 # Bucketed and N-dim fused gradient reduction (comm.py:130-289).
 # ---------------------------------------------------------------------------
+# ---------------------------------------------------------------------------
+# Single-process collectives over per-participant tensors (reference
+# comm.py:91-125): the simulator's forms, kept for drop-in code that builds
+# every coordinate's buffer in one process.  Sums run in ascending group-rank
+# order on the tensors' device, exactly like the reference.
+# ---------------------------------------------------------------------------
+def all_reduce(buffers, ledger=None, mesh: str = "", dims: str = ""):
+    """Sum in ascending group-rank order; every participant gets the result."""
+    shapes = {tuple(b.shape) for b in buffers}
+    if len(shapes) != 1:
+        raise CommError(f"all_reduce buffer shape mismatch: {shapes}")
+    acc = buffers[0].clone()
+    for b in buffers[1:]:
+        acc += b
+    if ledger is not None:
+        ledger.record("all_reduce", buffers[0].numel() * buffers[0].element_size(), len(buffers), mesh, dims)
+    return acc
+
+
+def all_gather(shards, ledger=None, mesh: str = "", dims: str = ""):
+    """Every participant receives the full shard list, in group-rank order."""
+    if ledger is not None:
+        ledger.record("all_gather", sum(s.numel() * s.element_size() for s in shards), len(shards), mesh, dims)
+    return list(shards)
+
+
+def reduce_scatter(buffers, slicer, ledger=None, mesh: str = "", dims: str = ""):
+    """Sum in ascending group-rank order, then hand participant k slicer(sum, k)."""
+    shapes = {tuple(b.shape) for b in buffers}
+    if len(shapes) != 1:
+        raise CommError(f"reduce_scatter buffer shape mismatch: {shapes}")
+    acc = buffers[0].clone()
+    for b in buffers[1:]:
+        acc += b
+    if ledger is not None:
+        ledger.record("reduce_scatter", buffers[0].numel() * buffers[0].element_size(), len(buffers), mesh, dims)
+    return [slicer(acc, k) for k in range(len(buffers))]
+
+
+@dataclass
+class GradBucket:
+    """One greedy gradient bucket (reference comm.py:131-138)."""
+    capacity_bytes: int
+    members: list = field(default_factory=list)  # DTensor refs
+    member_bytes: int = 0
+
+    def fits(self, nbytes: int) -> bool:
+        return not self.members or self.member_bytes + nbytes <= self.capacity_bytes
+
+
 def bucketize(tensors, capacity_bytes: int) -> list[list]:
     """Greedy buckets over the REVERSED creation order (gradients become ready
     back to front); a tensor larger than the capacity gets a bucket of its

@@ -143,6 +143,13 @@ def from_local(local: torch.Tensor, spec: ShardSpec, global_shape, coord=None) -
     return t
 
 
+def from_locals(locals_: dict, spec: ShardSpec, global_shape) -> dict:
+    """The reference's single-process constructor (dtensor.py:149-154) from
+    every coordinate's local tensor.  Here a DTensor is one rank's view, so
+    the result maps coord -> DTensor (each validated like from_local)."""
+    return {tuple(c): from_local(t, spec, global_shape, tuple(c)) for c, t in locals_.items()}
+
+
 def to_global(x: DTensor, ledger=None, mover=None) -> torch.Tensor:
     """Full tensor on every rank (redistribute to all-Replicate)."""
     rep = ShardSpec(x.mesh, tuple(Replicate() for _ in range(x.mesh.ndim)))
