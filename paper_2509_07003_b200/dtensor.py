@@ -112,6 +112,30 @@ class DTensor:
         if tuple(self.local.shape) != want:
             raise PlacementError(f"local at {self.coord}: shape {tuple(self.local.shape)}, expected {want}")
 
+    # --- reference DTensor helpers (dtensor.py:90-133), per-rank forms -------
+    def local_nbytes_max(self) -> int:
+        """Largest local shard over the mesh, in bytes (dtensor.py:90-91),
+        from the spec alone: every rank gets the same value, no communication."""
+        es = self.local.element_size()
+        return max(math.prod(local_shape_and_offset(self.meta.spec, self.shape, c).local_shape) * es
+                   for c in self.mesh.iter_coords())
+
+    def with_spec_and_locals(self, spec: ShardSpec, local: torch.Tensor) -> "DTensor":
+        return DTensor(replace(self.meta, spec=spec), local, self.coord)
+
+    def map_locals(self, fn) -> "DTensor":
+        return DTensor(self.meta, fn(self.local), self.coord)
+
+    def ones_like(self) -> "DTensor":
+        if any(isinstance(p, Partial) for p in self.meta.spec.placements):
+            raise RedistributeError("ones_like undefined for Partial placements")
+        return DTensor(replace(self.meta, requires_grad=False), torch.ones_like(self.local), self.coord)
+
+    def debug_dump(self) -> str:
+        flat = self.local.reshape(-1)
+        head = ",".join(f"{v:g}" for v in flat[:64].double().cpu().tolist())
+        return f"coord={self.coord} shape={list(self.local.shape)} data=[{head}{',...' if flat.numel() > 64 else ''}]"
+
     def __repr__(self):
         return f"DTensor(shape={self.shape}, spec={self.meta.spec}, dtype={self.dtype}, coord={self.coord})"
 

@@ -240,6 +240,18 @@ def test_reference_module_names_present():
         assert [n for n in names if not hasattr(o, n)] == [], mod
 
 
+def test_reference_class_methods_present():
+    """Public methods of the reference's core classes exist here too (DTensor's
+    per-rank forms, RngState, ShardSpec / ShardView, DeviceMesh, ledger)."""
+    import importlib
+    pairs = [("rng", "RngState"), ("placement", "ShardSpec"), ("placement", "ShardView"),
+             ("dtensor", "DTensor"), ("dtensor", "DTensorMeta"), ("mesh", "DeviceMesh")]
+    for mod, cls in pairs:
+        r = getattr(_ref_module(mod), cls)
+        o = getattr(importlib.import_module("paper_2509_07003_b200." + mod), cls)
+        assert [n for n in dir(r) if not n.startswith("_") and not hasattr(o, n)] == [], (mod, cls)
+
+
 def _ref_module(name):
     import importlib
     import sys
