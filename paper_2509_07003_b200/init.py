@@ -45,6 +45,26 @@ class Parameter:
     def materialized(self) -> bool:
         return self.value is not None
 
+    def materialize_global(self, state: RngState, *, device=None) -> torch.Tensor:
+        """Single-device eager init: the full global tensor (model.py:36-39);
+        advances `state` once."""
+        from .rng import generate_global
+        self.value = generate_global(self.shape, state, self.dist, self.dtype, device=device)
+        return self.value
+
+    def materialize_sharded(self, spec: ShardSpec, state: RngState, coord=None, *, device=None):
+        """Local-only init (model.py:41-46): this rank fills just its own shard
+        of the one global draw; advances `state` once.  Returns the DTensor
+        (the local shard is also kept in `value`)."""
+        from .dtensor import from_local
+        from .rng import generate_local
+        if coord is None:
+            import torch.distributed as dist_mod
+            rank = dist_mod.get_rank() if dist_mod.is_initialized() else 0
+            coord = spec.mesh.coords_of_rank(rank)
+        self.value = generate_local(spec, self.shape, state, self.dist, self.dtype, tuple(coord), device=device)
+        return from_local(self.value, spec, self.shape, tuple(coord))
+
 
 @functools.lru_cache(maxsize=4096)
 def _window(spec: ShardSpec, shape: tuple, coord: tuple):

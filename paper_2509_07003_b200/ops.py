@@ -320,3 +320,49 @@ def dropout_host(x_host: torch.Tensor, p: float, state: RngState, view: ShardVie
     cur.wait_stream(S["d2h"])
     torch.cuda.current_stream(dev).synchronize()
     return out
+
+
+# ---------------------------------------------------------------------------
+# Traced redistribute (reference ops.py:193-217): a placement change whose
+# backward sends the incoming gradient to `grad_spec` (default: the source
+# placement with Partial flipped to Replicate -- a Partial forward value
+# carries a replicated gradient).
+# ---------------------------------------------------------------------------
+class _RedistributeFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, local, x, dst, grad_spec, ledger):
+        from .dtensor import DTensor
+        from .dtensor import redistribute as dt_redistribute
+        src = DTensor(x.meta, local, x.coord)
+        y = dt_redistribute(src, dst, ledger)
+        ctx.meta, ctx.coord, ctx.dst, ctx.grad_spec, ctx.ledger = y.meta, x.coord, dst, grad_spec, ledger
+        return y.local
+
+    @staticmethod
+    def backward(ctx, g):
+        from dataclasses import replace as _replace
+        from .dtensor import DTensor
+        from .dtensor import redistribute as dt_redistribute
+        gd = DTensor(_replace(ctx.meta, dtype=g.dtype), g.contiguous(), ctx.coord)
+        if ctx.dst != ctx.grad_spec:
+            gd = dt_redistribute(gd, ctx.grad_spec, ctx.ledger)
+        return gd.local, None, None, None, None
+
+
+def redistribute(x, dst, grad_spec=None, ledger=None):
+    """Differentiable placement change of a DTensor (reference ops.py:193-217):
+    the forward is dtensor.redistribute; autograd on the local shard routes the
+    gradient back to `grad_spec`.  A plain (non-DTensor) tensor is returned
+    unchanged, as in the reference's single-device run."""
+    from dataclasses import replace as _replace
+    from .dtensor import DTensor
+    from .placement import Partial, Replicate, ShardSpec
+    if not isinstance(x, DTensor):
+        return x
+    if grad_spec is None:
+        src = x.meta.spec
+        grad_spec = ShardSpec(src.mesh, tuple(Replicate() if isinstance(p, Partial) else p
+                                              for p in src.placements))
+    local = _RedistributeFn.apply(x.local, x, dst, grad_spec, ledger)
+    return DTensor(_replace(x.meta, spec=dst), local, x.coord)
+

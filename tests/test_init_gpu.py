@@ -249,3 +249,21 @@ def test_cfg5_full_layer_pack_round_trip(P):
     segbuf = torch.zeros(seg, dtype=torch.uint8, device="cuda")
     mv.pack_local(locs, segbuf)
     assert torch.equal(segbuf, packed[k * seg:(k + 1) * seg])
+
+
+def test_parameter_materialize_global_and_sharded():
+    """Parameter.materialize_global / materialize_sharded (model.py:36-46): a
+    rank's shard equals its slice of the global init and both advance the
+    state by the same amount."""
+    mesh = S.create_mesh([("dp", 2), ("tp", 4)])
+    spec = ShardSpec(mesh, parse_placements("S(0),S(1)"))
+    p = I.Parameter((257, 64), R.Normal(0.0, 0.02), "bfloat16")
+    sg = R.RngState(9, 2, 64)
+    full = p.materialize_global(sg)
+    for coord in [(0, 0), (1, 3)]:
+        q = I.Parameter((257, 64), R.Normal(0.0, 0.02), "bfloat16")
+        ss = R.RngState(9, 2, 64)
+        d = q.materialize_sharded(spec, ss, coord)
+        v = local_shape_and_offset(spec, (257, 64), coord)
+        sl = tuple(slice(o, o + n) for o, n in zip(v.local_offset, v.local_shape))
+        assert torch.equal(bits(d.local), bits(full[sl])) and ss.offset == sg.offset

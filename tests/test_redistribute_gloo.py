@@ -231,3 +231,30 @@ def test_redistribute_many_bucketed_uneven_golden():
     """Bucket boundaries must not depend on a rank's (uneven) shard size:
     64-byte buckets over the golden cases, whose shards are uneven."""
     _spawn(_worker_golden, 4, (4,), 64)
+
+
+def _worker_traced_redistribute(rank, ws):
+    """ops.redistribute forward equals dtensor.redistribute; its backward sends
+    the gradient to the source placement (Partial flipped to Replicate)."""
+    from paper_2509_07003_b200 import create_mesh, ops
+    from paper_2509_07003_b200.dtensor import distribute, from_local, redistribute, to_global
+    from paper_2509_07003_b200.placement import ShardSpec, parse_placements
+    mesh = create_mesh([("dp", ws)])
+    coord = mesh.coords_of_rank(rank)
+    full = torch.arange(24, dtype=torch.float64).reshape(6, 4)
+    src = ShardSpec(mesh, parse_placements("S(0)"))
+    dst = ShardSpec(mesh, parse_placements("R"))
+    x = distribute(full, src, coord)
+    x.local.requires_grad_(True)
+    y = ops.redistribute(x, dst)
+    assert torch.equal(y.local.detach(), full)
+    w = torch.arange(24, dtype=torch.float64).reshape(6, 4) + 100 * rank
+    (y.local * w).sum().backward()
+    # grad of a Replicate output flows back to S(0): this rank's rows of w
+    # (the replicated cotangent is used as-is, as the reference does)
+    r0 = x.view.local_offset[0]
+    assert torch.equal(x.local.grad, w[r0:r0 + x.local.shape[0]])
+
+
+def test_traced_redistribute_gloo():
+    _spawn(_worker_traced_redistribute, 2)
