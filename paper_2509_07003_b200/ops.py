@@ -197,11 +197,17 @@ def _pipe_state(device, nbytes_in, nbytes_out, dtype_in, dtype_out, nbuf):
     key = (device, dtype_in, dtype_out, nbuf)
     st = _PIPE.get(key)
     if st is None or st["cap_in"] < nbytes_in or st["cap_out"] < nbytes_out:
+        if st is not None:  # in-flight (sync=False) work may still use the old buffers
+            for k in ("h2d", "comp", "d2h"):
+                st[k].synchronize()
         st = {"cap_in": nbytes_in, "cap_out": nbytes_out,
               "xin": [torch.empty(nbytes_in, dtype=torch.uint8, device=device) for _ in range(nbuf)],
               "yout": [torch.empty(nbytes_out, dtype=torch.uint8, device=device) for _ in range(nbuf)],
               "h2d": torch.cuda.Stream(device), "comp": torch.cuda.Stream(device),
-              "d2h": torch.cuda.Stream(device)}
+              "d2h": torch.cuda.Stream(device),
+              # per staging buffer: event after its last D2H (persists across calls so
+              # back-to-back sync=False calls never overwrite a buffer still being read)
+              "d2h_done": [None] * nbuf, "next": 0}
         _PIPE[key] = st
     return st
 
@@ -262,15 +268,19 @@ def _host_blocks(shape, view: ShardView, chunks: int):
 
 def dropout_host(x_host: torch.Tensor, p: float, state: RngState, view: ShardView | None = None, *,
                  out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None,
-                 device=None, chunks: int = 16) -> torch.Tensor:
+                 device=None, chunks: int = 16, sync: bool = True) -> torch.Tensor:
     """dropout_apply for a tensor in (pinned) HOST memory, result in host
     memory.  The window is cut into contiguous blocks of 1/chunks .. 1/8 of it
     (_host_blocks, tapered at both ends); block i's H2D copy, block i-1's fused kernel and block
     i-2's D2H copy run concurrently on three streams (PCIe is full duplex), so
     the end-to-end time approaches max(H2D, D2H) instead of their sum.  Values
     are identical to dropout_apply (each block is a sub-window of the same
-    global draw).  Does NOT advance `state`.  Blocks the host until the result
-    is ready."""
+    global draw).  Does NOT advance `state`.  With sync=True (default) it
+    blocks the host until the result is ready; with sync=False it returns at
+    once, stream-ordered after the caller's current stream (which waits for the
+    result): consecutive calls then keep both PCIe directions busy across
+    calls, like a prefetching input pipeline.  `x_host` must stay unchanged and
+    `out` unread until the stream reaches that point."""
     if x_host.is_cuda:
         raise ValueError("dropout_host expects a host tensor; use dropout_apply for device tensors")
     view = full_view(tuple(x_host.shape)) if view is None else view
@@ -290,11 +300,13 @@ def dropout_host(x_host: torch.Tensor, p: float, state: RngState, view: ShardVie
     S = _pipe_state(dev, cap * x_host.element_size(), cap * torch.empty((), dtype=yd).element_size(),
                     x_host.dtype, yd, nbuf)
     cur = torch.cuda.current_stream(dev)
-    d2h_done = [None] * nbuf
+    d2h_done = S["d2h_done"]
     for s in (S["h2d"], S["comp"], S["d2h"]):
         s.wait_stream(cur)
+    first = S["next"]
+    S["next"] = (first + len(blocks)) % nbuf
     for i, (ix, sub) in enumerate(blocks):
-        b = i % nbuf
+        b = (first + i) % nbuf
         xs = x_host[ix]
         n = xs.numel()
         if n == 0:
@@ -318,7 +330,8 @@ def dropout_host(x_host: torch.Tensor, p: float, state: RngState, view: ShardVie
             ev.record(S["d2h"])
             d2h_done[b] = ev
     cur.wait_stream(S["d2h"])
-    torch.cuda.current_stream(dev).synchronize()
+    if sync:
+        cur.synchronize()
     return out
 
 

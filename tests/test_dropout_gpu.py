@@ -219,3 +219,18 @@ def test_cuda_graph_capture_and_replay():
         assert torch.equal(bits(y), bits(ops.dropout_apply(x, p, ref, view)))
         ref.advance(x.numel())
     assert torch.equal(w, R.fill_random(S.placement.full_view((300, 64)), ref, R.Normal(0.0, 0.02), np.float32))
+
+
+def test_dropout_host_async_back_to_back():
+    """sync=False calls issued back to back (staging buffers reused across
+    calls) give exactly the per-call results once the stream is drained."""
+    shape, p = (8, 96, 64), 0.2
+    x = torch.randn(shape).to(torch.bfloat16).pin_memory()
+    outs = [torch.empty_like(x).pin_memory() for _ in range(5)]
+    st = R.RngState(31)
+    for i, o in enumerate(outs):
+        ops.dropout_host(x, p, R.RngState(31, i), out=o, chunks=4, sync=False)
+    torch.cuda.synchronize()
+    for i, o in enumerate(outs):
+        want = ops.dropout_apply(x.cuda(), p, R.RngState(31, i)).cpu()
+        assert torch.equal(bits(o), bits(want)), i
