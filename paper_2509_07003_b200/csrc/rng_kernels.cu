@@ -27,233 +27,9 @@
 #include <mutex>
 #include <vector>
 
-#include "sdr_core.cuh"
+#include "rng_common.cuh"
 
 namespace sdr {
-
-// ---------------------------------------------------------------------------
-// Generator parameters shared by fill and dropout.
-// ---------------------------------------------------------------------------
-struct Gen {
-  uint64_t theta;
-  uint64_t offset;
-  FastDiv64 div_theta;
-  RoundKeys keys;
-};
-
-inline Gen make_gen(const sdr_rng& r) {
-  Gen g;
-  g.theta = r.theta;
-  g.offset = r.offset;
-  g.div_theta = FastDiv64(r.theta);
-  g.keys = make_keys(r.seed);
-  return g;
-}
-
-// Rounds [R0, 10) for NE independent counters.
-template <int R0, int NE>
-__device__ __forceinline__ void rounds_from(const RoundKeys& K, uint32_t (&x0)[NE],
-                                            uint32_t (&x1)[NE], uint32_t (&x2)[NE],
-                                            uint32_t (&x3)[NE]) {
-#pragma unroll
-  for (int r = R0; r < 10; ++r) {
-#pragma unroll
-    for (int e = 0; e < NE; ++e) philox_round(x0[e], x1[e], x2[e], x3[e], K.k0[r], K.k1[r]);
-  }
-}
-
-// Words 0/1 of the blocks of global indices j0 .. j0+NE-1.
-template <int NE>
-__device__ __forceinline__ void chunk_words(const Gen& g, uint64_t j0, uint32_t (&w0)[NE],
-                                            uint32_t (&w1)[NE]) {
-  uint64_t b, t;
-  g.div_theta.divmod(j0, b, t);
-  const uint64_t beta = b + g.offset;
-  uint32_t x0[NE], x1[NE], x2[NE], x3[NE];
-  const RoundKeys& K = g.keys;
-  if (g.theta >= NE && t <= g.theta - NE && lo32(t) <= 0xFFFFFFFFu - (NE - 1)) {
-    // Shared beta: hoist the chunk-uniform products of rounds 1 and 2.
-    const uint32_t blo = lo32(beta), bhi = hi32(beta), tlo = lo32(t), thi = hi32(t);
-    const uint64_t pa = mul_wide(blo, kM0);
-    const uint32_t y2 = hi32(pa) ^ thi ^ K.k1[0];
-    const uint32_t y3 = lo32(pa);
-    const uint64_t pb0 = mul_wide(tlo, kM1);
-    const uint64_t pq = mul_wide(y2, kM1);
-    const uint32_t z1 = lo32(pq), hq = hi32(pq);
-#pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      const uint64_t pb = pb0 + static_cast<uint64_t>(e) * kM1;  // == M1*(tlo+e)
-      const uint32_t y0 = hi32(pb) ^ bhi ^ K.k0[0];
-      const uint32_t y1 = lo32(pb);
-      const uint64_t pa2 = mul_wide(y0, kM0);
-      x0[e] = hq ^ y1 ^ K.k0[1];
-      x1[e] = z1;
-      x2[e] = hi32(pa2) ^ y3 ^ K.k1[1];
-      x3[e] = lo32(pa2);
-    }
-    rounds_from<2, NE>(K, x0, x1, x2, x3);
-  } else {
-#pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      uint64_t be, te;
-      g.div_theta.divmod(j0 + e, be, te);
-      be += g.offset;
-      x0[e] = lo32(be);
-      x1[e] = hi32(be);
-      x2[e] = lo32(te);
-      x3[e] = hi32(te);
-    }
-    rounds_from<0, NE>(K, x0, x1, x2, x3);
-  }
-#pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    w0[e] = x0[e];
-    w1[e] = x1[e];
-  }
-}
-
-// Fast path when THETA is a power of two >= NE and every chunk starts at a
-// multiple of NE (host-checked): the chunk never straddles a THETA boundary,
-// so beta is chunk-uniform and no 64-bit division is needed.
-template <int NE>
-__device__ __forceinline__ void chunk_words_aligned(const Gen& g, uint64_t j0, uint32_t (&w0)[NE],
-                                                    uint32_t (&w1)[NE]) {
-  const uint32_t sh = g.div_theta.s;
-  const uint64_t beta = (j0 >> sh) + g.offset;
-  const uint64_t t = j0 & (g.theta - 1);
-  const RoundKeys& K = g.keys;
-  uint32_t x0[NE], x1[NE], x2[NE], x3[NE];
-  const uint32_t blo = lo32(beta), bhi = hi32(beta), tlo = lo32(t), thi = hi32(t);
-  const uint64_t pa = mul_wide(blo, kM0);
-  const uint32_t y2 = hi32(pa) ^ thi ^ K.k1[0];
-  const uint32_t y3 = lo32(pa);
-  const uint64_t pb0 = mul_wide(tlo, kM1);
-  const uint64_t pq = mul_wide(y2, kM1);
-  const uint32_t z1 = lo32(pq), hq = hi32(pq);
-#pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    const uint64_t pb = pb0 + static_cast<uint64_t>(e) * kM1;
-    const uint32_t y0 = hi32(pb) ^ bhi ^ K.k0[0];
-    const uint32_t y1 = lo32(pb);
-    const uint64_t pa2 = mul_wide(y0, kM0);
-    x0[e] = hq ^ y1 ^ K.k0[1];
-    x1[e] = z1;
-    x2[e] = hi32(pa2) ^ y3 ^ K.k1[1];
-    x3[e] = lo32(pa2);
-  }
-  rounds_from<2, NE>(K, x0, x1, x2, x3);
-#pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    w0[e] = x0[e];
-    w1[e] = x1[e];
-  }
-}
-
-// Word 1 only, for a keep/drop decision (dropout): the last two rounds need
-// just hi(M0*x0) of round 9 and lo(M1*x2) of round 10.  Same preconditions as
-// chunk_words_aligned.  A tie on the high threshold word (p = 2^-32) is
-// resolved by the caller with the full block.
-// Per-element part of the w1-only Philox given the chunk-uniform round-1/2
-// values (bhi, y3, hq, z1) and the 64-bit M1*tau of the chunk's first element.
-template <int NE>
-__device__ __forceinline__ void w1_body(const RoundKeys& K, uint32_t bhi, uint32_t y3, uint32_t hq,
-                                        uint32_t z1, uint64_t pb0, uint32_t (&w1)[NE]) {
-  uint32_t x0[NE], x1[NE], x2[NE], x3[NE];
-#pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    const uint64_t pb = pb0 + static_cast<uint64_t>(e) * kM1;
-    const uint32_t y0 = hi32(pb) ^ bhi ^ K.k0[0];
-    const uint32_t y1 = lo32(pb);
-    const uint64_t pa2 = mul_wide(y0, kM0);
-    x0[e] = hq ^ y1 ^ K.k0[1];
-    x1[e] = z1;
-    x2[e] = hi32(pa2) ^ y3 ^ K.k1[1];
-    x3[e] = lo32(pa2);
-  }
-#pragma unroll
-  for (int r = 2; r < 8; ++r) {
-#pragma unroll
-    for (int e = 0; e < NE; ++e) philox_round(x0[e], x1[e], x2[e], x3[e], K.k0[r], K.k1[r]);
-  }
-#pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    const uint32_t x2_9 = __umulhi(x0[e], kM0) ^ x3[e] ^ K.k1[8];  // round 9: x2 only
-    w1[e] = x2_9 * kM1;                                              // round 10: lo(M1*x2)
-  }
-}
-
-// Chunk-uniform round-1/2 values for counter (beta, tau0).
-struct Hoist {
-  uint32_t bhi, y3, hq, z1;
-};
-__device__ __forceinline__ Hoist hoist_beta(const RoundKeys& K, uint64_t beta, uint32_t thi) {
-  const uint64_t pa = mul_wide(lo32(beta), kM0);
-  const uint32_t y2 = hi32(pa) ^ thi ^ K.k1[0];
-  const uint64_t pq = mul_wide(y2, kM1);
-  return Hoist{hi32(beta), lo32(pa), hi32(pq), lo32(pq)};
-}
-
-// Word 1 only, for a keep/drop decision (dropout): the last two rounds need
-// just hi(M0*x0) of round 9 and lo(M1*x2) of round 10.  Same preconditions as
-// chunk_words_aligned.  A tie on the high threshold word (p = 2^-32) is
-// resolved by the caller with the full block.
-template <int NE>
-__device__ __forceinline__ void chunk_w1_aligned(const Gen& g, uint64_t j0, uint32_t (&w1)[NE]) {
-  const uint32_t sh = g.div_theta.s;
-  const uint64_t beta = (j0 >> sh) + g.offset;
-  const uint64_t t = j0 & (g.theta - 1);
-  const Hoist H = hoist_beta(g.keys, beta, hi32(t));
-  w1_body<NE>(g.keys, H.bhi, H.y3, H.hq, H.z1, mul_wide(lo32(t), kM1), w1);
-}
-
-// Words of one element at global index j (generic path).
-__device__ __forceinline__ void elem_words(const Gen& g, uint64_t j, uint32_t& w0, uint32_t& w1) {
-  uint64_t b, t;
-  g.div_theta.divmod(j, b, t);
-  b += g.offset;
-  uint32_t x0 = lo32(b), x1 = hi32(b), x2 = lo32(t), x3 = hi32(t);
-#pragma unroll
-  for (int r = 0; r < 10; ++r) philox_round(x0, x1, x2, x3, g.keys.k0[r], g.keys.k1[r]);
-  w0 = x0;
-  w1 = x1;
-}
-
-// ---------------------------------------------------------------------------
-// Output element types and conversions (NumPy / ml_dtypes semantics).
-// ---------------------------------------------------------------------------
-template <int DT> struct St;
-template <> struct St<SDR_F32> { using T = float; };
-template <> struct St<SDR_F64> { using T = double; };
-template <> struct St<SDR_BF16> { using T = uint16_t; };
-template <> struct St<SDR_F16> { using T = uint16_t; };
-template <> struct St<SDR_I64> { using T = int64_t; };
-template <> struct St<SDR_I32> { using T = int32_t; };
-template <> struct St<SDR_U8> { using T = uint8_t; };
-template <> struct St<SDR_BOOL> { using T = uint8_t; };
-
-__device__ __forceinline__ uint16_t bf16_bits(float f) {
-  return __bfloat16_as_ushort(__float2bfloat16_rn(f));
-}
-
-// float64 -> dtype with a single NumPy cast; bfloat16 goes through float32
-// first exactly like ml_dtypes' float64->bfloat16 cast.
-template <int DT>
-__device__ __forceinline__ typename St<DT>::T from_f64(double v) {
-  if constexpr (DT == SDR_F32) return __double2float_rn(v);
-  else if constexpr (DT == SDR_F64) return v;
-  else if constexpr (DT == SDR_BF16) return bf16_bits(__double2float_rn(v));
-  else if constexpr (DT == SDR_F16) return __half_as_ushort(__double2half(v));
-  else return typename St<DT>::T(0);
-}
-
-template <int DT>
-__device__ __forceinline__ typename St<DT>::T one_or_zero(bool b) {
-  if constexpr (DT == SDR_F32) return b ? 1.0f : 0.0f;
-  else if constexpr (DT == SDR_F64) return b ? 1.0 : 0.0;
-  else if constexpr (DT == SDR_BF16) return b ? uint16_t(0x3F80) : uint16_t(0);
-  else if constexpr (DT == SDR_F16) return b ? uint16_t(0x3C00) : uint16_t(0);
-  else return static_cast<typename St<DT>::T>(b ? 1 : 0);
-}
 
 // ---------------------------------------------------------------------------
 // Distribution parameters and the Normal mirror state.
@@ -321,12 +97,6 @@ __constant__ double c_npoly[9] = {
     kK1 * kK1 * kK1 * kK1 / 24.0, -0.5 * kK1 * kK1,   // cos(K d) - 1 = d^2 (c4 d^2 + c2)
     -kK1 * kK1 * kK1 / 6.0, kK1,                      // sin(K d) = d (s3 d^2 + K)
     0x1.62e42fefa39efp0};                             // 2 ln 2
-#ifndef SDR_PDL
-// Programmatic dependent launch for the dropout and fill fast kernels.  Every
-// PDL-launched kernel executes griddepcontrol.wait before touching memory the
-// previous grid may use, so early launch never reorders data accesses.
-#define SDR_PDL 1
-#endif
 #ifndef SDR_NORMAL_BF16_F32
 #define SDR_NORMAL_BF16_F32 1  // certified float32 Box-Muller for bfloat16 outputs
 #endif
@@ -623,66 +393,6 @@ __device__ __forceinline__ typename St<DT>::T dist_value(const DistP& P, const N
   }
 }
 
-// ---------------------------------------------------------------------------
-// Vector stores of kV elements.
-// ---------------------------------------------------------------------------
-template <typename T, int N>
-__device__ __forceinline__ void store_chunk(T* p, const T (&v)[N]) {
-  constexpr int bytes = sizeof(T) * N;
-  if constexpr (bytes == 4) {
-    uint32_t q;
-    memcpy(&q, v, 4);
-    __stcs(reinterpret_cast<unsigned int*>(p), q);
-  } else if constexpr (bytes == 8) {
-    uint2 q;
-    memcpy(&q, v, 8);
-    __stcs(reinterpret_cast<uint2*>(p), q);
-  } else {
-    static_assert(bytes % 16 == 0, "chunk must be 4, 8 or a multiple of 16 bytes");
-    uint4 q[bytes / 16];
-    memcpy(q, v, bytes);
-#pragma unroll
-    for (int i = 0; i < bytes / 16; ++i) __stcs(reinterpret_cast<uint4*>(p) + i, q[i]);
-  }
-}
-
-template <typename T, int N>
-__device__ __forceinline__ void load_chunk(const T* p, T (&v)[N]) {
-  constexpr int bytes = sizeof(T) * N;
-  if constexpr (bytes == 4) {
-    const uint32_t q = __ldcs(reinterpret_cast<const unsigned int*>(p));
-    memcpy(v, &q, 4);
-  } else if constexpr (bytes == 8) {
-    const uint2 q = __ldcs(reinterpret_cast<const uint2*>(p));
-    memcpy(v, &q, 8);
-  } else {
-    static_assert(bytes % 16 == 0, "chunk must be 4, 8 or a multiple of 16 bytes");
-    uint4 q[bytes / 16];
-#pragma unroll
-    for (int i = 0; i < bytes / 16; ++i) q[i] = __ldcs(reinterpret_cast<const uint4*>(p) + i);
-    memcpy(v, q, bytes);
-  }
-}
-
-// Global flat index of chunk q (CH elements inside one row of the canonical
-// view, nd >= 1): row/column by the launch-constant chunks-per-row divisor, the
-// inner outer-dims by their sizes; the outermost digit needs no division (the
-// row index is below its extent).
-__device__ __forceinline__ uint64_t outer_base(const ViewIndexer& ix, const FastDiv64& div_cpr,
-                                               uint64_t q, int CH) {
-  uint64_t row, cq;
-  div_cpr.divmod(q, row, cq);
-  const CanonView& cv = ix.cv;
-  uint64_t j = static_cast<uint64_t>(cv.base) + cq * CH;
-  for (int k = cv.nd - 1; k >= 1; --k) {
-    uint64_t qq, r;
-    ix.div_o[k].divmod(row, qq, r);
-    j += r * static_cast<uint64_t>(cv.ostride[k]);
-    row = qq;
-  }
-  return j + row * static_cast<uint64_t>(cv.ostride[0]);
-}
-
 // Incremental chunk walk of a grid-stride loop over a view with at most one
 // outer dim (nd <= 1): after one division for the first chunk, each step of
 // S = gridDim*blockDim chunks adds dj to the global index and dcq to the
@@ -971,299 +681,6 @@ __global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_batch(const FillArg
   }
 }
 
-// ---------------------------------------------------------------------------
-// Fused dropout: y = (x*m)*scale, m from Bernoulli(1-p) (engine.py:80-81).
-// ---------------------------------------------------------------------------
-struct DropArgs {
-  Gen g;
-  ViewIndexer ix;
-  const void* x;
-  void* y;
-  void* mask;
-  uint64_t keep_le;   // keep <=> (w1:w0) <= keep_le, i.e. k53 < ceil((1-p)*2^53)
-  uint32_t aligned;   // THETA pow2 >= chunk and every chunk start chunk-aligned
-  float scale32;
-  double scale64;
-  uint16_t scale16;  // f16 bits of the scale
-  uint32_t ragged;   // inner extent not a multiple of the chunk: k_dropout_ragged
-  uint64_t nchunks;
-  uint64_t chunks_per_row;
-  FastDiv64 div_cpr;
-};
-
-template <int XT> struct DropT { using T = typename St<XT>::T; };
-
-// y element for input dtype XT and output dtype YT; sets `nan` when the
-// result is a NaN (then drop_nan_fix() supplies the x86/NumPy bit pattern).
-template <int XT, int YT>
-__device__ __forceinline__ typename St<YT>::T drop_apply(const DropArgs& A, typename St<XT>::T x,
-                                                         bool keep, bool& nan) {
-  if constexpr (XT == SDR_F32) {
-    const float y = __fmul_rn(__fmul_rn(x, keep ? 1.0f : 0.0f), A.scale32);
-    nan = y != y;
-    return y;
-  } else if constexpr (XT == SDR_F64) {
-    const double y = __dmul_rn(__dmul_rn(x, keep ? 1.0 : 0.0), A.scale64);
-    nan = y != y;
-    return y;
-  } else if constexpr (XT == SDR_BF16) {
-    const float xf = __uint_as_float(static_cast<uint32_t>(x) << 16);
-    const float y = __fmul_rn(__fmul_rn(xf, keep ? 1.0f : 0.0f), A.scale32);
-    nan = y != y;
-    if constexpr (YT == SDR_F32) return y;
-    else return bf16_bits(y);
-  } else {  // SDR_F16: x*m exact in f16, then RNE(x16 * scale16)
-    const __half xh = __ushort_as_half(x);
-    const __half xm = __hmul(xh, keep ? __ushort_as_half(0x3C00) : __ushort_as_half(0));
-    const uint16_t y = __half_as_ushort(__hmul(xm, __ushort_as_half(A.scale16)));
-    nan = (y & 0x7FFFu) > 0x7C00u;
-    return y;
-  }
-}
-
-// NaN results as x86 SSE + NumPy / ml_dtypes produce them: a NaN input is
-// propagated quieted with its payload, inf*0 gives the negative default NaN;
-// float32->bfloat16 maps NaN to 0x7FC0 / 0xFFC0 (ml_dtypes), float->half keeps
-// sign and the top payload bits (numpy npy_floatbits_to_halfbits).
-template <int XT, int YT>
-__device__ __noinline__ typename St<YT>::T drop_nan_fix(typename St<XT>::T x) {
-  if constexpr (XT == SDR_F32) {
-    const uint32_t b = __float_as_uint(x);
-    return __uint_as_float((b & 0x7FFFFFFFu) > 0x7F800000u ? (b | 0x00400000u) : 0xFFC00000u);
-  } else if constexpr (XT == SDR_F64) {
-    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(x));
-    const bool isn = (b & 0x7FFFFFFFFFFFFFFFull) > 0x7FF0000000000000ull;
-    return __longlong_as_double(static_cast<long long>(isn ? (b | 0x0008000000000000ull)
-                                                           : 0xFFF8000000000000ull));
-  } else if constexpr (XT == SDR_BF16) {
-    const uint32_t b = static_cast<uint32_t>(x) << 16;
-    const uint32_t f = (b & 0x7FFFFFFFu) > 0x7F800000u ? (b | 0x00400000u) : 0xFFC00000u;
-    if constexpr (YT == SDR_F32) return __uint_as_float(f);
-    else return static_cast<uint16_t>((f & 0x80000000u) ? 0xFFC0u : 0x7FC0u);
-  } else {
-    const uint16_t b = x;
-    return static_cast<uint16_t>((b & 0x7FFFu) > 0x7C00u ? (b | 0x0200u) : 0xFE00u);
-  }
-}
-
-#ifndef SDR_DROP_MINB
-#define SDR_DROP_MINB 4
-#endif
-#ifndef SDR_DROP_SPLIT
-#define SDR_DROP_SPLIT 1   // Philox for the chunk in SPLIT passes
-#endif
-#ifndef SDR_DROP_CH
-#define SDR_DROP_CH 8      // elements per thread-chunk of the dropout kernel
-#endif
-constexpr int kDropCh = SDR_DROP_CH;
-
-__device__ __forceinline__ uint64_t drop_chunk_base(const DropArgs& A, uint64_t q) {
-  const CanonView& cv = A.ix.cv;
-  if (cv.nd == 0) return static_cast<uint64_t>(cv.base) + q * kDropCh;  // one contiguous run
-  return outer_base(A.ix, A.div_cpr, q, kDropCh);
-}
-
-
-// bf16 lanes of a 32-bit word as float32 (PRMT / LOP3 on the ALU pipe).
-__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(__byte_perm(w, 0u, 0x1044)); }
-__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
-
-// y = (x*m)*scale for one chunk given its keep flags; NaN fix-up; stores y
-// (and the mask when requested).
-template <int XT, int YT, int MT, int CH>
-__device__ __forceinline__ void drop_store(const DropArgs& A, uint64_t q,
-                                           const typename St<XT>::T (&xv)[CH], const bool (&keep)[CH]) {
-  using XTy = typename St<XT>::T;
-  using YTy = typename St<YT>::T;
-  YTy yv[CH];
-  bool anynan = false, nan[CH];
-#pragma unroll
-  for (int e = 0; e < CH; ++e) {
-    if constexpr (XT == SDR_BF16) {
-      uint32_t wd;
-      memcpy(&wd, &xv[e & ~1], 4);
-      const float xf = (e & 1) ? bf16_hi(wd) : bf16_lo(wd);
-      const float r = __fmul_rn(__fmul_rn(xf, keep[e] ? 1.0f : 0.0f), A.scale32);
-      nan[e] = r != r;
-      if constexpr (YT == SDR_F32) yv[e] = r;
-      else yv[e] = bf16_bits(r);
-    } else {
-      yv[e] = drop_apply<XT, YT>(A, xv[e], keep[e], nan[e]);
-    }
-    anynan |= nan[e];
-  }
-  if (anynan) {
-#pragma unroll
-    for (int e = 0; e < CH; ++e)
-      if (nan[e]) yv[e] = drop_nan_fix<XT, YT>(xv[e]);
-  }
-  store_chunk(static_cast<YTy*>(A.y) + q * CH, yv);
-  if constexpr (MT >= 0) {
-    using MTy = typename St<MT>::T;
-    if (A.mask != nullptr) {
-      MTy mv[CH];
-#pragma unroll
-      for (int e = 0; e < CH; ++e) mv[e] = one_or_zero<MT>(keep[e]);
-      store_chunk(static_cast<MTy*>(A.mask) + q * CH, mv);
-    }
-  }
-}
-
-template <int XT, int YT, int MT, bool ALIGNED>
-__global__ void __launch_bounds__(256, SDR_DROP_MINB) k_dropout_fast(const __grid_constant__ DropArgs A) {
-  using XTy = typename St<XT>::T;
-  using YTy = typename St<YT>::T;
-  const XTy* x = static_cast<const XTy*>(A.x);
-  YTy* y = static_cast<YTy*>(A.y);
-  constexpr int CH = kDropCh;
-  constexpr int NE = CH / SDR_DROP_SPLIT;
-#if SDR_PDL
-  // Programmatic dependent launch: let the next kernel on the stream start its
-  // CTAs as ours drain, and wait here until the previous grid's memory is
-  // visible (a no-op when launched without the attribute).
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < A.nchunks;
-       q += stride) {
-    XTy xv[CH];
-    load_chunk(x + q * CH, xv);
-    const uint64_t j0 = drop_chunk_base(A, q);  // (an incremental walk measured slower here)
-    YTy yv[CH];
-    bool keep[CH], anynan = false, nan[CH];
-#pragma unroll
-    for (int h = 0; h < SDR_DROP_SPLIT; ++h) {
-      uint32_t w0[NE], w1[NE];
-      if constexpr (ALIGNED) {
-        chunk_w1_aligned<NE>(A.g, j0 + h * NE, w1);
-      } else {
-        chunk_words<NE>(A.g, j0 + h * NE, w0, w1);
-      }
-#pragma unroll
-      for (int i = 0; i < NE; ++i) {
-        const int e = h * NE + i;
-        if constexpr (ALIGNED) {
-          // (w1:w0) <= keep_le is decided by w1 unless w1 equals its high word
-          // (p = 2^-32): per-element rare branch (measured faster than one
-          // merged branch per chunk)
-          const uint32_t H = hi32(A.keep_le);
-          keep[e] = w1[i] < H;
-          if (__builtin_expect(w1[i] == H, 0)) {
-            uint32_t f0, f1;
-            elem_words(A.g, j0 + e, f0, f1);
-            keep[e] = ((static_cast<uint64_t>(f1) << 32) | f0) <= A.keep_le;
-          }
-        }
-        if constexpr (!ALIGNED) {
-          const uint64_t u64 = (static_cast<uint64_t>(w1[i]) << 32) | w0[i];
-          keep[e] = u64 <= A.keep_le;
-        }
-        if constexpr (XT == SDR_BF16) {
-          // unpack from the raw 16 B vector: even lane = low half of a word
-          uint32_t wd;
-          memcpy(&wd, &xv[e & ~1], 4);
-          const float xf = (e & 1) ? bf16_hi(wd) : bf16_lo(wd);
-          const float r = __fmul_rn(__fmul_rn(xf, keep[e] ? 1.0f : 0.0f), A.scale32);
-          nan[e] = r != r;
-          if constexpr (YT == SDR_F32) yv[e] = r;
-          else yv[e] = bf16_bits(r);
-        } else {
-          yv[e] = drop_apply<XT, YT>(A, xv[e], keep[e], nan[e]);
-        }
-        anynan |= nan[e];
-      }
-    }
-    if (anynan) {
-#pragma unroll
-      for (int e = 0; e < CH; ++e)
-        if (nan[e]) yv[e] = drop_nan_fix<XT, YT>(xv[e]);
-    }
-    store_chunk(y + q * CH, yv);
-    if constexpr (MT >= 0) {
-      using MTy = typename St<MT>::T;
-      if (A.mask != nullptr) {
-        MTy mv[CH];
-#pragma unroll
-        for (int e = 0; e < CH; ++e) mv[e] = one_or_zero<MT>(keep[e]);
-        store_chunk(static_cast<MTy*>(A.mask) + q * CH, mv);
-      }
-    }
-  }
-}
-
-// Ragged rows (inner extent not a multiple of the chunk): chunk q = (row, cq)
-// covers columns [CH cq, min(CH cq + CH, inner)) of its row.  Philox is
-// computed CH-wide on consecutive global indices (hoisted rounds 1-2), x / y /
-// mask move per element (row starts are not 16 B aligned).
-template <int XT, int YT, int MT>
-__global__ void __launch_bounds__(256) k_dropout_ragged(const __grid_constant__ DropArgs A) {
-  using XTy = typename St<XT>::T;
-  using YTy = typename St<YT>::T;
-  constexpr int CH = kDropCh;
-  const XTy* x = static_cast<const XTy*>(A.x);
-  YTy* y = static_cast<YTy*>(A.y);
-  const CanonView& cv = A.ix.cv;
-  const uint64_t inner = static_cast<uint64_t>(cv.inner);
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < A.nchunks;
-       q += stride) {
-    uint64_t row, cq;
-    A.div_cpr.divmod(q, row, cq);
-    uint64_t j0 = static_cast<uint64_t>(cv.base) + cq * CH, r = row;
-    for (int k = cv.nd - 1; k >= 1; --k) {
-      uint64_t qq, rem;
-      A.ix.div_o[k].divmod(r, qq, rem);
-      j0 += rem * static_cast<uint64_t>(cv.ostride[k]);
-      r = qq;
-    }
-    if (cv.nd >= 1) j0 += r * static_cast<uint64_t>(cv.ostride[0]);
-    const uint64_t lq = row * inner + cq * CH;
-    const int nvalid = static_cast<int>(min(static_cast<uint64_t>(CH), inner - cq * CH));
-    uint32_t w0[CH], w1[CH];
-    chunk_words<CH>(A.g, j0, w0, w1);
-#pragma unroll
-    for (int e = 0; e < CH; ++e) {
-      if (e < nvalid) {
-        const uint64_t i = lq + e;
-        const bool keep = ((static_cast<uint64_t>(w1[e]) << 32) | w0[e]) <= A.keep_le;
-        bool nan;
-        const XTy xe = x[i];
-        const YTy v = drop_apply<XT, YT>(A, xe, keep, nan);
-        y[i] = nan ? drop_nan_fix<XT, YT>(xe) : v;
-        if constexpr (MT >= 0) {
-          using MTy = typename St<MT>::T;
-          if (A.mask != nullptr) static_cast<MTy*>(A.mask)[i] = one_or_zero<MT>(keep);
-        }
-      }
-    }
-  }
-}
-
-template <int XT, int YT, int MT>
-__global__ void __launch_bounds__(256) k_dropout_generic(const __grid_constant__ DropArgs A) {
-  using XTy = typename St<XT>::T;
-  using YTy = typename St<YT>::T;
-  const XTy* x = static_cast<const XTy*>(A.x);
-  YTy* y = static_cast<YTy*>(A.y);
-  const uint64_t n = static_cast<uint64_t>(A.ix.cv.numel);
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += stride) {
-    uint32_t w0, w1;
-    elem_words(A.g, A.ix.global_of(i), w0, w1);
-    const uint64_t u64 = (static_cast<uint64_t>(w1) << 32) | w0;
-    const bool keep = u64 <= A.keep_le;
-    bool nan;
-    const YTy v = drop_apply<XT, YT>(A, x[i], keep, nan);
-    y[i] = nan ? drop_nan_fix<XT, YT>(x[i]) : v;
-    if constexpr (MT >= 0) {
-      using MTy = typename St<MT>::T;
-      if (A.mask != nullptr) static_cast<MTy*>(A.mask)[i] = one_or_zero<MT>(keep);
-    }
-  }
-}
-
 // Raw Philox words for (tau, beta) arrays (KAT / debug entry).
 __global__ void k_philox_blocks(const uint64_t* tau, const uint64_t* beta, int64_t n,
                                 const __grid_constant__ RoundKeys K, uint32_t* words) {
@@ -1407,32 +824,6 @@ int canonicalize(const sdr_view& v, CanonView& cv) {
     cv.ostride[i] = mst[i];
   }
   return SDR_OK;
-}
-
-static int device_sms() {
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms > 0 ? sms : 148;
-}
-
-// Persistent grid: one wave of resident CTAs (SMs x occupancy), or fewer
-// blocks when the work is small.  Grid-stride loops cover the rest.
-template <typename K>
-static int grid_for(K kernel, uint64_t work, int threads, size_t dyn_smem = 0) {
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, dyn_smem) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
-  const uint64_t cap = static_cast<uint64_t>(device_sms()) * per_sm;
-  const uint64_t blocks = (work + threads - 1) / threads;
-  return static_cast<int>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
-}
-
-static int launch_grid(uint64_t work, int threads) {
-  const uint64_t blocks = (work + threads - 1) / threads;
-  const uint64_t cap = static_cast<uint64_t>(device_sms()) * 8;
-  return static_cast<int>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
 }
 
 // Per-device Normal mirror tables.
@@ -1599,48 +990,6 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
   return SDR_OK;
 }
 
-// Every chunk start j0 = base + sum(digit*ostride) + c*ch is a multiple of ch
-// and THETA is a power of two >= ch: no chunk straddles a THETA boundary.
-static bool chunks_aligned(const CanonView& cv, uint64_t theta, int ch) {
-  if ((theta & (theta - 1)) != 0 || theta < static_cast<uint64_t>(ch)) return false;
-  if (cv.base % ch != 0) return false;
-  for (int k = 0; k < cv.nd; ++k)
-    if (cv.ostride[k] % ch != 0) return false;
-  return true;
-}
-
-static void setup_chunks(const CanonView& cv, bool fast, uint64_t& nchunks, uint64_t& cpr,
-                         FastDiv64& div_cpr, int ch = kV) {
-  if (fast) {
-    cpr = static_cast<uint64_t>(cv.inner) / ch;
-    nchunks = static_cast<uint64_t>(cv.numel) / ch;
-  } else {
-    cpr = 1;
-    nchunks = 0;
-  }
-  div_cpr = FastDiv64(cpr > 0 ? cpr : 1);
-}
-
-// 256-thread launch with programmatic stream serialization (PDL) when SDR_PDL.
-template <typename K, typename Args>
-static void launch_pdl(K kernel, int grid, cudaStream_t s, const Args& A, size_t dyn_smem = 0) {
-#if SDR_PDL
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = dyn_smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kernel, A);
-#else
-  kernel<<<grid, 256, dyn_smem, s>>>(A);
-#endif
-}
-
 // Dynamic shared memory of the fill kernels (the float32 Normal tables exceed
 // the 48 KiB static limit), with the opt-in attribute set before each launch.
 template <int DIST, int DT>
@@ -1706,7 +1055,6 @@ static int dispatch_fill_dt(int dt, const FillArgs& A, bool fast, cudaStream_t s
   return check_launch();
 }
 
-static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 int fill(void* out, int dt, const sdr_dist& dist, const sdr_rng& rng, const sdr_view& view,
          cudaStream_t s) {
@@ -1745,69 +1093,6 @@ int fill(void* out, int dt, const sdr_dist& dist, const sdr_rng& rng, const sdr_
     case SDR_BERNOULLI: return dispatch_fill_dt<SDR_BERNOULLI>(dt, A, fast, s);
     default: return SDR_E_DIST;
   }
-}
-
-template <int XT, int YT, int MT>
-static int launch_drop(const DropArgs& A, bool fast, cudaStream_t s) {
-  if (A.ragged)
-    k_dropout_ragged<XT, YT, MT><<<grid_for(k_dropout_ragged<XT, YT, MT>, A.nchunks, 256), 256, 0, s>>>(A);
-  else if (fast && A.aligned)
-    launch_pdl(k_dropout_fast<XT, YT, MT, true>, grid_for(k_dropout_fast<XT, YT, MT, true>, A.nchunks, 256), s, A);
-  else if (fast)
-    launch_pdl(k_dropout_fast<XT, YT, MT, false>, grid_for(k_dropout_fast<XT, YT, MT, false>, A.nchunks, 256), s, A);
-  else
-    k_dropout_generic<XT, YT, MT><<<grid_for(k_dropout_generic<XT, YT, MT>, A.ix.cv.numel, 256), 256, 0, s>>>(A);
-  return check_launch();
-}
-
-template <int XT, int YT>
-static int dispatch_drop_mask(int mt, const DropArgs& A, bool fast, cudaStream_t s) {
-  if (A.mask == nullptr) return launch_drop<XT, YT, -1>(A, fast, s);
-  if (mt == SDR_U8 || mt == SDR_BOOL) return launch_drop<XT, YT, SDR_U8>(A, fast, s);
-  if (mt == XT) return launch_drop<XT, YT, XT>(A, fast, s);
-  return SDR_E_DTYPE;
-}
-
-int dropout(const void* x, int xt, void* y, int yt, void* mask, int mt, double p,
-            const sdr_rng& rng, const sdr_view& view, cudaStream_t s) {
-  if (!(p >= 0.0 && p < 1.0)) return SDR_E_PARAM;
-  if (rng.theta < 1) return SDR_E_INVALID;
-  CanonView cv;
-  int st = canonicalize(view, cv);
-  if (st != SDR_OK) return st;
-  if (cv.numel == 0) return SDR_OK;
-  if (x == nullptr || y == nullptr) return SDR_E_INVALID;
-  DropArgs A;
-  memset(static_cast<void*>(&A), 0, sizeof(A));
-  A.g = make_gen(rng);
-  A.ix = make_indexer(cv);
-  A.x = x;
-  A.y = y;
-  A.mask = mask;
-  // keep-prob 1-p in float64 (rng.py:242), threshold ceil((1-p)*2^53).
-  const double pk = 1.0 - p;
-  const uint64_t T = static_cast<uint64_t>(ceil(pk * 9007199254740992.0));  // >= 1 as p < 1
-  A.keep_le = (T >= (uint64_t{1} << 53)) ? ~uint64_t{0} : (T << 11) - 1;
-  const double scale = 1.0 / (1.0 - p);
-  A.scale64 = scale;
-  A.scale32 = static_cast<float>(scale);
-  A.scale16 = __half_as_ushort(__double2half(scale));
-  bool fast = cv.istride == 1 && cv.inner % kDropCh == 0 && aligned16(x) && aligned16(y) &&
-              (mask == nullptr || (reinterpret_cast<uintptr_t>(mask) & 7u) == 0);
-  setup_chunks(cv, fast, A.nchunks, A.chunks_per_row, A.div_cpr, kDropCh);
-  A.aligned = fast && chunks_aligned(cv, rng.theta, kDropCh);
-  if (!fast && cv.istride == 1 && cv.inner >= kDropCh) {  // ragged rows: chunked Philox, per-element I/O
-    A.ragged = 1;
-    A.chunks_per_row = (static_cast<uint64_t>(cv.inner) + kDropCh - 1) / kDropCh;
-    A.nchunks = static_cast<uint64_t>(cv.numel / cv.inner) * A.chunks_per_row;
-    A.div_cpr = FastDiv64(A.chunks_per_row);
-  }
-  if (xt == SDR_F32 && yt == SDR_F32) return dispatch_drop_mask<SDR_F32, SDR_F32>(mt, A, fast, s);
-  if (xt == SDR_F64 && yt == SDR_F64) return dispatch_drop_mask<SDR_F64, SDR_F64>(mt, A, fast, s);
-  if (xt == SDR_BF16 && yt == SDR_BF16) return dispatch_drop_mask<SDR_BF16, SDR_BF16>(mt, A, fast, s);
-  if (xt == SDR_BF16 && yt == SDR_F32) return dispatch_drop_mask<SDR_BF16, SDR_F32>(mt, A, fast, s);
-  if (xt == SDR_F16 && yt == SDR_F16) return dispatch_drop_mask<SDR_F16, SDR_F16>(mt, A, fast, s);
-  return SDR_E_DTYPE;
 }
 
 int philox_blocks(const uint64_t* tau, const uint64_t* beta, int64_t n, uint64_t seed,
