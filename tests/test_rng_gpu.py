@@ -323,3 +323,35 @@ def test_normal_fast_paths_equal_exact_path(dt, mean, std, monkeypatch):
         if path == "exact":
             assert R.normal_fallback_count() - before == 1500 * 1400
     assert torch.equal(outs["exact"], outs["f64"]) and torch.equal(outs["exact"], outs[None])
+
+
+def test_randomized_windows_match_oracle():
+    """150 seeded random (shape, placement, mesh, distribution, dtype, THETA)
+    cases -- odd extents, ragged rows, empty and uneven shards, 1-3 mesh dims --
+    every coordinate's shard against the oracle."""
+    rs = np.random.default_rng(20241017)
+    kinds = [("uniform01", (), "float32"), ("uniform", (-2.0, 3.0), "bfloat16"), ("normal", (0.5, 2.0), "float32"),
+             ("normal", (0.0, 0.02), "bfloat16"), ("bernoulli", (0.3,), "uint8"), ("randint", (-5, 17), "int64"),
+             ("normal", (1.0, 0.1), "float16"), ("uniform", (-1.0, 1.0), "float64")]
+    for case in range(150):
+        nd = int(rs.integers(1, 4))
+        shape = tuple(int(rs.integers(1, 70 if nd > 1 else 3000)) for _ in range(nd))
+        mdims = int(rs.integers(1, 3))
+        msizes = tuple(int(rs.integers(1, 5)) for _ in range(mdims))
+        used, pls = set(), []
+        for _ in range(mdims):
+            d = int(rs.integers(0, nd))
+            if d in used or rs.random() < 0.3:
+                pls.append("R")
+            else:
+                used.add(d)
+                pls.append(f"S({d})")
+        kind, params, dt = kinds[case % len(kinds)]
+        theta = [65536, 64, 7, 1][case % 4]
+        mesh = S.create_mesh([(f"m{i}", s) for i, s in enumerate(msizes)])
+        spec = ShardSpec(mesh, parse_placements(",".join(pls)))
+        seed, off = 1000 + case, int(rs.integers(0, 1 << 20))
+        locs = R.generate_distributed(spec, shape, R.RngState(seed, off, theta), _dist(kind, params), _np_dt(dt))
+        ref = O.fill_sharded(shape, _oracle_pl(spec), msizes, seed, off, theta, kind, params, _np_dt(dt))
+        for coord, t in locs.items():
+            assert _same(t, _oracle_tensor(ref[coord])), (case, shape, pls, msizes, kind, dt, theta, coord)
