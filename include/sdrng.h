@@ -165,6 +165,54 @@ int32_t sdr_pack_local(const sdr_pack_member* members, int32_t n, void* segment,
 int32_t sdr_unpack_local(const sdr_pack_member* members, int32_t n, const void* segment,
                          void* stream);
 
+/* ---- peer-memory collectives over NVLink / NVSwitch (CUDA IPC) ----------
+ *
+ * The fused redistribute without NCCL: every rank of a fiber owns a "peer
+ * heap" (flag words + two data halves) that all fiber ranks map through CUDA
+ * IPC.  A coalesced collective is then pack (local) -> sdr_peer_barrier ->
+ * one pull kernel that reads every peer's half over NVLink and writes the
+ * destination tensors directly:
+ *   S->R  sdr_unpack_gathered_peers   (comm.py:104-110 + _assemble_shards,
+ *                                      dtensor.py:261-283)
+ *   P->S  sdr_reduce_scatter_peers    (comm.py:113-125 + _local_slice,
+ *                                      dtensor.py:286-298)
+ * The reduction sums in ascending fiber-rank order with one rounding per add,
+ * in the tensor dtype, exactly like the reference's `acc += b` loop
+ * (comm.py:120-122), including x86 NaN propagation: results are bit-exact for
+ * any data, unlike a ring reduce-scatter.  Consecutive calls alternate the
+ * two halves, so one barrier per call suffices (a rank reaches barrier k+1
+ * only after its pull of call k).  Flags hold SDR_MAX_PEERS uint64 slots at
+ * the heap base; slot q = the last epoch peer q arrived at. */
+#define SDR_MAX_PEERS 64
+#define SDR_PEER_FLAG_BYTES 4096
+
+typedef struct { unsigned char bytes[64]; } sdr_ipc_handle;  /* cudaIpcMemHandle_t */
+
+/* cudaMalloc `bytes` on `device` (flags zeroed) and export its IPC handle. */
+int32_t sdr_peer_heap_alloc(int32_t device, int64_t bytes, void** base, sdr_ipc_handle* handle);
+/* Map a peer's heap (another process) into this process on `device`. */
+int32_t sdr_peer_heap_open(int32_t device, const sdr_ipc_handle* handle, void** base);
+int32_t sdr_peer_heap_close(void* base);  /* unmap a peer heap */
+int32_t sdr_peer_heap_free(void* base);   /* free this process's own heap */
+/* Device-side barrier of `nranks` fiber ranks: stores `epoch` (release, system
+ * scope) into slot `rank` of every rank's flags, then waits (acquire) until
+ * every slot of flags[rank] >= epoch.  flags: host array of nranks device
+ * pointers (each rank's heap base).  A wait longer than timeout_ns traps (the
+ * call fails loudly instead of hanging). */
+int32_t sdr_peer_barrier(void* const* flags, int32_t rank, int32_t nranks, uint64_t epoch,
+                         int64_t timeout_ns, void* stream);
+/* S->R pull: segment r of the gathered layout (sdr_unpack_gathered) is read
+ * from segs[r] (rank r's packed shard, usually in its peer heap). */
+int32_t sdr_unpack_gathered_peers(const sdr_pack_member* members, int32_t n,
+                                  const void* const* segs, int32_t nranks, void* stream);
+/* P->S pull: members are this rank's OUTPUT pieces (rows = this rank's rows,
+ * as sdr_unpack_local); packed[q] is rank q's rank-major packed buffer
+ * (sdr_pack_scatter).  out = sum over q ascending of packed[q] segment `rank`,
+ * in `dtype` (SDR_F32/F64/BF16/F16/I32/I64). */
+int32_t sdr_reduce_scatter_peers(const sdr_pack_member* members, int32_t n,
+                                 const void* const* packed, int64_t seg_bytes, int32_t nranks,
+                                 int32_t rank, int32_t dtype, void* stream);
+
 /* INT32 pipe microbenchmark: measured IMAD.WIDE.U32 and LOP3 throughput
  * (ops/s) on `device`, for the roofline denominator. */
 int32_t sdr_probe_int32(int32_t device, double* imad_wide_per_s, double* lop3_per_s,

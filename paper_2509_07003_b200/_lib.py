@@ -57,6 +57,14 @@ class SdrPackMember(C.Structure):
     ]
 
 
+MAX_PEERS = 64
+PEER_FLAG_BYTES = 4096
+
+
+class SdrIpcHandle(C.Structure):
+    _fields_ = [("bytes", C.c_ubyte * 64)]
+
+
 class NativeLibraryMissing(ImportError):
     pass
 
@@ -92,6 +100,17 @@ def _load():
         "sdr_pack_local": (C.c_int32, [P(SdrPackMember), C.c_int32, C.c_void_p, C.c_void_p]),
         "sdr_unpack_local": (C.c_int32, [P(SdrPackMember), C.c_int32, C.c_void_p, C.c_void_p]),
         "sdr_probe_int32": (C.c_int32, [C.c_int32, P(C.c_double), P(C.c_double), P(C.c_double)]),
+        "sdr_peer_heap_alloc": (C.c_int32, [C.c_int32, C.c_int64, P(C.c_void_p), P(SdrIpcHandle)]),
+        "sdr_peer_heap_open": (C.c_int32, [C.c_int32, P(SdrIpcHandle), P(C.c_void_p)]),
+        "sdr_peer_heap_close": (C.c_int32, [C.c_void_p]),
+        "sdr_peer_heap_free": (C.c_int32, [C.c_void_p]),
+        "sdr_peer_barrier": (C.c_int32, [P(C.c_void_p), C.c_int32, C.c_int32, C.c_uint64, C.c_int64,
+                                         C.c_void_p]),
+        "sdr_unpack_gathered_peers": (C.c_int32, [P(SdrPackMember), C.c_int32, P(C.c_void_p),
+                                                  C.c_int32, C.c_void_p]),
+        "sdr_reduce_scatter_peers": (C.c_int32, [P(SdrPackMember), C.c_int32, P(C.c_void_p),
+                                                 C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                                 C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -107,6 +126,8 @@ EXPORTED = (
     "sdr_philox_blocks", "sdr_fill", "sdr_fill_batch", "sdr_dropout", "sdr_normal_tables_load",
     "sdr_normal_tables_loaded", "sdr_normal_fallback_count", "sdr_unpack_gathered",
     "sdr_pack_scatter", "sdr_pack_local", "sdr_unpack_local", "sdr_probe_int32",
+    "sdr_peer_heap_alloc", "sdr_peer_heap_open", "sdr_peer_heap_close", "sdr_peer_heap_free",
+    "sdr_peer_barrier", "sdr_unpack_gathered_peers", "sdr_reduce_scatter_peers",
 )
 
 

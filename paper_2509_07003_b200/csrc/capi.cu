@@ -22,6 +22,16 @@ int pack_scatter(const sdr_pack_member* m, int n, void* packed, int64_t seg_byte
                  cudaStream_t s);
 int pack_local(const sdr_pack_member* m, int n, void* seg, cudaStream_t s);
 int unpack_local(const sdr_pack_member* m, int n, const void* seg, cudaStream_t s);
+int unpack_gathered_peers(const sdr_pack_member* m, int n, const void* const* segs, int nranks,
+                          cudaStream_t s);
+int reduce_scatter_peers(const sdr_pack_member* m, int n, const void* const* packed,
+                         int64_t seg_bytes, int nranks, int rank, int dtype, cudaStream_t s);
+int peer_barrier(void* const* flags, int rank, int nranks, uint64_t epoch, int64_t timeout_ns,
+                 cudaStream_t s);
+int peer_heap_alloc(int device, int64_t bytes, void** base, sdr_ipc_handle* handle);
+int peer_heap_open(int device, const sdr_ipc_handle* handle, void** base);
+int peer_heap_close(void* base);
+int peer_heap_free(void* base);
 }  // namespace sdr
 
 static cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
@@ -103,6 +113,35 @@ int32_t sdr_pack_local(const sdr_pack_member* members, int32_t n, void* segment,
 int32_t sdr_unpack_local(const sdr_pack_member* members, int32_t n, const void* segment,
                          void* stream) {
   return sdr::unpack_local(members, n, segment, as_stream(stream));
+}
+
+int32_t sdr_peer_heap_alloc(int32_t device, int64_t bytes, void** base, sdr_ipc_handle* handle) {
+  return sdr::peer_heap_alloc(device, bytes, base, handle);
+}
+
+int32_t sdr_peer_heap_open(int32_t device, const sdr_ipc_handle* handle, void** base) {
+  return sdr::peer_heap_open(device, handle, base);
+}
+
+int32_t sdr_peer_heap_close(void* base) { return sdr::peer_heap_close(base); }
+
+int32_t sdr_peer_heap_free(void* base) { return sdr::peer_heap_free(base); }
+
+int32_t sdr_peer_barrier(void* const* flags, int32_t rank, int32_t nranks, uint64_t epoch,
+                         int64_t timeout_ns, void* stream) {
+  return sdr::peer_barrier(flags, rank, nranks, epoch, timeout_ns, as_stream(stream));
+}
+
+int32_t sdr_unpack_gathered_peers(const sdr_pack_member* members, int32_t n,
+                                  const void* const* segs, int32_t nranks, void* stream) {
+  return sdr::unpack_gathered_peers(members, n, segs, nranks, as_stream(stream));
+}
+
+int32_t sdr_reduce_scatter_peers(const sdr_pack_member* members, int32_t n,
+                                 const void* const* packed, int64_t seg_bytes, int32_t nranks,
+                                 int32_t rank, int32_t dtype, void* stream) {
+  return sdr::reduce_scatter_peers(members, n, packed, seg_bytes, nranks, rank, dtype,
+                                   as_stream(stream));
 }
 
 int32_t sdr_probe_int32(int32_t device, double* imad_wide_per_s, double* lop3_per_s,

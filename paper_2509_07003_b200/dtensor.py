@@ -30,7 +30,7 @@ from dataclasses import dataclass, replace
 
 import torch
 
-from . import comm
+from . import comm, peer
 from .mesh import DeviceMesh
 from .movers import DEFAULT_MOVER, Member, layout
 from .placement import (
@@ -375,6 +375,12 @@ def _fused_gather(mesh, md, items, ledger, mover):
         send_members.append(Member(loc, o, rows_local, inner, chunk))
         recv_members.append(Member(full, o, rows_full, inner, chunk))
         outs.append(full)
+    dev = items[0][1][1].device
+    if _peer_gather(group, fiber, dev, send_members, recv_members, ledger, mesh, md, P):
+        for (x, slot), full in zip(items, outs):
+            slot[0] = slot[0].with_placement(md, Replicate())
+            slot[1] = full
+        return
     if len(items) == 1 and recv_members[0].outer <= 1 and recv_members[0].rows == P * recv_members[0].chunk:
         # zero-copy: the shard IS the rank segment and the output IS the
         # rank-major gathered buffer (outer == 1, even split)
@@ -384,7 +390,6 @@ def _fused_gather(mesh, md, items, ledger, mover):
         slot[0] = slot[0].with_placement(md, Replicate())
         slot[1] = outs[0]
         return
-    dev = items[0][1][1].device
     pipe = _Pipeline(dev)
     # bucket by the PADDED rank-segment bytes: identical on every rank of the
     # fiber (local shard sizes differ for uneven splits), so all ranks issue the
@@ -428,6 +433,12 @@ def _fused_reduce_scatter(mesh, md, items, ledger, mover):
         full_members.append(Member(loc, o, rows_full, inner, chunk))
         piece_members.append(Member(out, o, rows_mine, inner, chunk))
         outs.append(out)
+    if _peer_reduce_scatter(group, fiber, items[0][1][1], full_members, piece_members, ledger, mesh,
+                            md, P):
+        for (x, slot, dst_p), out in zip(items, outs):
+            slot[0] = slot[0].with_placement(md, dst_p)
+            slot[1] = out
+        return
     if len(items) == 1 and full_members[0].outer <= 1 and full_members[0].rows == P * full_members[0].chunk:
         # zero-copy: the full local tensor is already rank-major
         inp = items[0][1][1].contiguous()
@@ -457,6 +468,56 @@ def _fused_reduce_scatter(mesh, md, items, ledger, mover):
     for (x, slot, dst_p), out in zip(items, outs):
         slot[0] = slot[0].with_placement(md, dst_p)
         slot[1] = out
+
+
+def _padded_bytes(members) -> list[int]:
+    return [m.outer * m.chunk * m.inner * m.tensor.element_size() for m in members]
+
+
+def _peer_gather(group, fiber, dev, send_members, recv_members, ledger, mesh, md, P) -> bool:
+    """S->R over the peer-memory transport (peer.py): per bucket one pack, one
+    barrier and one pull kernel that writes the full tensors.  False when the
+    transport is off / impossible or a member exceeds the heap half (the same
+    answer on every fiber rank: sizes are the padded segment bytes)."""
+    hp = peer.heap_for(group, fiber, dev)
+    if hp is None:
+        return False
+    sizes = _padded_bytes(send_members)
+    if max(sizes, default=0) > hp.half:
+        return False
+    for idx in _buckets(sizes, cap=hp.half):
+        sm, rm = [send_members[i] for i in idx], [recv_members[i] for i in idx]
+        seg = layout(sm)
+        for a, b in zip(sm, rm):
+            b.seg_off = a.seg_off
+        hp.all_gather(sm, rm, seg)
+        if ledger is not None:
+            ledger.record("all_gather", seg * P, P, mesh.name, mesh.dim_names[md])
+    return True
+
+
+def _peer_reduce_scatter(group, fiber, t, full_members, piece_members, ledger, mesh, md, P) -> bool:
+    """P->S over the peer-memory transport: the pull kernel sums the fiber's
+    segments in ascending rank order (bit-exact vs comm.py:113-125) straight
+    into the output pieces."""
+    if not peer.reducible(t.dtype):
+        return False
+    hp = peer.heap_for(group, fiber, t.device)
+    if hp is None:
+        return False
+    sizes = _padded_bytes(full_members)
+    cap = hp.half // P // 256 * 256
+    if max(sizes, default=0) > cap:
+        return False
+    for idx in _buckets(sizes, cap=cap):
+        fm, pm = [full_members[i] for i in idx], [piece_members[i] for i in idx]
+        seg = layout(fm, align=16)
+        for f, q in zip(fm, pm):
+            q.seg_off = f.seg_off
+        hp.reduce_scatter(fm, pm, seg, t.dtype)
+        if ledger is not None:
+            ledger.record("reduce_scatter", seg * P, P, mesh.name, mesh.dim_names[md])
+    return True
 
 
 def _piece_shape(shp, dst_p, E, P, k):

@@ -1,0 +1,175 @@
+"""Peer-memory transport for the coalesced redistribute collectives.
+
+On an NVLink / NVSwitch node every rank of a fiber can load from every other
+rank's HBM.  A `PeerHeap` is one CUDA-IPC-exported allocation per rank and
+fiber (flag words + two data halves) mapped by all fiber ranks.  A coalesced
+collective then runs as three launches on the current stream, with no NCCL
+call and no host synchronisation:
+
+    pack my members into my half h   (sdr_pack_local / sdr_pack_scatter)
+    sdr_peer_barrier(epoch)          (release my flag, acquire everyone's)
+    ONE pull kernel                  (sdr_unpack_gathered_peers: S->R, or
+                                      sdr_reduce_scatter_peers: P->S)
+
+The pull reads the peers' halves over NVLink and writes the destination
+tensors directly, so the unpack pass of the NCCL path disappears and the
+reduce-scatter sums in ascending fiber-rank order -- the reference's
+`acc += b` loop (comm.py:113-125), bit for bit for every dtype.  Calls
+alternate halves, so one barrier per call is enough (include/sdrng.h).
+
+Selection (`transport()`): SDR_TRANSPORT=peer|nccl|auto (default auto = peer
+when every fiber rank is on this host and its device can reach ours; the
+decision is agreed by all fiber ranks).  SDR_PEER_HEAP_MB sizes the heap
+(default 256: two 128 MiB halves); buckets larger than a half go to NCCL.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import socket
+
+import torch
+
+from . import _lib
+
+_HEAPS: dict = {}
+_TIMEOUT_NS = int(float(os.environ.get("SDR_PEER_TIMEOUT_S", "30")) * 1e9)
+
+
+def transport() -> str:
+    t = os.environ.get("SDR_TRANSPORT", "auto")
+    if t not in ("auto", "peer", "nccl"):
+        raise ValueError(f"SDR_TRANSPORT must be auto, peer or nccl, not {t!r}")
+    return t
+
+
+def _stream(dev):
+    return _lib.stream_handle(dev)
+
+
+class PeerHeap:
+    """This rank's heap plus the mapped heaps of its fiber peers.  Created
+    collectively (every fiber rank, same order) on first use of a fiber."""
+
+    def __init__(self, group, fiber: list, dev: torch.device, half_bytes: int):
+        import torch.distributed as dist
+        self.dev = dev
+        self.fiber = list(fiber)
+        self.P = len(fiber)
+        self.rank = fiber.index(dist.get_rank())
+        self.half = int(half_bytes) // 256 * 256
+        self.epoch = 0
+        self.calls = 0
+        self.ok = False
+        self.bases: list = [None] * self.P
+        total = _lib.PEER_FLAG_BYTES + 2 * self.half
+        base, h = C.c_void_p(), _lib.SdrIpcHandle()
+        with torch.cuda.device(dev):
+            st = _lib.LIB.sdr_peer_heap_alloc(dev.index, total, C.byref(base), C.byref(h))
+        _lib.check(st, "sdr_peer_heap_alloc")
+        self.own = base.value
+        me = (socket.gethostname(), dev.index, bytes(h.bytes))
+        infos = [None] * self.P
+        dist.all_gather_object(infos, me, group=group)
+        reach = all(host == me[0] and (d == dev.index or torch.cuda.can_device_access_peer(dev.index, d))
+                    for host, d, _ in infos)
+        opened = []
+        if reach:
+            for q, (_, _, hb) in enumerate(infos):
+                if q == self.rank:
+                    self.bases[q] = self.own
+                    continue
+                hq = _lib.SdrIpcHandle()
+                C.memmove(hq.bytes, hb, 64)
+                p = C.c_void_p()
+                with torch.cuda.device(dev):
+                    st = _lib.LIB.sdr_peer_heap_open(dev.index, C.byref(hq), C.byref(p))
+                if st != _lib.OK:
+                    reach = False
+                    break
+                self.bases[q] = p.value
+                opened.append(p.value)
+        votes = [None] * self.P
+        dist.all_gather_object(votes, bool(reach), group=group)
+        self.ok = all(votes)
+        if not self.ok:
+            for p in opened:
+                _lib.LIB.sdr_peer_heap_close(p)
+            self.bases = [None] * self.P
+        self._flags = (C.c_void_p * self.P)(*self.bases) if self.ok else None
+
+    def _half_ptrs(self, h: int):
+        off = _lib.PEER_FLAG_BYTES + h * self.half
+        return (C.c_void_p * self.P)(*[b + off for b in self.bases])
+
+    def _barrier(self):
+        self.epoch += 1
+        st = _lib.LIB.sdr_peer_barrier(self._flags, self.rank, self.P, self.epoch, _TIMEOUT_NS,
+                                       _stream(self.dev))
+        _lib.check(st, "sdr_peer_barrier")
+
+    def _next_half(self) -> int:
+        h = self.calls & 1
+        self.calls += 1
+        return h
+
+    def all_gather(self, send_members, recv_members, seg_bytes: int):
+        """S->R: pack my shards into my half, barrier, pull every rank's
+        segment straight into the full member tensors."""
+        from .movers import CudaMover
+        if seg_bytes > self.half:
+            raise ValueError("bucket larger than the peer heap half")
+        h = self._next_half()
+        segs = self._half_ptrs(h)
+        arr = CudaMover._arr(send_members)
+        with torch.cuda.device(self.dev):
+            st = _lib.LIB.sdr_pack_local(arr, len(send_members), segs[self.rank], _stream(self.dev))
+            _lib.check(st, "sdr_pack_local")
+            self._barrier()
+            arr = CudaMover._arr(recv_members)
+            st = _lib.LIB.sdr_unpack_gathered_peers(arr, len(recv_members), segs, self.P,
+                                                    _stream(self.dev))
+        _lib.check(st, "sdr_unpack_gathered_peers")
+
+    def reduce_scatter(self, full_members, piece_members, seg_bytes: int, dtype: torch.dtype):
+        """P->S: pack my Partial tensors rank-major into my half, barrier, sum
+        my segment over every rank (ascending) straight into my pieces."""
+        from .movers import CudaMover
+        if seg_bytes * self.P > self.half:
+            raise ValueError("bucket larger than the peer heap half")
+        h = self._next_half()
+        bufs = self._half_ptrs(h)
+        arr = CudaMover._arr(full_members)
+        with torch.cuda.device(self.dev):
+            st = _lib.LIB.sdr_pack_scatter(arr, len(full_members), bufs[self.rank], seg_bytes, self.P,
+                                           _stream(self.dev))
+            _lib.check(st, "sdr_pack_scatter")
+            self._barrier()
+            arr = CudaMover._arr(piece_members)
+            st = _lib.LIB.sdr_reduce_scatter_peers(arr, len(piece_members), bufs, seg_bytes, self.P,
+                                                   self.rank, _SDR_DTYPE[dtype], _stream(self.dev))
+        _lib.check(st, "sdr_reduce_scatter_peers")
+
+
+_SDR_DTYPE = {torch.float32: _lib.F32, torch.float64: _lib.F64, torch.bfloat16: _lib.BF16,
+              torch.float16: _lib.F16, torch.int32: _lib.I32, torch.int64: _lib.I64}
+
+
+def reducible(dtype: torch.dtype) -> bool:
+    return dtype in _SDR_DTYPE
+
+
+def heap_for(group, fiber, dev: torch.device):
+    """The fiber's PeerHeap, or None when the peer transport is off or not
+    possible (then the caller uses NCCL).  Collective on first call."""
+    if group is None or dev.type != "cuda" or transport() == "nccl" or len(fiber) > _lib.MAX_PEERS:
+        return None
+    key = (tuple(fiber), dev.index)
+    hp = _HEAPS.get(key)
+    if hp is None:
+        half = int(float(os.environ.get("SDR_PEER_HEAP_MB", "256")) * (1 << 20)) // 2
+        hp = _HEAPS[key] = PeerHeap(group, fiber, dev, half)
+        if not hp.ok and transport() == "peer":
+            raise RuntimeError(f"SDR_TRANSPORT=peer but fiber {fiber} cannot map peer memory")
+    return hp if hp.ok else None

@@ -101,13 +101,14 @@ def test_redistribute_many_bucketed_pipeline_golden():
     _spawn(_worker_golden, 8, (2, 4), 1)
 
 
-def _worker_fused_grads(rank, ws, cuda=False):
+def _worker_fused_grads(rank, ws, cuda=False, transport="auto"):
     from cpu_mover import TorchCpuMover
     from paper_2509_07003_b200 import comm, create_mesh
     from paper_2509_07003_b200.dtensor import from_local
     from paper_2509_07003_b200.placement import ShardSpec, parse_placements
     if cuda:  # CUDA pack/unpack kernels, host-staged gloo collectives (see _worker_golden_cuda)
         os.environ["SDR_COMM_CPU_STAGING"] = "1"
+        os.environ["SDR_TRANSPORT"] = transport
         torch.cuda.set_device(0)
         from paper_2509_07003_b200.movers import CudaMover
         mover = CudaMover()
@@ -177,12 +178,15 @@ def test_redistribute_many_mixed_dtypes_gloo():
     _spawn(_worker_many_mixed, 3)
 
 
-def _worker_golden_cuda(rank, ws, mesh_sizes, bucket_bytes=None):
+def _worker_golden_cuda(rank, ws, mesh_sizes, bucket_bytes=None, transport="nccl"):
     """The same golden cases with device tensors and the CUDA pack/unpack
     kernels; every process shares cuda:0 and gloo carries the (host-staged)
     collectives (SDR_COMM_CPU_STAGING=1).  bucket_bytes forces the pipelined
-    multi-bucket path (pack / side-stream collective / unpack)."""
+    multi-bucket path (pack / side-stream collective / unpack).  transport
+    "peer" maps the ranks' peer heaps through CUDA IPC (same device here) and
+    runs the pack / barrier / pull kernels instead of the collectives."""
     os.environ["SDR_COMM_CPU_STAGING"] = "1"
+    os.environ["SDR_TRANSPORT"] = transport
     torch.cuda.set_device(0)
     from paper_2509_07003_b200 import dtensor as DT
     if bucket_bytes is not None:
@@ -216,14 +220,78 @@ def _worker_golden_cuda(rank, ws, mesh_sizes, bucket_bytes=None):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mesh_sizes,bucket", [((4,), None), ((2, 4), None), ((4,), 64), ((2, 4), 1)])
-def test_redistribute_golden_cuda_movers_multiprocess(mesh_sizes, bucket):
-    _spawn(_worker_golden_cuda, int(np.prod(mesh_sizes)), mesh_sizes, bucket)
+@pytest.mark.parametrize("mesh_sizes,bucket,transport", [
+    ((4,), None, "nccl"), ((2, 4), None, "nccl"), ((4,), 64, "nccl"), ((2, 4), 1, "nccl"),
+    ((4,), None, "peer"), ((2, 4), None, "peer"), ((2, 4), 1, "peer")])
+def test_redistribute_golden_cuda_movers_multiprocess(mesh_sizes, bucket, transport):
+    _spawn(_worker_golden_cuda, int(np.prod(mesh_sizes)), mesh_sizes, bucket, transport)
 
 
 @pytest.mark.gpu
-def test_bucketed_and_fused_grad_reduce_cuda_movers_multiprocess():
-    _spawn(_worker_fused_grads, 4, True)
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_bucketed_and_fused_grad_reduce_cuda_movers_multiprocess(transport):
+    _spawn(_worker_fused_grads, 4, True, transport)
+
+
+def _peer_rs_inputs(q, shapes, np_dtype):
+    """Rank q's Partial tensors: random non-integer values with NaN / inf
+    planted at rank-specific spots (exercise the x86 NaN rules)."""
+    rs = np.random.default_rng(1000 + q)
+    outs = []
+    for i, shp in enumerate(shapes):
+        a = (rs.standard_normal(shp) * (10.0 ** rs.integers(-3, 4, shp))).astype(np.float32)
+        flat = a.reshape(-1)
+        if flat.size > 8:
+            flat[(3 * q + i) % flat.size] = np.nan if q % 2 else -np.nan
+            flat[(5 * q + 2 * i + 1) % flat.size] = np.inf if q % 3 else -np.inf
+        outs.append(a.astype(np_dtype))
+    return outs
+
+
+def _worker_peer_reduce_scatter(rank, ws, dtype_name):
+    """P -> S through the peer pull kernel on non-integer data: bit-exact vs
+    the reference's reduction (NumPy / ml_dtypes `acc += b` in ascending rank
+    order, comm.py:113-125), NaN and inf included."""
+    os.environ["SDR_COMM_CPU_STAGING"] = "1"
+    os.environ["SDR_TRANSPORT"] = "peer"
+    torch.cuda.set_device(0)
+    import ml_dtypes
+    from paper_2509_07003_b200 import comm, create_mesh
+    from paper_2509_07003_b200.dtensor import from_local, redistribute_many
+    from paper_2509_07003_b200.placement import ShardSpec, parse_placements
+    np_dt = {"float32": np.float32, "float16": np.float16, "bfloat16": ml_dtypes.bfloat16,
+             "float64": np.float64}[dtype_name]
+    t_dt = getattr(torch, dtype_name)
+    mesh = create_mesh([("dp", ws)])
+    coord = mesh.coords_of_rank(rank)
+    shapes = [(13, 37), (8, 5, 6), (3,), (ws * 64, 128)]
+    dsts = ["S(0)", "S(1)", "S(0)", "S(0)"]
+    ins = [_peer_rs_inputs(q, shapes, np_dt) for q in range(ws)]
+    src = ShardSpec(mesh, parse_placements("P"))
+    xs = [from_local(torch.from_numpy(ins[rank][i].view(np.uint8).copy()).view(t_dt).reshape(shp).cuda(),
+                     src, shp, coord) for i, shp in enumerate(shapes)]
+    specs = [ShardSpec(mesh, parse_placements(d)) for d in dsts]
+    ledger = comm.CollectiveLedger()
+    ys = redistribute_many(xs, specs, ledger)
+    assert ledger.count("reduce_scatter") == 1
+    for i, (y, d) in enumerate(zip(ys, dsts)):
+        acc = ins[0][i].copy()
+        with np.errstate(all="ignore"):
+            for q in range(1, ws):
+                acc += ins[q][i]
+        dim = int(d[2])
+        E = shapes[i][dim]
+        c = -(-E // ws)
+        lo, hi = min(E, rank * c), min(E, rank * c + c)
+        want = np.ascontiguousarray(np.take(acc, np.arange(lo, hi), axis=dim))
+        got = y.local.cpu().contiguous().view(torch.uint8).numpy().tobytes()
+        assert got == want.view(np.uint8).tobytes(), (dtype_name, i, rank)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype_name", ["float32", "bfloat16", "float16", "float64"])
+def test_peer_reduce_scatter_bit_exact_nonint(dtype_name):
+    _spawn(_worker_peer_reduce_scatter, 3, dtype_name)
 
 
 
