@@ -34,6 +34,7 @@ import torch
 from . import _lib
 
 _HEAPS: dict = {}
+STATS = {"all_gather": 0, "reduce_scatter": 0}  # pull launches of this process
 _TIMEOUT_NS = int(float(os.environ.get("SDR_PEER_TIMEOUT_S", "30")) * 1e9)
 
 
@@ -131,6 +132,7 @@ class PeerHeap:
             st = _lib.LIB.sdr_unpack_gathered_peers(arr, len(recv_members), segs, self.P,
                                                     _stream(self.dev))
         _lib.check(st, "sdr_unpack_gathered_peers")
+        STATS["all_gather"] += 1
 
     def reduce_scatter(self, full_members, piece_members, seg_bytes: int, dtype: torch.dtype):
         """P->S: pack my Partial tensors rank-major into my half, barrier, sum
@@ -150,6 +152,7 @@ class PeerHeap:
             st = _lib.LIB.sdr_reduce_scatter_peers(arr, len(piece_members), bufs, seg_bytes, self.P,
                                                    self.rank, _SDR_DTYPE[dtype], _stream(self.dev))
         _lib.check(st, "sdr_reduce_scatter_peers")
+        STATS["reduce_scatter"] += 1
 
 
 _SDR_DTYPE = {torch.float32: _lib.F32, torch.float64: _lib.F64, torch.bfloat16: _lib.BF16,

@@ -217,6 +217,8 @@ def _worker_golden_cuda(rank, ws, mesh_sizes, bucket_bytes=None, transport="nccl
     ys = redistribute_many(xs, dsts, comm.CollectiveLedger(), mover=mover)
     for y, want, c in zip(ys, wants, cases):
         assert y.local.cpu().numpy().tobytes() == np.ascontiguousarray(want).tobytes(), ("many", c)
+    from paper_2509_07003_b200 import peer
+    assert (peer.STATS["all_gather"] > 0) == (transport == "peer")
 
 
 @pytest.mark.gpu
@@ -244,6 +246,8 @@ def _peer_rs_inputs(q, shapes, np_dtype):
         if flat.size > 8:
             flat[(3 * q + i) % flat.size] = np.nan if q % 2 else -np.nan
             flat[(5 * q + 2 * i + 1) % flat.size] = np.inf if q % 3 else -np.inf
+            flat[(7 * q + i + 2) % flat.size] = 1e-39 * (q + 1)  # f32 / bf16 subnormal
+            flat[(11 * q + i + 4) % flat.size] = -3e-6 * (q + 1)  # f16 subnormal
         outs.append(a.astype(np_dtype))
     return outs
 
@@ -274,6 +278,8 @@ def _worker_peer_reduce_scatter(rank, ws, dtype_name):
     ledger = comm.CollectiveLedger()
     ys = redistribute_many(xs, specs, ledger)
     assert ledger.count("reduce_scatter") == 1
+    from paper_2509_07003_b200 import peer
+    assert peer.STATS["reduce_scatter"] == 1
     for i, (y, d) in enumerate(zip(ys, dsts)):
         acc = ins[0][i].copy()
         with np.errstate(all="ignore"):
