@@ -541,9 +541,20 @@ def _fused_all_reduce(mesh, dims, items, ledger, mover):
         for _, slot in items:
             slot[1] = slot[1].clone()
         return
-    group, _ = comm.fiber_group(mesh, tuple(dims))
+    group, fiber = comm.fiber_group(mesh, tuple(dims))
     members = [Member(slot[1].contiguous(), 1, 1, slot[1].numel(), 1) for _, slot in items]
     seg = layout(members, align=16)
+    t0 = items[0][1][1]
+    hp = peer.heap_for(group, fiber, t0.device) if peer.reducible(t0.dtype) else None
+    if hp is not None:
+        outs = [torch.empty_like(m.tensor) for m in members]
+        if hp.all_reduce([m.tensor for m in members], outs):
+            if ledger is not None:
+                ledger.record("all_reduce", seg, P, mesh.name,
+                              "+".join(mesh.dim_names[d] for d in dims))
+            for (_, slot), o in zip(items, outs):
+                slot[1] = o
+            return
     dt = items[0][1][1].dtype
     es = items[0][1][1].element_size()
     buf = torch.empty(seg // es, dtype=dt, device=items[0][1][1].device)  # gaps never read

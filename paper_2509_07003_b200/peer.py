@@ -34,7 +34,7 @@ import torch
 from . import _lib
 
 _HEAPS: dict = {}
-STATS = {"all_gather": 0, "reduce_scatter": 0}  # pull launches of this process
+STATS = {"all_gather": 0, "reduce_scatter": 0, "all_reduce": 0}  # pull launches of this process
 _TIMEOUT_NS = int(float(os.environ.get("SDR_PEER_TIMEOUT_S", "30")) * 1e9)
 
 
@@ -153,6 +153,47 @@ class PeerHeap:
                                                    self.rank, _SDR_DTYPE[dtype], _stream(self.dev))
         _lib.check(st, "sdr_reduce_scatter_peers")
         STATS["reduce_scatter"] += 1
+
+
+    def all_reduce(self, ins: list, outs: list) -> bool:
+        """P->R for contiguous tensors of one dtype: reduce-scatter pull of my
+        chunk of every tensor into my half's result area, a second barrier,
+        then a gather pull of every rank's reduced chunk into `outs`.  Sums
+        in ascending rank order (bit-exact vs comm.py:91-101).  False (nothing
+        launched) when the call does not fit a half; identical on every rank."""
+        from .movers import CudaMover, Member, layout
+        P = self.P
+        full = [Member(t, 1, t.numel(), 1, -(-t.numel() // P)) for t in ins]
+        seg = layout(full)
+        if seg * (P + 1) > self.half:
+            return False
+        res = [Member(o, 1, o.numel(), 1, m.chunk, m.seg_off) for o, m in zip(outs, full)]
+        h = self._next_half()
+        bufs = self._half_ptrs(h)
+        results = (C.c_void_p * P)(*[b + P * seg for b in bufs])
+        es = ins[0].element_size()
+        pieces = (_lib.SdrPackMember * max(1, len(full)))()
+        for i, m in enumerate(full):
+            lo = min(m.rows, self.rank * m.chunk)
+            pieces[i].data = results[self.rank] + m.seg_off
+            pieces[i].outer, pieces[i].inner, pieces[i].chunk_rows = 1, 1, m.chunk
+            pieces[i].rows = min(m.rows, lo + m.chunk) - lo
+            pieces[i].seg_off, pieces[i].elem_bytes = m.seg_off, es
+        arr = CudaMover._arr(full)
+        with torch.cuda.device(self.dev):
+            s = _stream(self.dev)
+            _lib.check(_lib.LIB.sdr_pack_scatter(arr, len(full), bufs[self.rank], seg, P, s),
+                       "sdr_pack_scatter")
+            self._barrier()
+            _lib.check(_lib.LIB.sdr_reduce_scatter_peers(pieces, len(full), bufs, seg, P, self.rank,
+                                                         _SDR_DTYPE[ins[0].dtype], s),
+                       "sdr_reduce_scatter_peers")
+            self._barrier()
+            arr = CudaMover._arr(res)
+            _lib.check(_lib.LIB.sdr_unpack_gathered_peers(arr, len(res), results, P, s),
+                       "sdr_unpack_gathered_peers")
+        STATS["all_reduce"] += 1
+        return True
 
 
 _SDR_DTYPE = {torch.float32: _lib.F32, torch.float64: _lib.F64, torch.bfloat16: _lib.BF16,

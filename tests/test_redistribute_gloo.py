@@ -143,6 +143,9 @@ def _worker_fused_grads(rank, ws, cuda=False, transport="auto"):
         assert b.meta.spec == f.meta.spec
         assert not b.meta.spec.partial_mesh_dims()
     assert len(rep_b["skipped"]) == 1 and len(rep_f["skipped"]) == 1
+    if cuda:
+        from paper_2509_07003_b200 import peer
+        assert (peer.STATS["all_reduce"] > 0) == (transport == "peer")
     # N-d fusion: the P,P group takes one round instead of one per dim
     assert len(rep_f["rounds"]) < len(rep_b["rounds"])
 
@@ -252,7 +255,7 @@ def _peer_rs_inputs(q, shapes, np_dtype):
     return outs
 
 
-def _worker_peer_reduce_scatter(rank, ws, dtype_name):
+def _worker_peer_reduce_scatter(rank, ws, dtype_name, to_replicate=False):
     """P -> S through the peer pull kernel on non-integer data: bit-exact vs
     the reference's reduction (NumPy / ml_dtypes `acc += b` in ascending rank
     order, comm.py:113-125), NaN and inf included."""
@@ -269,7 +272,7 @@ def _worker_peer_reduce_scatter(rank, ws, dtype_name):
     mesh = create_mesh([("dp", ws)])
     coord = mesh.coords_of_rank(rank)
     shapes = [(13, 37), (8, 5, 6), (3,), (ws * 64, 128)]
-    dsts = ["S(0)", "S(1)", "S(0)", "S(0)"]
+    dsts = ["R"] * 4 if to_replicate else ["S(0)", "S(1)", "S(0)", "S(0)"]
     ins = [_peer_rs_inputs(q, shapes, np_dt) for q in range(ws)]
     src = ShardSpec(mesh, parse_placements("P"))
     xs = [from_local(torch.from_numpy(ins[rank][i].view(np.uint8).copy()).view(t_dt).reshape(shp).cuda(),
@@ -277,14 +280,19 @@ def _worker_peer_reduce_scatter(rank, ws, dtype_name):
     specs = [ShardSpec(mesh, parse_placements(d)) for d in dsts]
     ledger = comm.CollectiveLedger()
     ys = redistribute_many(xs, specs, ledger)
-    assert ledger.count("reduce_scatter") == 1
+    kind = "all_reduce" if to_replicate else "reduce_scatter"
+    assert ledger.count(kind) == 1
     from paper_2509_07003_b200 import peer
-    assert peer.STATS["reduce_scatter"] == 1
+    assert peer.STATS[kind] == 1
     for i, (y, d) in enumerate(zip(ys, dsts)):
         acc = ins[0][i].copy()
         with np.errstate(all="ignore"):
             for q in range(1, ws):
                 acc += ins[q][i]
+        if to_replicate:
+            got = y.local.cpu().contiguous().view(torch.uint8).numpy().tobytes()
+            assert got == acc.view(np.uint8).tobytes(), (dtype_name, i, rank, "R")
+            continue
         dim = int(d[2])
         E = shapes[i][dim]
         c = -(-E // ws)
@@ -298,6 +306,14 @@ def _worker_peer_reduce_scatter(rank, ws, dtype_name):
 @pytest.mark.parametrize("dtype_name", ["float32", "bfloat16", "float16", "float64"])
 def test_peer_reduce_scatter_bit_exact_nonint(dtype_name):
     _spawn(_worker_peer_reduce_scatter, 3, dtype_name)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype_name", ["float32", "bfloat16"])
+def test_peer_all_reduce_bit_exact_nonint(dtype_name):
+    """P -> R: reduce pull + second barrier + gather pull, bit-exact vs the
+    reference's ascending-rank sum (comm.py:91-101)."""
+    _spawn(_worker_peer_reduce_scatter, 4, dtype_name, True)
 
 
 
