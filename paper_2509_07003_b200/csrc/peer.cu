@@ -111,6 +111,10 @@ __device__ __forceinline__ void vadd(V& acc, const V& x) {
   memcpy(&acc, a, sizeof(V));
 }
 
+#ifndef SDR_REDUCE_MINB
+#define SDR_REDUCE_MINB 5  // 48 regs: 5 CTAs per SM (latency-bound pull; A/B: 1 -> 4.4, 5 -> 5.1 TB/s at P=2)
+#endif
+
 struct PeerPtrs {
   const unsigned char* p[SDR_MAX_PEERS];
 };
@@ -120,7 +124,7 @@ struct PeerPtrs {
 // All U loads of one peer are issued before they are summed, so each thread
 // keeps U NVLink reads in flight.
 template <int DT, typename V>
-__global__ void __launch_bounds__(256) k_reduce_peers(const __grid_constant__ JobTable T,
+__global__ void __launch_bounds__(256, SDR_REDUCE_MINB) k_reduce_peers(const __grid_constant__ JobTable T,
                                                       const __grid_constant__ PeerPtrs B,
                                                       int nranks) {
   constexpr int U = static_cast<int>(kTileBytes / (sizeof(V) * 256));
