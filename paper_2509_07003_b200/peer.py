@@ -20,7 +20,8 @@ alternate halves, so one barrier per call is enough (include/sdrng.h).
 Selection (`transport()`): SDR_TRANSPORT=peer|nccl|auto (default auto = peer
 when every fiber rank is on this host and its device can reach ours; the
 decision is agreed by all fiber ranks).  SDR_PEER_HEAP_MB sizes the heap
-(default 256: two 128 MiB halves); buckets larger than a half go to NCCL.
+(default 256: two 128 MiB halves); buckets larger than a half go to NCCL,
+and so do collectives issued while a CUDA graph is being captured.
 """
 
 from __future__ import annotations
@@ -208,6 +209,11 @@ def heap_for(group, fiber, dev: torch.device):
     """The fiber's PeerHeap, or None when the peer transport is off or not
     possible (then the caller uses NCCL).  Collective on first call."""
     if group is None or dev.type != "cuda" or transport() == "nccl" or len(fiber) > _lib.MAX_PEERS:
+        return None
+    if torch.cuda.is_current_stream_capturing():
+        # barrier epochs and heap halves are chosen on the host per call, so a
+        # replayed graph would reuse them: captured collectives go to NCCL
+        # (every rank captures the same code, so all ranks agree)
         return None
     key = (tuple(fiber), dev.index)
     hp = _HEAPS.get(key)
