@@ -168,4 +168,25 @@ int unpack_local(const sdr_pack_member* M, int n, const void* seg, cudaStream_t 
   return run_jobs(jobs, s);
 }
 
+// Force-load the copy kernels (CUDA lazy loading loads a kernel at its first
+// launch, and that load waits for running kernels: a host thread that launches
+// a not-yet-loaded kernel behind a spinning peer barrier would stall).
+int preload_copy_kernels() {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaSuccess;
+  const void* fns[] = {
+      reinterpret_cast<const void*>(&k_copy_tiles_p<uint4>), reinterpret_cast<const void*>(&k_copy_tiles_p<uint2>),
+      reinterpret_cast<const void*>(&k_copy_tiles_p<uint32_t>), reinterpret_cast<const void*>(&k_copy_tiles_p<uint16_t>),
+      reinterpret_cast<const void*>(&k_copy_tiles_p<unsigned char>), reinterpret_cast<const void*>(&k_copy_tiles<uint4>),
+      reinterpret_cast<const void*>(&k_copy_tiles<uint2>), reinterpret_cast<const void*>(&k_copy_tiles<uint32_t>),
+      reinterpret_cast<const void*>(&k_copy_tiles<uint16_t>), reinterpret_cast<const void*>(&k_copy_tiles<unsigned char>)};
+  for (const void* f : fns)
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, f);
+  if (e != cudaSuccess) {
+    set_cuda_error(e);
+    return SDR_E_CUDA;
+  }
+  return SDR_OK;
+}
+
 }  // namespace sdr

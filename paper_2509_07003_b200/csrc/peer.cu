@@ -344,10 +344,43 @@ static int cuda_status(cudaError_t e) {
   return SDR_E_CUDA;
 }
 
+int preload_copy_kernels();
+
+// Load every kernel a peer collective launches (see preload_copy_kernels):
+// behind a spinning barrier, a lazy load at the pull's first launch would
+// stall this rank's host thread -- and deadlock ranks driven by one thread.
+static int preload_peer_kernels() {
+  int st = preload_copy_kernels();
+  if (st != SDR_OK) return st;
+  cudaFuncAttributes a;
+  const void* fns[] = {
+      reinterpret_cast<const void*>(&k_peer_barrier),
+      reinterpret_cast<const void*>(&k_gather_peers<uint4>), reinterpret_cast<const void*>(&k_gather_peers<uint2>),
+      reinterpret_cast<const void*>(&k_gather_peers<uint32_t>), reinterpret_cast<const void*>(&k_gather_peers<uint16_t>),
+      reinterpret_cast<const void*>(&k_gather_peers<unsigned char>),
+#define SDR_RP(DT) reinterpret_cast<const void*>(&k_reduce_peers<DT, uint4>), \
+      reinterpret_cast<const void*>(&k_reduce_peers<DT, uint2>)
+      SDR_RP(SDR_F32), SDR_RP(SDR_F64), SDR_RP(SDR_BF16), SDR_RP(SDR_F16), SDR_RP(SDR_I32), SDR_RP(SDR_I64),
+#undef SDR_RP
+      reinterpret_cast<const void*>(&k_reduce_peers<SDR_F32, uint32_t>),
+      reinterpret_cast<const void*>(&k_reduce_peers<SDR_I32, uint32_t>),
+      reinterpret_cast<const void*>(&k_reduce_peers<SDR_BF16, uint32_t>),
+      reinterpret_cast<const void*>(&k_reduce_peers<SDR_F16, uint32_t>),
+      reinterpret_cast<const void*>(&k_reduce_peers<SDR_BF16, uint16_t>),
+      reinterpret_cast<const void*>(&k_reduce_peers<SDR_F16, uint16_t>)};
+  for (const void* f : fns) {
+    const cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  return SDR_OK;
+}
+
 int peer_heap_alloc(int device, int64_t bytes, void** base, sdr_ipc_handle* handle) {
   static_assert(sizeof(sdr_ipc_handle) == sizeof(cudaIpcMemHandle_t), "IPC handle size");
   if (base == nullptr || handle == nullptr || bytes < SDR_PEER_FLAG_BYTES) return SDR_E_INVALID;
   DeviceGuard g(device);
+  const int pst = preload_peer_kernels();
+  if (pst != SDR_OK) return pst;
   void* p = nullptr;
   int st = cuda_status(cudaMalloc(&p, static_cast<size_t>(bytes)));
   if (st != SDR_OK) return st;
