@@ -123,6 +123,7 @@ def run(a):
                             "parallelism": f"tp{ws}", "per_gpu_elements": n_local,
                             "elements_per_s": round(total / ms * 1e3, 1)})
     else:
+        from paper_2509_07003_b200 import peer
         from paper_2509_07003_b200.dtensor import from_local, redistribute_many
         dp = 2 if ws % 2 == 0 else 1
         tp = ws // dp
@@ -158,7 +159,10 @@ def run(a):
                             "parallelism": f"dp{dp}xtp{tp}", "ms_allgather": round(ms_ag, 4),
                             "ms_reducescatter": round(ms_rs, 4),
                             "busbw_reducescatter": round(busbw(ms_rs), 3),
-                            "payload_bytes_per_fiber": S})
+                            "payload_bytes_per_fiber": S,
+                            # peer-memory pulls (peer.py) or NCCL; SDR_TRANSPORT=nccl forces NCCL
+                            "transport": "peer" if peer.STATS["all_gather"] else
+                                         ("nccl" if dp > 1 else "none")})
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
