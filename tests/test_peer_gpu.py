@@ -126,3 +126,73 @@ def test_concurrent_ranks_gather_and_reduce_scatter(P, iters):
                 if not torch.equal(pm[i].tensor, sums[i].narrow(dim, lo, hi - lo)):
                     bad.append(("reduce", it, r, i))
     assert not bad, f"{len(bad)} of {n} results differ (first {bad[:5]})"
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16, torch.float64,
+                                   torch.int32, torch.int64])
+def test_pull_kernels_local_peers(dtype):
+    """Both pull kernels with P local 'peer' buffers (no barrier): ragged
+    members (odd extents, empty trailing pieces, 2-byte-aligned spans), every
+    reducible dtype; sums of integer-valued data are exact in any order."""
+    from paper_2509_07003_b200 import _lib
+    from paper_2509_07003_b200.movers import CudaMover, layout
+    code = {torch.float32: _lib.F32, torch.bfloat16: _lib.BF16, torch.float16: _lib.F16,
+            torch.float64: _lib.F64, torch.int32: _lib.I32, torch.int64: _lib.I64}[dtype]
+    g = torch.Generator(device="cuda").manual_seed(7)
+    P = 5
+    shapes = [((3, 17), 1), ((2,), 0), ((9, 4, 3), 1), ((40, 33), 0), ((1, 1), 0)]
+    st = torch.cuda.current_stream().cuda_stream
+    for r in range(P):
+        fm, pm, want = [], [], []
+        packed = []
+        # every rank's full Partial tensor, packed rank-major by sdr_pack_scatter
+        fulls = [[torch.randint(-50, 50, s, device="cuda", generator=g).to(dtype) for s, _ in shapes]
+                 for _ in range(P)]
+        for q in range(P):
+            mq = []
+            for (shp, dim), t in zip(shapes, fulls[q]):
+                E = shp[dim]
+                c = -(-E // P)
+                outer = int(torch.tensor(shp[:dim]).prod()) if dim else 1
+                inner = int(torch.tensor(shp[dim + 1:]).prod()) if dim + 1 < len(shp) else 1
+                mq.append(_mk(t, outer, E, inner, c))
+            seg = layout(mq)
+            buf = torch.empty(seg * P, dtype=torch.uint8, device="cuda")
+            _lib.check(_lib.LIB.sdr_pack_scatter(CudaMover._arr(mq), len(mq), buf.data_ptr(), seg, P, st), "ps")
+            packed.append(buf)
+            fm = mq
+        for (shp, dim), m in zip(shapes, fm):
+            E = shp[dim]
+            c = -(-E // P)
+            lo, hi = min(E, r * c), min(E, r * c + c)
+            tot = sum(fulls[q][len(pm)] for q in range(P))
+            want.append(tot.narrow(dim, lo, hi - lo))
+            pm.append(_mk(torch.empty_like(want[-1]), m.outer, hi - lo, m.inner, c, m.seg_off))
+        ptrs = (C.c_void_p * P)(*[b.data_ptr() for b in packed])
+        _lib.check(_lib.LIB.sdr_reduce_scatter_peers(CudaMover._arr(pm), len(pm), ptrs, seg, P, r, code, st),
+                   "rs")
+        for w, m in zip(want, pm):
+            assert torch.equal(m.tensor, w.to(dtype)), (dtype, r)
+        # gather pull: segment q = rank q's shard, each in its own buffer
+        segs, recv = [], []
+        for q in range(P):
+            sm = []
+            for (shp, dim), t in zip(shapes, fulls[0]):
+                E = shp[dim]
+                c = -(-E // P)
+                lo, hi = min(E, q * c), min(E, q * c + c)
+                outer = int(torch.tensor(shp[:dim]).prod()) if dim else 1
+                inner = int(torch.tensor(shp[dim + 1:]).prod()) if dim + 1 < len(shp) else 1
+                sm.append(_mk(t.narrow(dim, lo, hi - lo).contiguous(), outer, hi - lo, inner, c))
+            sseg = layout(sm)
+            b = torch.empty(max(sseg, 16), dtype=torch.uint8, device="cuda")
+            _lib.check(_lib.LIB.sdr_pack_local(CudaMover._arr(sm), len(sm), b.data_ptr(), st), "pl")
+            segs.append(b)
+            if q == 0:
+                for (shp, dim), m in zip(shapes, sm):
+                    recv.append(_mk(torch.empty(shp, dtype=dtype, device="cuda"), m.outer, shp[dim], m.inner,
+                                    m.chunk, m.seg_off))
+        sp = (C.c_void_p * P)(*[b.data_ptr() for b in segs])
+        _lib.check(_lib.LIB.sdr_unpack_gathered_peers(CudaMover._arr(recv), len(recv), sp, P, st), "g")
+        for m, t in zip(recv, fulls[0]):
+            assert torch.equal(m.tensor, t), (dtype, "gather")
