@@ -169,16 +169,29 @@ def dropout_input_spec(x):
     return best[1]
 
 
-def dtensor_dropout(x, p: float, state: RngState | None = None, ledger=None, *, mover=None):
+def dropout_plan_directive(site: str, x) -> str:
+    """The static-plan directive the reference records for a dropout call
+    site (dispatch.py:612-624): `annotate <site>.<in> <placements>`, naming the
+    placement the mask is drawn at.  Replaying it (dtensor_dropout(at=...))
+    draws the same global mask at the same placement."""
+    from .placement import format_placements
+    return f"annotate {site}.<in> {format_placements(dropout_input_spec(x).placements)}"
+
+
+def dtensor_dropout(x, p: float, state: RngState | None = None, ledger=None, *, mover=None,
+                    at=None):
     """Dropout of a DTensor with single-device semantics.  The mask is this
     rank's slice of ONE global Bernoulli(1-p) draw over the input window, the
     state advances by ceil(global_numel/THETA) on every rank (dispatch.py:
-    567-576); p == 0 returns x untouched and draws nothing (ops.py:174-175)."""
+    567-576); p == 0 returns x untouched and draws nothing (ops.py:174-175).
+    `at` (a ShardSpec) is the static-eager path: the placement a recorded
+    plan annotated for this site (dispatch.py:604-608), instead of the
+    dynamic choice."""
     from .dtensor import DTensor, redistribute
     if p == 0.0:
         return x
     state = runtime_mod.current().rng if state is None else state
-    target = dropout_input_spec(x)
+    target = dropout_input_spec(x) if at is None else at
     if target != x.meta.spec:
         x = redistribute(x, target, ledger, mover=mover)
     y = dropout_apply(x.local, p, state, x.view)

@@ -156,6 +156,11 @@ def test_dropout_strategy_matches_reference_dispatch():
         spec = ShardSpec(mesh, parse_placements(src))
         x = DTensor(DTensorMeta((8, 8), spec, torch.float32), torch.zeros(1), (0, 0))
         assert str(dropout_input_spec(x).placements) == str(parse_placements(want)), (src, want)
+        # the static-plan directive the reference records for the site (dispatch.py:619-624)
+        from paper_2509_07003_b200.ops import dropout_plan_directive
+        from paper_2509_07003_b200.placement import format_placements
+        assert dropout_plan_directive("blk0.drop", x) == \
+            f"annotate blk0.drop.<in> {format_placements(parse_placements(want))}"
 
 
 @pytest.mark.parametrize("pl,sizes", [("S(0),S(1)", (2, 3)), ("P,S(1)", (2, 2)), ("IS(0,2),R", (2, 2)),
