@@ -11,6 +11,7 @@
 // dtype -- the reference's `acc = b0.copy(); acc += b1; ...` (comm.py:120-122)
 // bit for bit, x86 NaN propagation included.
 #include <cstdio>
+#include <utility>
 
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -111,6 +112,39 @@ __device__ __forceinline__ void vadd(V& acc, const V& x) {
   memcpy(&acc, a, sizeof(V));
 }
 
+// Programmatic dependent launch along pack -> barrier -> pull: the barrier and
+// the pull are launched with programmatic stream serialization, so their
+// launch overlaps the previous kernel; each executes griddepcontrol.wait (all
+// prerequisite grids complete, memory visible) before touching memory.
+#ifndef SDR_PEER_PDL
+#define SDR_PEER_PDL 1
+#endif
+
+__device__ __forceinline__ void pdl_wait() {
+#if SDR_PEER_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_dep(void (*kernel)(KArgs...), unsigned grid, unsigned block, cudaStream_t s,
+                       Args&&... args) {
+#if SDR_PEER_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+#else
+  kernel<<<grid, block, 0, s>>>(std::forward<Args>(args)...);
+#endif
+}
+
 #ifndef SDR_REDUCE_MINB
 #define SDR_REDUCE_MINB 5  // 48 regs: 5 CTAs per SM (latency-bound pull; A/B: 1 -> 4.4, 5 -> 5.1 TB/s at P=2)
 #endif
@@ -131,6 +165,7 @@ __global__ void __launch_bounds__(256, SDR_REDUCE_MINB) k_reduce_peers(const __g
   const unsigned char* so[U];
   unsigned char* dv[U];
   const int total = tile_slots<V, U>(T.jobs, T.prefix, T.n, so, dv);
+  pdl_wait();
   V acc[U];
 #pragma unroll
   for (int u = 0; u < U; ++u)
@@ -158,6 +193,7 @@ __global__ void __launch_bounds__(256) k_gather_peers(const __grid_constant__ Jo
   const unsigned char* sv[U];
   unsigned char* dv[U];
   const int total = tile_slots<V, U>(T.jobs, T.prefix, T.n, sv, dv);
+  pdl_wait();
   V v[U];
 #pragma unroll
   for (int u = 0; u < U; ++u)
@@ -176,6 +212,10 @@ struct PeerFlags {
 // kernels on this stream (the pack) before the release store.
 __global__ void k_peer_barrier(const __grid_constant__ PeerFlags F, int rank, int nranks,
                                unsigned long long epoch, long long timeout_ns) {
+  pdl_wait();  // the pack before us has completed and is visible
+  // No early trigger: the pull's CTAs would sit resident in griddepcontrol.wait
+  // on every SM while we spin, starving other streams of the same GPU (with
+  // ranks as streams of one GPU that deadlocks: tests/test_peer_gpu.py).
   const int t = threadIdx.x;
   if (t >= nranks) return;
   asm volatile("fence.acq_rel.sys;" ::: "memory");
@@ -242,11 +282,11 @@ int unpack_gathered_peers(const sdr_pack_member* M, int n, const void* const* se
   }
   return launch_groups(jobs, [&](const JobTable& T, unsigned grid, int vec) {
     switch (vec) {
-      case 16: k_gather_peers<uint4><<<grid, 256, 0, s>>>(T); break;
-      case 8: k_gather_peers<uint2><<<grid, 256, 0, s>>>(T); break;
-      case 4: k_gather_peers<uint32_t><<<grid, 256, 0, s>>>(T); break;
-      case 2: k_gather_peers<uint16_t><<<grid, 256, 0, s>>>(T); break;
-      default: k_gather_peers<unsigned char><<<grid, 256, 0, s>>>(T); break;
+      case 16: launch_dep(k_gather_peers<uint4>, grid, 256, s, T); break;
+      case 8: launch_dep(k_gather_peers<uint2>, grid, 256, s, T); break;
+      case 4: launch_dep(k_gather_peers<uint32_t>, grid, 256, s, T); break;
+      case 2: launch_dep(k_gather_peers<uint16_t>, grid, 256, s, T); break;
+      default: launch_dep(k_gather_peers<unsigned char>, grid, 256, s, T); break;
     }
   });
 }
@@ -256,12 +296,12 @@ static void launch_reduce(const JobTable& T, unsigned grid, int vec, const PeerP
                           int nranks, cudaStream_t s) {
   using E = typename Elem<DT>::T;
   if (vec >= 16) {
-    k_reduce_peers<DT, uint4><<<grid, 256, 0, s>>>(T, B, nranks);
+    launch_dep(k_reduce_peers<DT, uint4>, grid, 256, s, T, B, nranks);
   } else if (vec >= 8) {
-    k_reduce_peers<DT, uint2><<<grid, 256, 0, s>>>(T, B, nranks);
+    launch_dep(k_reduce_peers<DT, uint2>, grid, 256, s, T, B, nranks);
   } else if constexpr (sizeof(E) <= 4) {
-    if (vec >= 4) k_reduce_peers<DT, uint32_t><<<grid, 256, 0, s>>>(T, B, nranks);
-    else if constexpr (sizeof(E) <= 2) k_reduce_peers<DT, uint16_t><<<grid, 256, 0, s>>>(T, B, nranks);
+    if (vec >= 4) launch_dep(k_reduce_peers<DT, uint32_t>, grid, 256, s, T, B, nranks);
+    else if constexpr (sizeof(E) <= 2) launch_dep(k_reduce_peers<DT, uint16_t>, grid, 256, s, T, B, nranks);
   }
 }
 
@@ -320,7 +360,8 @@ int peer_barrier(void* const* flags, int rank, int nranks, uint64_t epoch, int64
     if (flags[q] == nullptr) return SDR_E_INVALID;
     F.p[q] = static_cast<unsigned long long*>(flags[q]);
   }
-  k_peer_barrier<<<1, 32 * ((nranks + 31) / 32), 0, s>>>(F, rank, nranks, epoch, timeout_ns);
+  launch_dep(k_peer_barrier, 1u, 32u * ((nranks + 31) / 32), s, F, rank, nranks,
+             static_cast<unsigned long long>(epoch), static_cast<long long>(timeout_ns));
   return check_launch();
 }
 
