@@ -547,8 +547,17 @@ def _fused_all_reduce(mesh, dims, items, ledger, mover):
     t0 = items[0][1][1]
     hp = peer.heap_for(group, fiber, t0.device) if peer.reducible(t0.dtype) else None
     if hp is not None:
-        outs = [torch.empty_like(m.tensor) for m in members]
-        if hp.all_reduce([m.tensor for m in members], outs):
+        # buckets of whole members whose rank-chunked segment fits a half
+        # P+1 times (packed input + reduced chunk); sizes are identical on
+        # every rank, so all ranks take the same branch
+        es = t0.element_size()
+        sizes = [-(-(-(-m.tensor.numel() // P) * es) // 16) * 16 for m in members]
+        cap = hp.half // (P + 1) // 256 * 256
+        if max(sizes, default=0) <= cap:
+            outs = [torch.empty_like(m.tensor) for m in members]
+            for idx in _buckets(sizes, cap=cap):
+                ok = hp.all_reduce([members[i].tensor for i in idx], [outs[i] for i in idx])
+                assert ok, "peer all-reduce bucket does not fit the heap half"
             if ledger is not None:
                 ledger.record("all_reduce", seg, P, mesh.name,
                               "+".join(mesh.dim_names[d] for d in dims))

@@ -255,12 +255,14 @@ def _peer_rs_inputs(q, shapes, np_dtype):
     return outs
 
 
-def _worker_peer_reduce_scatter(rank, ws, dtype_name, to_replicate=False):
+def _worker_peer_reduce_scatter(rank, ws, dtype_name, to_replicate=False, heap_mb=None):
     """P -> S through the peer pull kernel on non-integer data: bit-exact vs
     the reference's reduction (NumPy / ml_dtypes `acc += b` in ascending rank
     order, comm.py:113-125), NaN and inf included."""
     os.environ["SDR_COMM_CPU_STAGING"] = "1"
     os.environ["SDR_TRANSPORT"] = "peer"
+    if heap_mb is not None:  # small heap: the call is cut into several buckets
+        os.environ["SDR_PEER_HEAP_MB"] = str(heap_mb)
     torch.cuda.set_device(0)
     import ml_dtypes
     from paper_2509_07003_b200 import comm, create_mesh
@@ -271,8 +273,8 @@ def _worker_peer_reduce_scatter(rank, ws, dtype_name, to_replicate=False):
     t_dt = getattr(torch, dtype_name)
     mesh = create_mesh([("dp", ws)])
     coord = mesh.coords_of_rank(rank)
-    shapes = [(13, 37), (8, 5, 6), (3,), (ws * 64, 128)]
-    dsts = ["R"] * 4 if to_replicate else ["S(0)", "S(1)", "S(0)", "S(0)"]
+    shapes = [(13, 37), (8, 5, 6), (3,), (ws * 64, 128), (ws * 64, 128)]
+    dsts = ["R"] * 5 if to_replicate else ["S(0)", "S(1)", "S(0)", "S(0)", "S(1)"]
     ins = [_peer_rs_inputs(q, shapes, np_dt) for q in range(ws)]
     src = ShardSpec(mesh, parse_placements("P"))
     xs = [from_local(torch.from_numpy(ins[rank][i].view(np.uint8).copy()).view(t_dt).reshape(shp).cuda(),
@@ -281,9 +283,11 @@ def _worker_peer_reduce_scatter(rank, ws, dtype_name, to_replicate=False):
     ledger = comm.CollectiveLedger()
     ys = redistribute_many(xs, specs, ledger)
     kind = "all_reduce" if to_replicate else "reduce_scatter"
-    assert ledger.count(kind) == 1
     from paper_2509_07003_b200 import peer
-    assert peer.STATS[kind] == 1
+    assert peer.STATS[kind] == (1 if heap_mb is None else 2), peer.STATS
+    # one ledger entry per bucket for S/P->S (as the NCCL bucket pipeline),
+    # one per logical all-reduce
+    assert ledger.count(kind) == (1 if to_replicate else peer.STATS[kind])
     for i, (y, d) in enumerate(zip(ys, dsts)):
         acc = ins[0][i].copy()
         with np.errstate(all="ignore"):
@@ -314,6 +318,15 @@ def test_peer_all_reduce_bit_exact_nonint(dtype_name):
     """P -> R: reduce pull + second barrier + gather pull, bit-exact vs the
     reference's ascending-rank sum (comm.py:91-101)."""
     _spawn(_worker_peer_reduce_scatter, 4, dtype_name, True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("to_replicate", [False, True])
+def test_peer_bucketed_small_heap(to_replicate):
+    """A heap too small for the whole call: whole-member buckets, one pull
+    each, still bit-exact."""
+    _spawn(_worker_peer_reduce_scatter, 4, "float32", to_replicate,
+           0.4 if to_replicate else 0.3)
 
 
 
