@@ -42,6 +42,8 @@ template <typename V, int U>
 __device__ __forceinline__ int tile_slots(const CopyJob* __restrict__ jobs,
                                           const int64_t* __restrict__ prefix, int n,
                                           const unsigned char* (&sv)[U], unsigned char* (&dv)[U]) {
+  // tile bytes = U vectors x 256 threads (jobs are built with the same size)
+  constexpr int64_t kTB = static_cast<int64_t>(U) * sizeof(V) * 256;
   const int64_t t = blockIdx.x;
   int lo = 0, hi = n - 1;
   while (lo < hi) {
@@ -61,8 +63,8 @@ __device__ __forceinline__ int tile_slots(const CopyJob* __restrict__ jobs,
   } else {
     s0 = lt / J.parts;
     cnt = 1;
-    off = (lt - s0 * J.parts) * kTileBytes;
-    len = min(kTileBytes, J.span_bytes - off);
+    off = (lt - s0 * J.parts) * kTB;
+    len = min(kTB, J.span_bytes - off);
   }
   const int lv = static_cast<int>(len / static_cast<int64_t>(sizeof(V)));
   // Thread element i = tid + 256u -> (span r, vector c), stepped incrementally:
@@ -114,7 +116,8 @@ inline int widest(std::initializer_list<int64_t> vals) {
 }
 
 inline void add_job(std::vector<CopyJob>& jobs, const void* src, void* dst, int64_t nspans,
-                    int64_t span_bytes, int64_t src_stride, int64_t dst_stride) {
+                    int64_t span_bytes, int64_t src_stride, int64_t dst_stride,
+                    int64_t tile_bytes = kTileBytes) {
   if (nspans <= 0 || span_bytes <= 0) return;
   CopyJob J;
   memset(&J, 0, sizeof(J));
@@ -124,13 +127,13 @@ inline void add_job(std::vector<CopyJob>& jobs, const void* src, void* dst, int6
   J.span_bytes = span_bytes;
   J.src_stride = src_stride;
   J.dst_stride = dst_stride;
-  if (span_bytes < kTileBytes) {
-    J.spt = kTileBytes / span_bytes;
+  if (span_bytes < tile_bytes) {
+    J.spt = tile_bytes / span_bytes;
     J.parts = 1;
     J.tiles = (nspans + J.spt - 1) / J.spt;
   } else {
     J.spt = 1;
-    J.parts = (span_bytes + kTileBytes - 1) / kTileBytes;
+    J.parts = (span_bytes + tile_bytes - 1) / tile_bytes;
     J.tiles = nspans * J.parts;
   }
   J.vec = widest({static_cast<int64_t>(reinterpret_cast<uintptr_t>(src)),

@@ -149,6 +149,14 @@ static void launch_dep(void (*kernel)(KArgs...), unsigned grid, unsigned block, 
 #define SDR_REDUCE_MINB 5  // 48 regs: 5 CTAs per SM (latency-bound pull; A/B: 1 -> 4.4, 5 -> 5.1 TB/s at P=2)
 #endif
 
+#ifndef SDR_REDUCE_TILE
+#define SDR_REDUCE_TILE 16384
+#endif
+#ifndef SDR_REDUCE_PAIRS
+#define SDR_REDUCE_PAIRS 0
+#endif
+constexpr int64_t kReduceTile = SDR_REDUCE_TILE;
+
 struct PeerPtrs {
   const unsigned char* p[SDR_MAX_PEERS];
 };
@@ -161,7 +169,7 @@ template <int DT, typename V>
 __global__ void __launch_bounds__(256, SDR_REDUCE_MINB) k_reduce_peers(const __grid_constant__ JobTable T,
                                                       const __grid_constant__ PeerPtrs B,
                                                       int nranks) {
-  constexpr int U = static_cast<int>(kTileBytes / (sizeof(V) * 256));
+  constexpr int U = static_cast<int>(kReduceTile / (sizeof(V) * 256));
   const unsigned char* so[U];
   unsigned char* dv[U];
   const int total = tile_slots<V, U>(T.jobs, T.prefix, T.n, so, dv);
@@ -171,7 +179,25 @@ __global__ void __launch_bounds__(256, SDR_REDUCE_MINB) k_reduce_peers(const __g
   for (int u = 0; u < U; ++u)
     if (static_cast<int>(threadIdx.x) + u * 256 < total)
       acc[u] = *reinterpret_cast<const V*>(B.p[0] + reinterpret_cast<uintptr_t>(so[u]));
-  for (int q = 1; q < nranks; ++q) {
+  int q = 1;
+#if SDR_REDUCE_PAIRS
+  for (; q + 1 < nranks; q += 2) {  // two peers per round: 2U loads in flight
+    V x[U], y[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (static_cast<int>(threadIdx.x) + u * 256 < total) {
+        x[u] = *reinterpret_cast<const V*>(B.p[q] + reinterpret_cast<uintptr_t>(so[u]));
+        y[u] = *reinterpret_cast<const V*>(B.p[q + 1] + reinterpret_cast<uintptr_t>(so[u]));
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (static_cast<int>(threadIdx.x) + u * 256 < total) {
+        vadd<DT>(acc[u], x[u]);
+        vadd<DT>(acc[u], y[u]);
+      }
+  }
+#endif
+  for (; q < nranks; ++q) {
     V x[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -333,7 +359,7 @@ int reduce_scatter_peers(const sdr_pack_member* M, int n, const void* const* pac
     // source = offset of my segment's slot inside every rank's packed buffer
     const uintptr_t off = static_cast<uintptr_t>(rank * seg_bytes + m.seg_off);
     add_job(jobs, reinterpret_cast<const void*>(off), m.data, m.outer, m.rows * row_b,
-            m.chunk_rows * row_b, m.rows * row_b);
+            m.chunk_rows * row_b, m.rows * row_b, kReduceTile);
   }
   for (const CopyJob& J : jobs)
     if (J.vec < es) return SDR_E_ALIGN;

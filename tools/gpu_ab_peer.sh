@@ -1,3 +1,1 @@
-for v in peer_nopdl peer_pdl_notrig peer_pdl; do echo "== $v"; SDR_LIB_PATH=variants/$v.so timeout 200 python tools/time_peer_conc.py 2>&1; done
-SDR_LIB_PATH=variants/peer_pdl.so timeout 300 python -m pytest tests/test_peer_gpu.py -q -x 2>&1 | tail -2
-for v in peer_nopdl peer_pdl; do echo "== pack $v"; SDR_LIB_PATH=variants/$v.so timeout 200 python tools/time_pack.py 2>&1; done
+for v in r_base r_t8 r_t8p r_t8p_mb4 r_t16p r_t8_mb6 r_t8p_mb6; do echo "== $v"; SDR_LIB_PATH=variants/$v.so timeout 200 python tools/time_peer.py 2>&1 | head -2; done
