@@ -95,9 +95,11 @@ class PeerHeap:
         votes = [None] * self.P
         dist.all_gather_object(votes, bool(reach), group=group)
         self.ok = all(votes)
-        if not self.ok:
+        if not self.ok:  # give everything back: this fiber uses NCCL
             for p in opened:
                 _lib.LIB.sdr_peer_heap_close(p)
+            _lib.LIB.sdr_peer_heap_free(self.own)
+            self.own = None
             self.bases = [None] * self.P
         self._flags = (C.c_void_p * self.P)(*self.bases) if self.ok else None
 
