@@ -266,3 +266,21 @@ def _ref_module(name):
     if ref_src not in sys.path:
         sys.path.insert(0, ref_src)
     return importlib.import_module("spmdsim." + name)
+
+
+def test_peer_transport_selection(monkeypatch):
+    """SDR_TRANSPORT parsing and the cases that must stay on NCCL without
+    touching the GPU: no process group, CPU tensors, forced nccl."""
+    import torch
+    from paper_2509_07003_b200 import peer
+    monkeypatch.setenv("SDR_TRANSPORT", "bogus")
+    with pytest.raises(ValueError):
+        peer.transport()
+    for t in ("auto", "peer", "nccl"):
+        monkeypatch.setenv("SDR_TRANSPORT", t)
+        assert peer.transport() == t
+        assert peer.heap_for(None, [0, 1], torch.device("cpu")) is None
+        assert peer.heap_for(object(), [0, 1], torch.device("cpu")) is None
+    monkeypatch.setenv("SDR_TRANSPORT", "nccl")
+    assert peer.heap_for(object(), [0, 1], torch.device("cuda", 0)) is None
+    assert peer.reducible(torch.bfloat16) and not peer.reducible(torch.bool)
