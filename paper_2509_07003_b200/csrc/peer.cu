@@ -157,6 +157,14 @@ static void launch_dep(void (*kernel)(KArgs...), unsigned grid, unsigned block, 
 #endif
 constexpr int64_t kReduceTile = SDR_REDUCE_TILE;
 
+// Loads of peer memory bypass the caches (ld.global.cv): a half is rewritten
+// by its owner every other call, so no line of it may be reused from a cache
+// across calls; the owner's L2 is the point of coherence.
+template <typename V>
+__device__ __forceinline__ V load_peer(const unsigned char* p) {
+  return __ldcv(reinterpret_cast<const V*>(p));
+}
+
 struct PeerPtrs {
   const unsigned char* p[SDR_MAX_PEERS];
 };
@@ -178,7 +186,7 @@ __global__ void __launch_bounds__(256, SDR_REDUCE_MINB) k_reduce_peers(const __g
 #pragma unroll
   for (int u = 0; u < U; ++u)
     if (static_cast<int>(threadIdx.x) + u * 256 < total)
-      acc[u] = *reinterpret_cast<const V*>(B.p[0] + reinterpret_cast<uintptr_t>(so[u]));
+      acc[u] = load_peer<V>(B.p[0] + reinterpret_cast<uintptr_t>(so[u]));
   int q = 1;
 #if SDR_REDUCE_PAIRS
   for (; q + 1 < nranks; q += 2) {  // two peers per round: 2U loads in flight
@@ -186,8 +194,8 @@ __global__ void __launch_bounds__(256, SDR_REDUCE_MINB) k_reduce_peers(const __g
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (static_cast<int>(threadIdx.x) + u * 256 < total) {
-        x[u] = *reinterpret_cast<const V*>(B.p[q] + reinterpret_cast<uintptr_t>(so[u]));
-        y[u] = *reinterpret_cast<const V*>(B.p[q + 1] + reinterpret_cast<uintptr_t>(so[u]));
+        x[u] = load_peer<V>(B.p[q] + reinterpret_cast<uintptr_t>(so[u]));
+        y[u] = load_peer<V>(B.p[q + 1] + reinterpret_cast<uintptr_t>(so[u]));
       }
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -202,7 +210,7 @@ __global__ void __launch_bounds__(256, SDR_REDUCE_MINB) k_reduce_peers(const __g
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (static_cast<int>(threadIdx.x) + u * 256 < total)
-        x[u] = *reinterpret_cast<const V*>(B.p[q] + reinterpret_cast<uintptr_t>(so[u]));
+        x[u] = load_peer<V>(B.p[q] + reinterpret_cast<uintptr_t>(so[u]));
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (static_cast<int>(threadIdx.x) + u * 256 < total) vadd<DT>(acc[u], x[u]);
@@ -223,7 +231,7 @@ __global__ void __launch_bounds__(256) k_gather_peers(const __grid_constant__ Jo
   V v[U];
 #pragma unroll
   for (int u = 0; u < U; ++u)
-    if (static_cast<int>(threadIdx.x) + u * 256 < total) v[u] = *reinterpret_cast<const V*>(sv[u]);
+    if (static_cast<int>(threadIdx.x) + u * 256 < total) v[u] = load_peer<V>(sv[u]);
 #pragma unroll
   for (int u = 0; u < U; ++u)
     if (static_cast<int>(threadIdx.x) + u * 256 < total) *reinterpret_cast<V*>(dv[u]) = v[u];
