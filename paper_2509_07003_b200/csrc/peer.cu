@@ -153,7 +153,7 @@ static void launch_dep(void (*kernel)(KArgs...), unsigned grid, unsigned block, 
 #define SDR_REDUCE_TILE 16384
 #endif
 #ifndef SDR_REDUCE_PAIRS
-#define SDR_REDUCE_PAIRS 0
+#define SDR_REDUCE_PAIRS 0  // two peers per load round (A/B: no gain, profiles/r01_peer_reduce_tile_ab.txt)
 #endif
 constexpr int64_t kReduceTile = SDR_REDUCE_TILE;
 
@@ -169,7 +169,7 @@ struct PeerPtrs {
   const unsigned char* p[SDR_MAX_PEERS];
 };
 
-// One CTA per <= kTileBytes tile of the output pieces.  Job `src` fields are
+// One CTA per <= kReduceTile tile of the output pieces.  Job `src` fields are
 // byte OFFSETS into every rank's packed buffer (same layout on every rank).
 // All U loads of one peer are issued before they are summed, so each thread
 // keeps U NVLink reads in flight.
