@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["dropout", "randn", "embed", "init", "redistribute"],
+    ap.add_argument("--workload", choices=["dropout", "randn", "embed", "init", "redistribute", "peer"],
                     default="dropout",
                     help="dropout = BASELINE cfg2 (the driver's line); the others are the secondary "
                          "configs 1, 3, 4 and 5, printed in the same JSON shape")

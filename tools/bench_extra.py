@@ -9,6 +9,8 @@ init         cfg4: all 291 LLaMA-3-8B params, Normal(0,0.02) bf16, TP=N (strong)
 redistribute cfg5: one LLaMA-3-8B layer's params on DP x TP: fused all-gather over
              DP (S->R) then reduce-scatter of same-shaped grads (P->S); at N=1
              this measures pack + local copy + unpack only (no peers).
+peer         cfg5 through the peer transport with all 8 DP2 x TP4 ranks emulated
+             as concurrent streams of one GPU (tools/peer_emul.py); N=1 only.
 """
 import json
 import math
@@ -122,6 +124,50 @@ def run(a):
                     config={"workload": "cfg4: LLaMA-3-8B 291 params normal(0,0.02) bf16, TP placements",
                             "parallelism": f"tp{ws}", "per_gpu_elements": n_local,
                             "elements_per_s": round(total / ms * 1e3, 1)})
+    elif a.workload == "peer":
+        if ws > 1:
+            raise SystemExit("--workload peer emulates all cfg5 ranks on one GPU: run it with N=1")
+        from tools.peer_emul import Emulated
+        em = Emulated()
+        cur = torch.cuda.current_stream(dev)
+        for _ in range(a.warmup):
+            em.step()
+        ok = em.check()
+        torch.cuda.synchronize(dev)
+        ev0, ev1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        torch.cuda._sleep(int(4e8))  # the host enqueues all steps of all 8 streams behind this
+        ev0.record(cur)
+        for s_ in em.streams:
+            s_.wait_stream(cur)
+        for _ in range(a.steps):
+            em.step()
+        for s_ in em.streams:
+            cur.wait_stream(s_)
+        ev1.record(cur)
+        torch.cuda.synchronize(dev)
+        ms = ev0.elapsed_time(ev1) / a.steps
+        nbytes = em.hbm_bytes_per_step()
+        em.close()
+        try:
+            with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "MEASURED_PEAKS.json")) as f:
+                hbm_peak = float(json.load(f)["hbm_gbs"])
+        except (OSError, KeyError, ValueError):
+            hbm_peak = 6650.0  # fallback figure of B200_PROFILING.md
+        gbs = nbytes / ms / 1e6
+        line.update(metric="cfg5 fused redistribute via peer transport, all 8 ranks emulated on one GPU "
+                           "(HBM-side GB/s)", value=round(gbs, 1), unit="GB/s", ms_per_step=round(ms, 4),
+                    scaling="none", dtype="bf16", gpu_launches=a.steps * em.n * 6,
+                    roofline={"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                              "frac": round(gbs / hbm_peak, 4), "traffic": None},
+                    config={"workload": "cfg5: one LLaMA-3-8B layer on DP2 x TP4; per step every rank "
+                                        "does the fused S->R all-gather over its DP fiber and the fused "
+                                        "P->S reduce-scatter of same-shaped grads (pack -> device barrier "
+                                        "-> pull kernel), 8 ranks as 8 concurrent streams of one GPU",
+                            "parallelism": "dp2xtp4 emulated", "bit_exact_check": ok,
+                            "hbm_bytes_per_step": nbytes,
+                            "note": "all ranks share one GPU's HBM: this is the pipeline's HBM-side rate, "
+                                    "not an NVLink rate"})
     else:
         from paper_2509_07003_b200 import peer
         from paper_2509_07003_b200.dtensor import from_local, redistribute_many
