@@ -479,10 +479,10 @@ def _peer_gather(group, fiber, dev, send_members, recv_members, ledger, mesh, md
     barrier and one pull kernel that writes the full tensors.  False when the
     transport is off / impossible or a member exceeds the heap half (the same
     answer on every fiber rank: sizes are the padded segment bytes)."""
-    hp = peer.heap_for(group, fiber, dev)
+    sizes = _padded_bytes(send_members)
+    hp = peer.heap_for(group, fiber, dev, need_half=max(sizes, default=0))
     if hp is None:
         return False
-    sizes = _padded_bytes(send_members)
     if max(sizes, default=0) > hp.half:
         return False
     for idx in _buckets(sizes, cap=hp.half):
@@ -502,10 +502,10 @@ def _peer_reduce_scatter(group, fiber, t, full_members, piece_members, ledger, m
     into the output pieces."""
     if not peer.reducible(t.dtype):
         return False
-    hp = peer.heap_for(group, fiber, t.device)
+    sizes = _padded_bytes(full_members)
+    hp = peer.heap_for(group, fiber, t.device, need_half=max(sizes, default=0) * P + 256 * P)
     if hp is None:
         return False
-    sizes = _padded_bytes(full_members)
     cap = hp.half // P // 256 * 256
     if max(sizes, default=0) > cap:
         return False
@@ -545,13 +545,14 @@ def _fused_all_reduce(mesh, dims, items, ledger, mover):
     members = [Member(slot[1].contiguous(), 1, 1, slot[1].numel(), 1) for _, slot in items]
     seg = layout(members, align=16)
     t0 = items[0][1][1]
-    hp = peer.heap_for(group, fiber, t0.device) if peer.reducible(t0.dtype) else None
+    es = t0.element_size()
+    # rank-chunked segment bytes per member (identical on every rank)
+    sizes = [-(-(-(-m.tensor.numel() // P) * es) // 16) * 16 for m in members]
+    hp = (peer.heap_for(group, fiber, t0.device, need_half=max(sizes, default=0) * (P + 1) + 256 * (P + 1))
+          if peer.reducible(t0.dtype) else None)
     if hp is not None:
-        # buckets of whole members whose rank-chunked segment fits a half
-        # P+1 times (packed input + reduced chunk); sizes are identical on
-        # every rank, so all ranks take the same branch
-        es = t0.element_size()
-        sizes = [-(-(-(-m.tensor.numel() // P) * es) // 16) * 16 for m in members]
+        # buckets of whole members whose segment fits a half P+1 times
+        # (packed input + reduced chunk); all ranks take the same branch
         cap = hp.half // (P + 1) // 256 * 256
         if max(sizes, default=0) <= cap:
             outs = [torch.empty_like(m.tensor) for m in members]

@@ -207,9 +207,16 @@ def reducible(dtype: torch.dtype) -> bool:
     return dtype in _SDR_DTYPE
 
 
-def heap_for(group, fiber, dev: torch.device):
+def _max_half() -> int:
+    return int(float(os.environ.get("SDR_PEER_HEAP_MAX_MB", "4096")) * (1 << 20)) // 2
+
+
+def heap_for(group, fiber, dev: torch.device, need_half: int = 0):
     """The fiber's PeerHeap, or None when the peer transport is off or not
-    possible (then the caller uses NCCL).  Collective on first call."""
+    possible (then the caller uses NCCL).  Collective on first call, and when
+    a call needs a larger half than the heap has (`need_half` bytes, up to
+    SDR_PEER_HEAP_MAX_MB / 2): the heap is then regrown on every fiber rank
+    (they all pass the same need, computed from padded segment sizes)."""
     if group is None or dev.type != "cuda" or transport() == "nccl" or len(fiber) > _lib.MAX_PEERS:
         return None
     if torch.cuda.is_current_stream_capturing():
@@ -217,11 +224,32 @@ def heap_for(group, fiber, dev: torch.device):
         # replayed graph would reuse them: captured collectives go to NCCL
         # (every rank captures the same code, so all ranks agree)
         return None
+    need_half = -(-int(need_half) // 256) * 256
     key = (tuple(fiber), dev.index)
     hp = _HEAPS.get(key)
     if hp is None:
         half = int(float(os.environ.get("SDR_PEER_HEAP_MB", "256")) * (1 << 20)) // 2
-        hp = _HEAPS[key] = PeerHeap(group, fiber, dev, half)
+        hp = _HEAPS[key] = PeerHeap(group, fiber, dev, max(half, min(need_half, _max_half())))
         if not hp.ok and transport() == "peer":
             raise RuntimeError(f"SDR_TRANSPORT=peer but fiber {fiber} cannot map peer memory")
+    elif hp.ok and hp.half < need_half <= _max_half():
+        hp = _HEAPS[key] = _regrow(hp, group, fiber, dev, max(need_half, 2 * hp.half))
     return hp if hp.ok else None
+
+
+def _regrow(hp: PeerHeap, group, fiber, dev, half: int) -> PeerHeap:
+    """Replace a fiber's heap by a larger one.  A device barrier first: every
+    rank has then finished its pulls from the old halves (stream order), so
+    after a host sync the mappings can be closed; a host barrier keeps the
+    owners from freeing before every importer has closed."""
+    import torch.distributed as dist
+    with torch.cuda.device(dev):
+        hp._barrier()
+        torch.cuda.current_stream(dev).synchronize()
+    for q, b in enumerate(hp.bases):
+        if q != hp.rank and b is not None:
+            _lib.LIB.sdr_peer_heap_close(b)
+    dist.barrier(group=group)
+    _lib.LIB.sdr_peer_heap_free(hp.own)
+    STATS["regrow"] = STATS.get("regrow", 0) + 1
+    return PeerHeap(group, fiber, dev, half)

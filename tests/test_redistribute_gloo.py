@@ -281,13 +281,21 @@ def _worker_peer_reduce_scatter(rank, ws, dtype_name, to_replicate=False, heap_m
                      src, shp, coord) for i, shp in enumerate(shapes)]
     specs = [ShardSpec(mesh, parse_placements(d)) for d in dsts]
     ledger = comm.CollectiveLedger()
-    ys = redistribute_many(xs, specs, ledger)
     kind = "all_reduce" if to_replicate else "reduce_scatter"
     from paper_2509_07003_b200 import peer
-    assert peer.STATS[kind] == (1 if heap_mb is None else 2), peer.STATS
+    regrow = heap_mb is not None and heap_mb < 0.1
+    if regrow:  # a tiny first call creates a small heap; the main call must regrow it
+        redistribute_many([xs[2]], [specs[2]])
+    before = peer.STATS[kind]
+    ys = redistribute_many(xs, specs, ledger)
+    pulls = peer.STATS[kind] - before
+    if regrow:
+        assert peer.STATS.get("regrow", 0) == 1 and pulls >= 1, peer.STATS
+    else:
+        assert pulls == (1 if heap_mb is None else 2), peer.STATS
     # one ledger entry per bucket for S/P->S (as the NCCL bucket pipeline),
     # one per logical all-reduce
-    assert ledger.count(kind) == (1 if to_replicate else peer.STATS[kind])
+    assert ledger.count(kind) == (1 if to_replicate else pulls)
     for i, (y, d) in enumerate(zip(ys, dsts)):
         acc = ins[0][i].copy()
         with np.errstate(all="ignore"):
@@ -318,6 +326,15 @@ def test_peer_all_reduce_bit_exact_nonint(dtype_name):
     """P -> R: reduce pull + second barrier + gather pull, bit-exact vs the
     reference's ascending-rank sum (comm.py:91-101)."""
     _spawn(_worker_peer_reduce_scatter, 4, dtype_name, True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("to_replicate", [False, True])
+def test_peer_heap_regrows_for_large_member(to_replicate):
+    """The first call needs a larger half than SDR_PEER_HEAP_MB gives: every
+    fiber rank regrows its heap (device barrier, close, host barrier, free,
+    re-exchange) and the call stays on the peer transport, bit-exact."""
+    _spawn(_worker_peer_reduce_scatter, 4, "float32", to_replicate, 0.05)
 
 
 @pytest.mark.gpu
