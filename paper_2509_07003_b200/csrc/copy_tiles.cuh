@@ -97,7 +97,10 @@ __device__ __forceinline__ int tile_slots(const CopyJob* __restrict__ jobs,
 // Small calls (the common case: a layer's members x ranks): the job table is a
 // kernel parameter -- no allocation or H2D copy per call, and the launch is
 // stream-capturable into a CUDA graph.
-constexpr int kParamJobs = 96;
+#ifndef SDR_PARAM_JOBS
+#define SDR_PARAM_JOBS 96
+#endif
+constexpr int kParamJobs = SDR_PARAM_JOBS;
 struct JobTable {
   int32_t n;
   int32_t pad_;
