@@ -378,3 +378,49 @@ def _worker_traced_redistribute(rank, ws):
 
 def test_traced_redistribute_gloo():
     _spawn(_worker_traced_redistribute, 2)
+
+
+def _worker_golden_cpu_peer(rank, ws, mesh_sizes, initial_half):
+    """The golden redistribute cases through dtensor's PEER-transport host
+    logic on CPU: peer.heap_for patched to a gloo-backed stand-in with the
+    same contract (tests/cpu_peer.py).  A small initial half forces whole-
+    member buckets and a heap sized past it; every fiber rank must issue the
+    same pulls in the same order, and the results must equal the reference's
+    (regrowth itself: test_peer_heap_regrows_for_large_member on the GPU)."""
+    import functools
+    import cpu_peer
+    from paper_2509_07003_b200 import comm, create_mesh, peer
+    from paper_2509_07003_b200.dtensor import from_local, redistribute_many
+    from paper_2509_07003_b200.placement import ShardSpec, parse_placements
+    peer.heap_for = functools.partial(cpu_peer.heap_for, initial_half=initial_half)
+    man, arr = _golden()
+    mesh = create_mesh([(f"m{j}", s) for j, s in enumerate(mesh_sizes)])
+    coord = mesh.coords_of_rank(rank)
+    tag = "_".join(map(str, coord))
+    cases = [c for c in man["redistribute"] if tuple(c["mesh"]) == tuple(mesh_sizes)]
+    xs, dsts, wants = [], [], []
+    for c in cases:
+        src = ShardSpec(mesh, parse_placements(c["src"]))
+        xs.append(from_local(torch.from_numpy(np.ascontiguousarray(arr[c["key"] + "_in_" + tag])), src,
+                             tuple(c["shape"]), coord))
+        dsts.append(ShardSpec(mesh, parse_placements(c["dst"])))
+        wants.append(arr[c["key"] + "_out_" + tag])
+    ys = redistribute_many(xs, dsts, comm.CollectiveLedger())
+    for y, want, c in zip(ys, wants, cases):
+        assert y.local.numpy().tobytes() == np.ascontiguousarray(want).tobytes(), ("peer-cpu", c)
+    assert cpu_peer.LOG, "the peer path did not run"
+    logs = [None] * ws
+    dist.all_gather_object(logs, (coord, cpu_peer.LOG))
+    # ranks of one fiber see identical pull sequences; all ranks pull
+    assert all(l for _, l in logs), logs
+    if len(mesh_sizes) == 1:
+        assert len({tuple(l) for _, l in logs}) == 1, logs
+    if initial_half < 1024:  # the heaps were sized (or regrown) past the initial half
+        assert any(h.half > initial_half for h in cpu_peer._HEAPS.values())
+
+
+@pytest.mark.parametrize("mesh_sizes,initial_half", [((4,), 1 << 20), ((2, 4), 1 << 20), ((4,), 256),
+                                                     ((2, 4), 256)])
+def test_peer_transport_host_logic_cpu(mesh_sizes, initial_half):
+    _spawn(_worker_golden_cpu_peer, int(np.prod(mesh_sizes)), mesh_sizes, initial_half)
+
