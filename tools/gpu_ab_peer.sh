@@ -1,1 +1,1 @@
-for v in pj96 pj8 pj96 pj8; do echo "== $v"; SDR_LIB_PATH=variants/$v.so timeout 200 python tools/time_peer_conc.py 2>&1; done
+for v in r_base r_mb6 r_mb6p r_base r_mb6 r_mb6p; do echo "== $v"; SDR_LIB_PATH=variants/$v.so timeout 200 python tools/time_peer.py 2>&1 | head -2; done
