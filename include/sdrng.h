@@ -102,6 +102,15 @@ int32_t sdr_philox_blocks(const uint64_t* tau, const uint64_t* beta, int64_t n, 
 int32_t sdr_fill(void* out, int32_t out_dtype, const sdr_dist* dist, const sdr_rng* rng,
                  const sdr_view* view, void* stream);
 
+/* The distribution plug-in point Distribution.transform(words, dtype)
+ * (rng.py:104-110; the five transforms rng.py:113-182): out[i] = value of
+ * `dist` for the Philox block whose words 0 and 1 are w0[i], w1[i] (device
+ * arrays of n uint32; no distribution reads words 2-3).  Same arithmetic as
+ * sdr_fill (the fill kernels call the same device transform), so
+ * transform(blocks(...)) == fill_random(...) bit for bit. */
+int32_t sdr_transform(const uint32_t* w0, const uint32_t* w1, int64_t n, const sdr_dist* dist,
+                      void* out, int32_t out_dtype, void* stream);
+
 /* Multi-tensor fill: n independent fills in ONE launch (Module.materialize,
  * model.py:121-132 -> generate_distributed, rng.py:220-235).  Each fill has
  * its own dist/rng/view/dtype.  Table arrays are host memory. */

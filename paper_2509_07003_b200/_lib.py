@@ -85,6 +85,8 @@ def _load():
                                           C.c_void_p, C.c_void_p]),
         "sdr_fill": (C.c_int32, [C.c_void_p, C.c_int32, P(SdrDist), P(SdrRng), P(SdrView),
                                  C.c_void_p]),
+        "sdr_transform": (C.c_int32, [C.c_void_p, C.c_void_p, C.c_int64, P(SdrDist), C.c_void_p,
+                                      C.c_int32, C.c_void_p]),
         "sdr_fill_batch": (C.c_int32, [P(C.c_void_p), P(C.c_int32), P(SdrDist), P(SdrRng),
                                        P(SdrView), C.c_int32, C.c_void_p]),
         "sdr_dropout": (C.c_int32, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
@@ -123,7 +125,7 @@ LIB = _load()
 
 EXPORTED = (
     "sdr_version", "sdr_strerror", "sdr_last_cuda_error", "sdr_philox_block_host",
-    "sdr_philox_blocks", "sdr_fill", "sdr_fill_batch", "sdr_dropout", "sdr_normal_tables_load",
+    "sdr_philox_blocks", "sdr_fill", "sdr_transform", "sdr_fill_batch", "sdr_dropout", "sdr_normal_tables_load",
     "sdr_normal_tables_loaded", "sdr_normal_fallback_count", "sdr_unpack_gathered",
     "sdr_pack_scatter", "sdr_pack_local", "sdr_unpack_local", "sdr_probe_int32",
     "sdr_peer_heap_alloc", "sdr_peer_heap_open", "sdr_peer_heap_close", "sdr_peer_heap_free",

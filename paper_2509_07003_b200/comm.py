@@ -66,8 +66,10 @@ def _host_staged(t) -> bool:
     return t.is_cuda and os.environ.get("SDR_COMM_CPU_STAGING") == "1"
 
 
-def all_gather_into(recv, send, group, ledger=None, mesh="", dims="", P=1):
-    """recv[P*len(send)] <- every fiber member's `send`, in fiber order."""
+def all_gather_into(recv, send, group, ledger=None, mesh="", dims="", P=1, nbytes=None):
+    """recv[P*len(send)] <- every fiber member's `send`, in fiber order.
+    `nbytes` is the payload the ledger records (default: recv's bytes); a
+    coalesced call passes its members' real bytes, without padding."""
     import torch.distributed as dist
     if P == 1 or group is None:
         recv.copy_(send)
@@ -78,11 +80,13 @@ def all_gather_into(recv, send, group, ledger=None, mesh="", dims="", P=1):
     else:
         dist.all_gather_into_tensor(recv, send, group=group)
     if ledger is not None:
-        ledger.record("all_gather", recv.numel() * recv.element_size(), P, mesh, dims)
+        ledger.record("all_gather", recv.numel() * recv.element_size() if nbytes is None else nbytes,
+                      P, mesh, dims)
 
 
-def reduce_scatter_into(out, inp, group, ledger=None, mesh="", dims="", P=1):
-    """out <- this rank's segment of the elementwise sum of every member's inp."""
+def reduce_scatter_into(out, inp, group, ledger=None, mesh="", dims="", P=1, nbytes=None):
+    """out <- this rank's segment of the elementwise sum of every member's inp
+    (`nbytes`: the ledger payload, as in all_gather_into)."""
     import torch.distributed as dist
     if P == 1 or group is None:
         out.copy_(inp)
@@ -93,10 +97,11 @@ def reduce_scatter_into(out, inp, group, ledger=None, mesh="", dims="", P=1):
     else:
         dist.reduce_scatter_tensor(out, inp, op=dist.ReduceOp.SUM, group=group)
     if ledger is not None:
-        ledger.record("reduce_scatter", inp.numel() * inp.element_size(), P, mesh, dims)
+        ledger.record("reduce_scatter", inp.numel() * inp.element_size() if nbytes is None else nbytes,
+                      P, mesh, dims)
 
 
-def all_reduce_into(buf, group, ledger=None, mesh="", dims="", P=1):
+def all_reduce_into(buf, group, ledger=None, mesh="", dims="", P=1, nbytes=None):
     import torch.distributed as dist
     if P > 1 and group is not None and _host_staged(buf):
         b = buf.cpu()
@@ -105,7 +110,8 @@ def all_reduce_into(buf, group, ledger=None, mesh="", dims="", P=1):
     elif P > 1 and group is not None:
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
     if ledger is not None:
-        ledger.record("all_reduce", buf.numel() * buf.element_size(), P, mesh, dims)
+        ledger.record("all_reduce", buf.numel() * buf.element_size() if nbytes is None else nbytes,
+                      P, mesh, dims)
 
 
 # ---------------------------------------------------------------------------
@@ -164,11 +170,14 @@ class GradBucket:
 def bucketize(tensors, capacity_bytes: int) -> list[list]:
     """Greedy buckets over the REVERSED creation order (gradients become ready
     back to front); a tensor larger than the capacity gets a bucket of its
-    own (reference comm.py:140-150).  Sizes are local-shard bytes."""
+    own (reference comm.py:140-150).  Sizes are the largest local shard over
+    the mesh (local_nbytes_max, as the reference's _pack_buckets): derived
+    from the spec alone, so every rank -- in every fiber -- cuts the same
+    buckets even for uneven shards."""
     out: list[list] = []
     used = 0
     for t in tensors[::-1]:
-        nb = t.local.numel() * t.local.element_size()
+        nb = t.local_nbytes_max()
         if not out or (used + nb > capacity_bytes and out[-1]):
             out.append([])
             used = 0
@@ -199,7 +208,7 @@ def _reduce_buckets(members, dims, bucket_bytes, ledger, mover, rounds, label):
     out = {}
     for bucket in bucketize(members, bucket_bytes):
         slots = [[m.meta.spec, m.local] for m in bucket]
-        _fused_all_reduce(mesh, dims, list(zip(bucket, slots)), ledger, mover)
+        _fused_all_reduce(mesh, dims, list(zip(bucket, slots)), ledger, mover, ledger_mesh=label)
         rounds.append(("all_reduce", label, tuple(mesh.dim_names[d] for d in dims)))
         for m, (spec, loc) in zip(bucket, slots):
             for d in dims:

@@ -8,6 +8,8 @@ int fill_batch(void* const* outs, const int32_t* dts, const sdr_dist* dists, con
                const sdr_view* views, int n, cudaStream_t s);
 int dropout(const void* x, int xt, void* y, int yt, void* mask, int mt, double p,
             const sdr_rng& rng, const sdr_view& view, cudaStream_t s);
+int transform(const uint32_t* w0, const uint32_t* w1, int64_t n, const sdr_dist& dist, void* out,
+              int dt, cudaStream_t s);
 int philox_blocks(const uint64_t* tau, const uint64_t* beta, int64_t n, uint64_t seed,
                   uint32_t* words, cudaStream_t s);
 int normal_tables_load(int device, const double* r_host, const double* c_host, double* er,
@@ -71,6 +73,12 @@ int32_t sdr_fill(void* out, int32_t out_dtype, const sdr_dist* dist, const sdr_r
                  const sdr_view* view, void* stream) {
   if (dist == nullptr || rng == nullptr || view == nullptr) return SDR_E_INVALID;
   return sdr::fill(out, out_dtype, *dist, *rng, *view, as_stream(stream));
+}
+
+int32_t sdr_transform(const uint32_t* w0, const uint32_t* w1, int64_t n, const sdr_dist* dist,
+                      void* out, int32_t out_dtype, void* stream) {
+  if (dist == nullptr) return SDR_E_INVALID;
+  return sdr::transform(w0, w1, n, *dist, out, out_dtype, as_stream(stream));
 }
 
 int32_t sdr_fill_batch(void* const* outs, const int32_t* out_dtypes, const sdr_dist* dists,

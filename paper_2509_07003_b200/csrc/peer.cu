@@ -253,7 +253,9 @@ __global__ void k_peer_barrier(const __grid_constant__ PeerFlags F, int rank, in
   const int t = threadIdx.x;
   if (t >= nranks) return;
   asm volatile("fence.acq_rel.sys;" ::: "memory");
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(F.p[t] + rank), "l"(epoch) : "memory");
+  // max, not a plain store: a slot's epoch can never move backwards, whatever
+  // order two barrier kernels of this rank happen to run in
+  asm volatile("red.release.sys.global.max.u64 [%0], %1;" ::"l"(F.p[t] + rank), "l"(epoch) : "memory");
   const unsigned long long* mine = F.p[rank] + t;
   unsigned long long t0, now, v;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));

@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "rng_common.cuh"
@@ -332,6 +333,24 @@ __global__ void k_philox_blocks(const uint64_t* tau, const uint64_t* beta, int64
   words[4 * i + 1] = x1;
   words[4 * i + 2] = x2;
   words[4 * i + 3] = x3;
+}
+
+// Distribution.transform (rng.py:104-182): words -> values, elementwise, with
+// the same device transform the fill kernels use.
+template <int DIST, int DT>
+__global__ void __launch_bounds__(256) k_transform(const uint32_t* __restrict__ w0,
+                                                   const uint32_t* __restrict__ w1, int64_t n,
+                                                   const __grid_constant__ DistP P, void* out) {
+  const NormalLut* L = nullptr;
+  if constexpr (DIST == SDR_NORMAL) {
+    __shared__ __align__(16) NormalLut s_lut;
+    stage_lut(&s_lut, P.nm.lut);
+    L = &s_lut;
+  }
+  using T = typename St<DT>::T;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    static_cast<T*>(out)[i] = dist_value<DIST, DT>(P, L, __ldg(w0 + i), __ldg(w1 + i));
 }
 
 // Exhaustive calibration of the Normal fast path against the NumPy tables:
@@ -732,6 +751,60 @@ int fill(void* out, int dt, const sdr_dist& dist, const sdr_rng& rng, const sdr_
     case SDR_BERNOULLI: return dispatch_fill_dt<SDR_BERNOULLI>(dt, A, fast, s);
     default: return SDR_E_DIST;
   }
+}
+
+// Calls f(std::integral_constant<int, DT>) for the output dtypes the
+// reference's NumPy/ml_dtypes path gives distribution DIST; SDR_E_DTYPE else.
+template <int DIST, typename F>
+static int with_dtype(int dt, F&& f) {
+  constexpr bool flt = true, half = DIST != SDR_UNIFORM01 && DIST != SDR_RANDINT;
+  constexpr bool ints = DIST == SDR_RANDINT || DIST == SDR_BERNOULLI, bytes = DIST == SDR_BERNOULLI;
+  switch (dt) {
+    case SDR_F32: if constexpr (flt) return f(std::integral_constant<int, SDR_F32>{}); break;
+    case SDR_F64: if constexpr (flt) return f(std::integral_constant<int, SDR_F64>{}); break;
+    case SDR_BF16: if constexpr (half) return f(std::integral_constant<int, SDR_BF16>{}); break;
+    case SDR_F16: if constexpr (half) return f(std::integral_constant<int, SDR_F16>{}); break;
+    case SDR_I64: if constexpr (ints) return f(std::integral_constant<int, SDR_I64>{}); break;
+    case SDR_I32: if constexpr (ints) return f(std::integral_constant<int, SDR_I32>{}); break;
+    case SDR_U8: if constexpr (bytes) return f(std::integral_constant<int, SDR_U8>{}); break;
+    case SDR_BOOL: if constexpr (bytes) return f(std::integral_constant<int, SDR_BOOL>{}); break;
+    default: break;
+  }
+  return SDR_E_DTYPE;
+}
+
+template <typename F>
+static int with_dist(int kind, F&& f) {
+  switch (kind) {
+    case SDR_UNIFORM01: return f(std::integral_constant<int, SDR_UNIFORM01>{});
+    case SDR_UNIFORM: return f(std::integral_constant<int, SDR_UNIFORM>{});
+    case SDR_NORMAL: return f(std::integral_constant<int, SDR_NORMAL>{});
+    case SDR_RANDINT: return f(std::integral_constant<int, SDR_RANDINT>{});
+    case SDR_BERNOULLI: return f(std::integral_constant<int, SDR_BERNOULLI>{});
+    default: return SDR_E_DIST;
+  }
+}
+
+int transform(const uint32_t* w0, const uint32_t* w1, int64_t n, const sdr_dist& dist, void* out,
+              int dt, cudaStream_t s) {
+  if (n < 0) return SDR_E_INVALID;
+  if (dtype_size(dt) == 0) return SDR_E_DTYPE;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DistP P;
+  const int st = fill_dist_params(dist, dt, P, dev);
+  if (st != SDR_OK) return st;
+  if (n == 0) return SDR_OK;
+  if (w0 == nullptr || w1 == nullptr || out == nullptr) return SDR_E_INVALID;
+  return with_dist(dist.kind, [&](auto dk) {
+    constexpr int DIST = decltype(dk)::value;
+    return with_dtype<DIST>(dt, [&](auto dtc) {
+      constexpr int DT = decltype(dtc)::value;
+      const int grid = grid_for(k_transform<DIST, DT>, static_cast<uint64_t>(n), 256);
+      k_transform<DIST, DT><<<grid, 256, 0, s>>>(w0, w1, n, P, out);
+      return check_launch();
+    });
+  });
 }
 
 int philox_blocks(const uint64_t* tau, const uint64_t* beta, int64_t n, uint64_t seed,

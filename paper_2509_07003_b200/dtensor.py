@@ -402,8 +402,8 @@ def _fused_gather(mesh, md, items, ledger, mover):
         send = torch.empty(seg, dtype=torch.uint8, device=dev)
         recv = torch.empty(seg * P, dtype=torch.uint8, device=dev)
         mover.pack_local(sm, send)
-        pipe.collective(lambda r=recv, s_=send: comm.all_gather_into(
-            r, s_, group, ledger, mesh.name, mesh.dim_names[md], P), (send, recv),
+        pipe.collective(lambda r=recv, s_=send, nb=_real_bytes(rm): comm.all_gather_into(
+            r, s_, group, ledger, mesh.name, mesh.dim_names[md], P, nbytes=nb), (send, recv),
             lambda r=recv, rm_=rm, sg=seg: mover.unpack_gathered(rm_, r, sg, P))
     pipe.drain()
     for (x, slot), full in zip(items, outs):
@@ -461,13 +461,20 @@ def _fused_reduce_scatter(mesh, md, items, ledger, mover):
         packed = torch.empty(seg * P // es, dtype=dt, device=dev)
         mover.pack_scatter(fm, packed.view(torch.uint8), seg, P)
         piece_buf = torch.empty(seg // es, dtype=dt, device=dev)
-        pipe.collective(lambda o=piece_buf, i=packed: comm.reduce_scatter_into(
-            o, i, group, ledger, mesh.name, mesh.dim_names[md], P), (packed, piece_buf),
+        pipe.collective(lambda o=piece_buf, i=packed, nb=_real_bytes(fm): comm.reduce_scatter_into(
+            o, i, group, ledger, mesh.name, mesh.dim_names[md], P, nbytes=nb), (packed, piece_buf),
             lambda pb=piece_buf, pm_=pm: mover.unpack_local(pm_, pb.view(torch.uint8)))
     pipe.drain()
     for (x, slot, dst_p), out in zip(items, outs):
         slot[0] = slot[0].with_placement(md, dst_p)
         slot[1] = out
+
+
+def _real_bytes(members) -> int:
+    """Ledger payload of a coalesced call: the members' own bytes (what the
+    reference's per-tensor collectives record, comm.py:91-125), without the
+    ceil-block padding and alignment gaps of the packed layout."""
+    return sum(m.tensor.numel() * m.tensor.element_size() for m in members)
 
 
 def _padded_bytes(members) -> list[int]:
@@ -492,7 +499,7 @@ def _peer_gather(group, fiber, dev, send_members, recv_members, ledger, mesh, md
             b.seg_off = a.seg_off
         hp.all_gather(sm, rm, seg)
         if ledger is not None:
-            ledger.record("all_gather", seg * P, P, mesh.name, mesh.dim_names[md])
+            ledger.record("all_gather", _real_bytes(rm), P, mesh.name, mesh.dim_names[md])
     return True
 
 
@@ -516,7 +523,7 @@ def _peer_reduce_scatter(group, fiber, t, full_members, piece_members, ledger, m
             q.seg_off = f.seg_off
         hp.reduce_scatter(fm, pm, seg, t.dtype)
         if ledger is not None:
-            ledger.record("reduce_scatter", seg * P, P, mesh.name, mesh.dim_names[md])
+            ledger.record("reduce_scatter", _real_bytes(fm), P, mesh.name, mesh.dim_names[md])
     return True
 
 
@@ -531,11 +538,13 @@ def _piece_shape(shp, dst_p, E, P, k):
     return out
 
 
-def _fused_all_reduce(mesh, dims, items, ledger, mover):
+def _fused_all_reduce(mesh, dims, items, ledger, mover, ledger_mesh=None):
     """items: (x, [spec, local]); one all-reduce over the fiber spanned by
     `dims` (one dim, or several flattened -- N-d fusion) of all locals packed
     back to back.  Replaces each slot's local with a new reduced tensor (the
-    inputs are never modified)."""
+    inputs are never modified).  The ledger records the members' bytes under
+    `ledger_mesh` (the flattened mesh's name for N-d fusion, comm.py:270)."""
+    ledger_mesh = mesh.name if ledger_mesh is None else ledger_mesh
     P = math.prod(mesh.sizes[d] for d in dims)
     if P == 1:
         for _, slot in items:
@@ -557,10 +566,11 @@ def _fused_all_reduce(mesh, dims, items, ledger, mover):
         if max(sizes, default=0) <= cap:
             outs = [torch.empty_like(m.tensor) for m in members]
             for idx in _buckets(sizes, cap=cap):
-                ok = hp.all_reduce([members[i].tensor for i in idx], [outs[i] for i in idx])
-                assert ok, "peer all-reduce bucket does not fit the heap half"
+                if not hp.all_reduce([members[i].tensor for i in idx], [outs[i] for i in idx]):
+                    # every rank computes the same sizes, so all ranks fail here together
+                    raise RuntimeError("peer all-reduce bucket does not fit the heap half")
             if ledger is not None:
-                ledger.record("all_reduce", seg, P, mesh.name,
+                ledger.record("all_reduce", _real_bytes(members), P, ledger_mesh,
                               "+".join(mesh.dim_names[d] for d in dims))
             for (_, slot), o in zip(items, outs):
                 slot[1] = o
@@ -569,7 +579,8 @@ def _fused_all_reduce(mesh, dims, items, ledger, mover):
     es = items[0][1][1].element_size()
     buf = torch.empty(seg // es, dtype=dt, device=items[0][1][1].device)  # gaps never read
     mover.pack_local(members, buf.view(torch.uint8))
-    comm.all_reduce_into(buf, group, ledger, mesh.name, "+".join(mesh.dim_names[d] for d in dims), P)
+    comm.all_reduce_into(buf, group, ledger, ledger_mesh, "+".join(mesh.dim_names[d] for d in dims), P,
+                         nbytes=_real_bytes(members))
     outs = [Member(torch.empty_like(m.tensor), 1, 1, m.inner, 1, m.seg_off) for m in members]
     mover.unpack_local(outs, buf.view(torch.uint8))
     for (_, slot), o in zip(items, outs):

@@ -25,8 +25,8 @@ import torch
 
 from . import _lib
 from .placement import ShardSpec, full_view, local_shape_and_offset
-from .rng import Distribution, RngState, _TORCH_OF_CODE, _device, _param_error, dtype_code, \
-    ensure_normal_tables
+from .rng import Distribution, RngState, _TORCH_OF_CODE, _device, _note_allocation, _param_error, \
+    dtype_code, ensure_normal_tables
 
 
 @dataclass
@@ -123,6 +123,8 @@ def materialize(params, state: RngState, init_specs: dict | None = None, coord=N
     with torch.cuda.device(dev):
         st = _lib.LIB.sdr_fill_batch(outs, dts, dists, rngs, views, n, _lib.stream_handle(dev))
     _lib.check(st, "sdr_fill_batch", _param_error)
+    for t in result.values():  # one fill per parameter, as the sequential walk records (rng.py:204)
+        _note_allocation(t.numel())
     state.offset = offset
     for name, p in todo:
         p.value = result[name]

@@ -33,6 +33,23 @@ def _check_p(status):
     return None
 
 
+def _check_buffer(name: str, buf, x: torch.Tensor, dtypes: tuple):
+    """A caller-supplied output/mask buffer the kernel writes through a raw
+    pointer: it must match x's shape and device, be contiguous, and have one
+    of `dtypes` -- anything else would be a silent wrong or out-of-bounds
+    write."""
+    if not isinstance(buf, torch.Tensor):
+        raise TypeError(f"`{name}` must be a torch.Tensor, got {type(buf).__name__}")
+    if buf.dtype not in dtypes:
+        raise TypeError(f"`{name}` has dtype {buf.dtype}, expected one of {dtypes}")
+    if tuple(buf.shape) != tuple(x.shape):
+        raise ValueError(f"`{name}` has shape {tuple(buf.shape)}, x has {tuple(x.shape)}")
+    if buf.device != x.device:
+        raise ValueError(f"`{name}` is on {buf.device}, x is on {x.device}")
+    if not buf.is_contiguous():
+        raise ValueError(f"`{name}` must be contiguous")
+
+
 def dropout_apply(x: torch.Tensor, p: float, state: RngState, view: ShardView | None = None, *,
                   out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None,
                   mask: torch.Tensor | None = None) -> torch.Tensor:
@@ -54,12 +71,15 @@ def dropout_apply(x: torch.Tensor, p: float, state: RngState, view: ShardView | 
         raise ValueError(f"x has shape {tuple(x.shape)}, window is {view.local_shape}")
     x = x.contiguous()
     yd = x.dtype if out_dtype is None else out_dtype
+    if yd != x.dtype and not (x.dtype == torch.bfloat16 and yd == torch.float32):
+        raise TypeError(f"dropout of {x.dtype} produces {x.dtype} (or float32 for bfloat16), not {yd}")
     if out is None:
         out = torch.empty(x.shape, dtype=yd, device=x.device)
+    else:
+        _check_buffer("out", out, x, (yd,))
     mcode = -1
     if mask is not None:
-        if mask.shape != x.shape or not mask.is_contiguous():
-            raise ValueError("mask must be contiguous with x's shape")
+        _check_buffer("mask", mask, x, (torch.uint8, torch.bool, x.dtype))
         mcode = dtype_code(mask.dtype)
     if x.numel() == 0:
         return out
@@ -303,6 +323,8 @@ def dropout_host(x_host: torch.Tensor, p: float, state: RngState, view: ShardVie
     yd = x_host.dtype if out_dtype is None else out_dtype
     if out is None:
         out = torch.empty(x_host.shape, dtype=yd, pin_memory=True)
+    else:
+        _check_buffer("out", out, x_host, (yd,))
     x_host = x_host.contiguous()
     if x_host.dim() == 0:
         blocks = [((), view)]

@@ -36,7 +36,10 @@ from . import _lib
 
 _HEAPS: dict = {}
 STATS = {"all_gather": 0, "reduce_scatter": 0, "all_reduce": 0}  # pull launches of this process
-_TIMEOUT_NS = int(float(os.environ.get("SDR_PEER_TIMEOUT_S", "30")) * 1e9)
+# A rank legitimately far behind its peers (checkpointing, eval, a one-time
+# compile) must not trip the device barrier's trap: default to NCCL's own
+# 10-minute collective timeout.
+_TIMEOUT_NS = int(float(os.environ.get("SDR_PEER_TIMEOUT_S", "600")) * 1e9)
 
 
 def transport() -> str:
@@ -64,6 +67,7 @@ class PeerHeap:
         self.epoch = 0
         self.calls = 0
         self.ok = False
+        self._stream = None  # stream of the last call (see _order)
         self.bases: list = [None] * self.P
         total = _lib.PEER_FLAG_BYTES + 2 * self.half
         base, h = C.c_void_p(), _lib.SdrIpcHandle()
@@ -103,6 +107,20 @@ class PeerHeap:
             self.bases = [None] * self.P
         self._flags = (C.c_void_p * self.P)(*self.bases) if self.ok else None
 
+    def _order(self):
+        """All work on the heap must run in call order: the one-barrier-per-call
+        argument (a rank reaches barrier k+1 only after its pull of call k)
+        and the monotone epochs rely on it.  Calls on one stream are ordered by
+        the stream; when a call arrives on a different stream than the last
+        one, it first waits for everything queued on that stream so far
+        (which includes the last pull)."""
+        s = torch.cuda.current_stream(self.dev)
+        if self._stream is not None and self._stream != s:
+            ev = torch.cuda.Event()
+            ev.record(self._stream)
+            s.wait_event(ev)
+        self._stream = s
+
     def _half_ptrs(self, h: int):
         off = _lib.PEER_FLAG_BYTES + h * self.half
         return (C.c_void_p * self.P)(*[b + off for b in self.bases])
@@ -124,6 +142,7 @@ class PeerHeap:
         from .movers import CudaMover
         if seg_bytes > self.half:
             raise ValueError("bucket larger than the peer heap half")
+        self._order()
         h = self._next_half()
         segs = self._half_ptrs(h)
         arr = CudaMover._arr(send_members)
@@ -143,6 +162,7 @@ class PeerHeap:
         from .movers import CudaMover
         if seg_bytes * self.P > self.half:
             raise ValueError("bucket larger than the peer heap half")
+        self._order()
         h = self._next_half()
         bufs = self._half_ptrs(h)
         arr = CudaMover._arr(full_members)
@@ -170,6 +190,7 @@ class PeerHeap:
         seg = layout(full)
         if seg * (P + 1) > self.half:
             return False
+        self._order()
         res = [Member(o, 1, o.numel(), 1, m.chunk, m.seg_off) for o, m in zip(outs, full)]
         h = self._next_half()
         bufs = self._half_ptrs(h)

@@ -410,7 +410,45 @@ def backend_block(seed: int, tau_virtual: int, beta_virtual: int) -> tuple[int, 
     return tuple(int(x) for x in w[0].tolist())
 
 
-def transform_words(dist: Distribution, words, dtype=np.float64) -> torch.Tensor:
-    """Not available: the distribution transforms are fused into the fill
-    kernels (there is no standalone words -> values path)."""
-    raise NotImplementedError("transforms are fused into sdr_fill; use fill_random")
+def _words_tensor(w, dev) -> torch.Tensor:
+    """uint32 Philox words (NumPy array, Python ints or a torch tensor holding
+    the uint32 values) as a contiguous int32 CUDA tensor of the same bits."""
+    if isinstance(w, torch.Tensor):
+        if w.dtype in (torch.int32, torch.uint32):
+            t = w.view(torch.int32) if w.dtype == torch.uint32 else w
+        else:  # wrap the uint32 value into int32 two's complement explicitly
+            t = w.to(torch.int64) & 0xFFFFFFFF
+            t = (t - (t >= 2 ** 31).to(torch.int64) * 2 ** 32).to(torch.int32)
+        return t.to(device=dev).contiguous()
+    a = np.ascontiguousarray(np.asarray(w, dtype=np.uint32))
+    return torch.from_numpy(a.view(np.int32).copy()).to(dev)
+
+
+def transform_words(dist: Distribution, words, dtype=np.float64, *, device=None) -> torch.Tensor:
+    """Distribution.transform (reference rng.py:104-182): the values of `dist`
+    for Philox blocks given by their words, computed on the GPU by the same
+    device transform the fill kernels use (sdr_transform).  `words` is the
+    reference's 4-tuple (w0, w1, w2, w3) of uint32 arrays (NumPy or torch);
+    words 2-3 are never read.  The result has w0's shape and the dtype the
+    reference returns (e.g. float64 for Uniform01 of a non-float32 dtype)."""
+    if not isinstance(dist, Distribution) or type(dist).native is Distribution.native:
+        raise TypeError(f"{type(dist).__name__} has no sm_100a kernel (no CPU fallback)")
+    if len(words) != 4:
+        raise ValueError(f"expected the 4 words of a Philox block, got {len(words)}")
+    dev = _device(device)
+    w0, w1 = _words_tensor(words[0], dev), _words_tensor(words[1], dev)
+    if tuple(w0.shape) != tuple(w1.shape):
+        raise ValueError(f"word arrays differ in shape: {tuple(w0.shape)} vs {tuple(w1.shape)}")
+    code = dist.out_code(dtype_code(dtype))
+    out = torch.empty(w0.shape, dtype=_TORCH_OF_CODE[code], device=dev)
+    if dist.kind == _lib.NORMAL:
+        with torch.cuda.device(dev):
+            ensure_normal_tables(dev)
+    nd = dist.native()
+    n = w0.numel()
+    with torch.cuda.device(dev):
+        st = _lib.LIB.sdr_transform(w0.data_ptr() if n else None, w1.data_ptr() if n else None, n,
+                                    C.byref(nd), out.data_ptr() if n else None, code,
+                                    _lib.stream_handle(dev))
+    _lib.check(st, "sdr_transform", _param_error)
+    return out

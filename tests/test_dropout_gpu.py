@@ -234,3 +234,30 @@ def test_dropout_host_async_back_to_back():
     for i, o in enumerate(outs):
         want = ops.dropout_apply(x.cuda(), p, R.RngState(31, i)).cpu()
         assert torch.equal(bits(o), bits(want)), i
+
+
+def test_dropout_apply_rejects_bad_buffers():
+    """A wrong `out` or `mask` must raise, never reach the kernel (a short or
+    wrong-dtype buffer would be an out-of-bounds or wrong write)."""
+    x = torch.randn(8, 64, device="cuda").to(torch.bfloat16)
+    st = R.RngState(3)
+    good = ops.dropout_apply(x, 0.1, st)
+    for bad, exc in [(torch.empty(8, 64, device="cuda", dtype=torch.float16), TypeError),
+                     (torch.empty(8, 63, device="cuda", dtype=torch.bfloat16), ValueError),
+                     (torch.empty(64, 8, device="cuda", dtype=torch.bfloat16).t(), ValueError),
+                     (torch.empty(8, 64, dtype=torch.bfloat16), ValueError)]:
+        with pytest.raises(exc):
+            ops.dropout_apply(x, 0.1, st, out=bad)
+    for bad, exc in [(torch.empty(8, 64, dtype=torch.uint8), ValueError),        # host mask
+                     (torch.empty(8, 32, device="cuda", dtype=torch.uint8), ValueError),
+                     (torch.empty(8, 64, device="cuda", dtype=torch.int32), TypeError)]:
+        with pytest.raises(exc):
+            ops.dropout_apply(x, 0.1, st, mask=bad)
+    with pytest.raises(TypeError):
+        ops.dropout_apply(x, 0.1, st, out_dtype=torch.float16)
+    y = torch.empty_like(x)
+    m = torch.empty(8, 64, device="cuda", dtype=torch.bool)
+    ops.dropout_apply(x, 0.1, st, out=y, mask=m)
+    assert torch.equal(bits(y), bits(good))
+    nz = x != 0
+    assert torch.equal(m[nz], (good != 0)[nz])

@@ -284,3 +284,71 @@ def test_peer_transport_selection(monkeypatch):
     monkeypatch.setenv("SDR_TRANSPORT", "nccl")
     assert peer.heap_for(object(), [0, 1], torch.device("cuda", 0)) is None
     assert peer.reducible(torch.bfloat16) and not peer.reducible(torch.bool)
+
+
+def test_dropout_buffer_validation():
+    """ops._check_buffer guards every caller-supplied buffer the dropout kernel
+    writes through a raw pointer (wrong dtype -> TypeError; shape, device or
+    layout -> ValueError), as fill_random does for `out`."""
+    import torch
+    from paper_2509_07003_b200.ops import _check_buffer
+    x = torch.zeros(4, 6, dtype=torch.bfloat16)
+    _check_buffer("out", torch.empty(4, 6, dtype=torch.bfloat16), x, (torch.bfloat16,))
+    with pytest.raises(TypeError):
+        _check_buffer("out", torch.empty(4, 6, dtype=torch.float16), x, (torch.bfloat16,))
+    with pytest.raises(TypeError):
+        _check_buffer("mask", [0] * 24, x, (torch.uint8,))
+    with pytest.raises(ValueError):
+        _check_buffer("out", torch.empty(4, 5, dtype=torch.bfloat16), x, (torch.bfloat16,))
+    with pytest.raises(ValueError):
+        _check_buffer("out", torch.empty(6, 4, dtype=torch.bfloat16).t(), x, (torch.bfloat16,))
+    with pytest.raises(ValueError):
+        _check_buffer("mask", torch.empty(4, 6, dtype=torch.uint8, device="meta"), x, (torch.uint8,))
+
+
+def test_cost_model_matches_reference():
+    """comm.cost_model_eval against the reference's pinned values
+    (test_comm.py:157-175, test_acceptance.py:289-318): T_v = 2SB sum (P_i-1)/P_i,
+    T_f = 2SB (prod P - 1)/prod P; 4/3 at (2,2), 1.778 at (8,8)."""
+    from fractions import Fraction
+    from paper_2509_07003_b200.comm import CommError, CostParams, cost_model_eval
+    tv, tf, r = cost_model_eval(CostParams(1000, Fraction(1, 100), (2, 2)))
+    assert (tv, tf, r) == (Fraction(20), Fraction(15), Fraction(4, 3))
+    _, _, r88 = cost_model_eval(CostParams(1 << 20, Fraction(1), (8, 8)))
+    assert r88 == Fraction(7 * 2 * 64, 8 * 63) and abs(float(r88) - 1.778) < 1e-3
+    assert cost_model_eval(CostParams(8, Fraction(1), (4,)))[2] == 1  # one dim: nothing to fuse
+    for p in [(2,), (2, 2), (2, 4), (8, 8), (2, 2, 2)]:  # fusing never costs more
+        tv, tf, r = cost_model_eval(CostParams(64, Fraction(3), p))
+        assert tf <= tv and r >= 1
+    with pytest.raises(CommError):
+        CostParams(0, Fraction(1), (2,))
+    with pytest.raises(CommError):
+        CostParams(8, Fraction(1), ())
+    with pytest.raises(CommError):
+        CostParams(8, Fraction(1), (0, 2))
+
+
+def test_cost_model_ac07_and_ledger_bytes():
+    """Reference acceptance ac07 (test_acceptance.py:289-318): exact rational
+    formulas, ratio -> N at P_i = 2^10, ledger 2S(P-1)/P per device; plus
+    test_comm.py:167-172 (fused == vanilla iff one dim)."""
+    import math
+    from fractions import Fraction
+    from paper_2509_07003_b200.comm import CostParams, all_reduce, cost_model_eval
+    from paper_2509_07003_b200.ledger import CollectiveLedger
+    B = Fraction(1, 10 ** 9)
+    for N in (1, 2, 3):
+        for counts in itertools.product((2, 4, 8, 16), repeat=N):
+            tv, tf, ratio = cost_model_eval(CostParams(4096, B, counts))
+            ev = 2 * 4096 * B * sum(Fraction(p - 1, p) for p in counts)
+            prod = math.prod(counts)
+            ef = 2 * 4096 * B * Fraction(prod - 1, prod)
+            assert (tv, tf, ratio) == (ev, ef, ev / ef)
+            assert (tf == tv) == (N == 1)
+        _, _, ratio = cost_model_eval(CostParams(1, B, tuple([1 << 10] * N)))
+        assert abs(float(ratio) - N) / N <= 1e-3
+    import torch
+    for P in (2, 4, 8, 16):
+        ledger = CollectiveLedger()
+        all_reduce([torch.zeros(128, dtype=torch.float64) for _ in range(P)], ledger)
+        assert ledger.entries[0].bytes_per_device == Fraction(2 * 1024 * (P - 1), P)

@@ -267,3 +267,30 @@ def test_parameter_materialize_global_and_sharded():
         v = local_shape_and_offset(spec, (257, 64), coord)
         sl = tuple(slice(o, o + n) for o, n in zip(v.local_offset, v.local_shape))
         assert torch.equal(bits(d.local), bits(full[sl])) and ss.offset == sg.offset
+
+
+def test_deferred_init_allocates_shard_sized_buffers():
+    """Port of the reference's test_plan.py:124-139 onto init.materialize (the
+    one-launch deferred init): with fc1.weight S(1) and fc2.weight S(0) on a
+    4-rank tp mesh, every fill is shard-sized, and the merged shards equal the
+    eager single-device init bitwise."""
+    mesh = S.create_mesh([("tp", 4)])
+    # MLP(16, 32, 8) of the reference: fc1 [16, 32], fc2 [32, 8], scaled-normal init (model.py:140-160)
+    def params():
+        return {"fc1.weight": I.Parameter((16, 32), R.Normal(0.0, 16 ** -0.5), np.float64),
+                "fc2.weight": I.Parameter((32, 8), R.Normal(0.0, 32 ** -0.5), np.float64)}
+    specs = {"fc1.weight": ShardSpec(mesh, parse_placements("S(1)")),
+             "fc2.weight": ShardSpec(mesh, parse_placements("S(0)"))}
+    shards = {}
+    for coord in mesh.iter_coords():
+        with R.track_allocations() as alloc:
+            shards[coord] = I.materialize(params(), R.RngState(7), specs, coord)
+        assert 0 < alloc["max_elements"] <= 16 * 32 // 4
+    ref = params()
+    with R.track_allocations() as alloc:
+        I.materialize(ref, R.RngState(7))
+    assert alloc["max_elements"] == 16 * 32  # the eager path fills whole tensors
+    fc1 = torch.cat([shards[(k,)]["fc1.weight"] for k in range(4)], dim=1)
+    fc2 = torch.cat([shards[(k,)]["fc2.weight"] for k in range(4)], dim=0)
+    assert torch.equal(bits(fc1), bits(ref["fc1.weight"].value))
+    assert torch.equal(bits(fc2), bits(ref["fc2.weight"].value))

@@ -424,3 +424,47 @@ def _worker_golden_cpu_peer(rank, ws, mesh_sizes, initial_half):
 def test_peer_transport_host_logic_cpu(mesh_sizes, initial_half):
     _spawn(_worker_golden_cpu_peer, int(np.prod(mesh_sizes)), mesh_sizes, initial_half)
 
+
+
+def _worker_uneven_rounds(rank, ws):
+    """Bucket boundaries come from local_nbytes_max (the largest shard over the
+    mesh, reference comm.py:140-150), so every rank cuts the same buckets even
+    when its own shard is smaller: (5,4) f64 under (P, S(0)) on 2x2 gives
+    shards of 96 B (tp=0) and 64 B (tp=1); two grads at 128 B per bucket make
+    2 buckets on EVERY rank (local bytes would give 1 on the tp=1 ranks).
+    The ledger records real (unpadded) member bytes, and the N-d fused reduce
+    records the flattened mesh's name (comm.py:270)."""
+    from cpu_mover import TorchCpuMover
+    from paper_2509_07003_b200 import comm, create_mesh
+    from paper_2509_07003_b200.dtensor import from_local
+    from paper_2509_07003_b200.placement import ShardSpec, local_shape_and_offset, parse_placements
+    mover = TorchCpuMover()
+    mesh = create_mesh([("dp", 2), ("tp", 2)])
+    coord = mesh.coords_of_rank(rank)
+    spec = ShardSpec(mesh, parse_placements("P,S(0)"))
+    v = local_shape_and_offset(spec, (5, 4), coord)
+    grads = [from_local(torch.full(v.local_shape, float(rank + 10 * i), dtype=torch.float64), spec,
+                        (5, 4), coord) for i in range(2)]
+    assert grads[0].local_nbytes_max() == 96
+    ledger = comm.CollectiveLedger()
+    out, rep = comm.bucketed_grad_reduce(grads, bucket_bytes=128, ledger=ledger, mover=mover)
+    assert len(rep["rounds"]) == 2, rep["rounds"]
+    dp_peer = mesh.coords_of_rank(rank)
+    other = [r for r in range(ws) if mesh.coords_of_rank(r)[1] == dp_peer[1]]
+    for i, o in enumerate(out):
+        assert torch.equal(o.local, torch.full(v.local_shape, float(sum(other) + 20 * i), dtype=torch.float64))
+    assert [e.payload_bytes for e in ledger.entries] == [v.local_shape[0] * 4 * 8] * 2
+    # N-d fusion: the ledger names the flattened mesh and counts unpadded bytes
+    spec2 = ShardSpec(mesh, parse_placements("P,P"))
+    g2 = [from_local(torch.ones(3, dtype=torch.float32) * rank, spec2, (3,), coord),
+          from_local(torch.ones(5, dtype=torch.float32), spec2, (5,), coord)]
+    l2 = comm.CollectiveLedger()
+    out2, rep2 = comm.fused_nd_grad_reduce(g2, bucket_bytes=1 << 20, ledger=l2, mover=mover)
+    flat = mesh.flatten_dims(["dp", "tp"])
+    assert [(e.mesh, e.payload_bytes, e.participants) for e in l2.entries] == [(flat.name, 32, 4)]
+    assert rep2["rounds"] == [("all_reduce", flat.name, ("dp", "tp"))]
+    assert torch.equal(out2[0].local, torch.full((3,), 6.0)) and torch.equal(out2[1].local, torch.full((5,), 4.0))
+
+
+def test_grad_buckets_use_local_nbytes_max_uneven_gloo():
+    _spawn(_worker_uneven_rounds, 4)

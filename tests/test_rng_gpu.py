@@ -355,3 +355,58 @@ def test_randomized_windows_match_oracle():
         ref = O.fill_sharded(shape, _oracle_pl(spec), msizes, seed, off, theta, kind, params, _np_dt(dt))
         for coord, t in locs.items():
             assert _same(t, _oracle_tensor(ref[coord])), (case, shape, pls, msizes, kind, dt, theta, coord)
+
+
+@pytest.mark.parametrize("kind,params,dt", CASES + [("uniform01", (), "bfloat16"),
+                                                     ("bernoulli", (1.0,), "bool"),
+                                                     ("bernoulli", (0.0,), "int64")])
+def test_distribution_transform_plugin_matches_oracle(kind, params, dt):
+    """Distribution.transform(words, dtype) -- the reference's distribution
+    plug-in point (rng.py:104-182) -- on the GPU (sdr_transform) equals the
+    oracle's transform of the same words bit for bit, and equals fill_random
+    over the indices the words were drawn for."""
+    rs = np.random.default_rng(abs(hash((kind, dt))) % (1 << 32))
+    n = 1 << 17
+    tau = rs.integers(0, 1 << 40, n, dtype=np.uint64)
+    beta = rs.integers(0, 1 << 62, n, dtype=np.uint64)
+    words = O.blocks(0xC0FFEE, tau, beta)  # (4, n) uint32
+    want = O.transform(kind, params, words, _np_dt(dt))
+    got = _dist(kind, params).transform(tuple(words), _np_dt(dt))
+    assert got.is_cuda and got.shape == (n,)
+    assert _same(got, _oracle_tensor(want)), (kind, params, dt)
+    # torch word tensors (device, int64 holding uint32) give the same values
+    tw = tuple(torch.from_numpy(w.astype(np.int64)).cuda() for w in words)
+    assert _same(_dist(kind, params).transform(tw, _np_dt(dt)), _oracle_tensor(want))
+    # transform(blocks of the window's counters) == fill_random of the window
+    st = R.RngState(99, 12345, 64)
+    shape = (37, 48)
+    j = np.arange(np.prod(shape), dtype=np.uint64)
+    w2 = O.blocks(99, j % np.uint64(64), j // np.uint64(64) + np.uint64(12345))
+    via_words = _dist(kind, params).transform(tuple(w2), _np_dt(dt)).reshape(shape)
+    via_fill = R.fill_random(full_view(shape), st, _dist(kind, params), _np_dt(dt))
+    assert torch.equal(bits(via_words), bits(via_fill))
+
+
+def test_distribution_transform_errors():
+    words = tuple(np.zeros(4, dtype=np.uint32) for _ in range(4))
+    with pytest.raises(TypeError):
+        R.RandInt(0, 5).transform(words, "bfloat16")   # no bf16 randint in the reference's dtypes
+    with pytest.raises(ValueError):
+        R.Normal().transform(words[:2], np.float32)      # the reference unpacks 4 words
+
+    class Custom(R.Distribution):
+        pass
+
+    with pytest.raises(TypeError):
+        Custom().transform(words, np.float32)            # no kernel, no CPU fallback
+    assert R.Uniform01().transform(tuple(np.zeros(0, dtype=np.uint32) for _ in range(4)),
+                                   np.float32).numel() == 0
+
+
+def test_allocation_tracking_is_local_sized():
+    """Port of the reference's test_rng.py:124-129."""
+    mesh = S.create_mesh([("x", 4)])
+    spec = ShardSpec(mesh, parse_placements("S(0)"))
+    with R.track_allocations() as alloc:
+        R.generate_distributed(spec, (64, 64), R.RngState(0), R.Uniform01())
+    assert 0 < alloc["max_elements"] <= 64 * 64 // 4
