@@ -106,6 +106,61 @@ def cpu_measure(n_elems: int, cores: int, piece_rows: int = 2048):
     return elems / secs, secs, elems
 
 
+def cpu_info() -> dict:
+    """Host CPU model, usable cores and NumPy's SIMD dispatch (BASELINE.md
+    section 2 asks for them next to every CPU number)."""
+    import numpy as np
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    simd = {}
+    try:
+        from numpy._core._multiarray_umath import __cpu_baseline__, __cpu_dispatch__, __cpu_features__
+        simd = {"baseline": list(__cpu_baseline__),
+                "dispatch_found": [f for f in __cpu_dispatch__ if __cpu_features__.get(f)]}
+    except ImportError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(),
+            "affinity": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None,
+            "numpy": np.__version__, "numpy_simd": simd}
+
+
+def parity_check(y, x, view, seed: int, offset: int, n_rows: int = 256) -> dict:
+    """Checker for the timed output: `n_rows` rows of 4096 elements spread over
+    this rank's shard (every batch, sequence positions spread across the shard)
+    of the LAST timed step's y, against the oracle restatement of
+    rng.py:185-242 + engine.py:80-81 (the reference's f32 result, rounded to
+    bf16).  The oracle is only the checker here."""
+    import ml_dtypes
+    import numpy as np
+    import torch
+    from oracle import rng_oracle as O
+    B, n, W = view.local_shape
+    s0 = view.local_offset[1]
+    per_b = max(1, n_rows // B)
+    rows = [(b, int(s)) for b in range(B) for s in np.linspace(0, n - 1, min(per_b, n)).round()]
+    bi = torch.tensor([r[0] for r in rows], device=y.device)
+    si = torch.tensor([r[1] for r in rows], device=y.device)
+    ys = y[bi, si].cpu().view(torch.int16).numpy().view(np.uint16)
+    xs = x[bi, si].cpu().view(torch.int16).numpy().view(np.uint16).view(ml_dtypes.bfloat16)
+    rb = np.array([r[0] for r in rows], dtype=np.int64)
+    rs = np.array([r[1] for r in rows], dtype=np.int64)
+    j = (((rb * SHAPE[1] + s0 + rs) * SHAPE[2])[:, None] + np.arange(W, dtype=np.int64)[None, :]).reshape(-1)
+    keep = O.fill_indices(j, seed, offset, 65536, "bernoulli", (1.0 - P_DROP,), ml_dtypes.bfloat16)
+    ref = O.dropout_apply(xs.reshape(-1), keep, P_DROP).astype(ml_dtypes.bfloat16).view(np.uint16)
+    bad = int(np.count_nonzero(ref != ys.reshape(-1)))
+    return {"checked": int(ref.size), "mismatches": bad,
+            "what": f"{len(rows)} rows x {W} of the last timed step's y (all batches, sequence rows "
+                    f"spread over the shard) vs oracle/rng_oracle.py (rng.py:185-242 + engine.py:80-81) "
+                    f"rounded to bf16"}
+
+
 def run_reference(a):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -132,7 +187,8 @@ def run_reference(a):
                    "parallelism": f"sp{ws}"},
         "cpu_baseline": {"value": round(gbs, 6), "unit": "GB/s", "cores": cores, "kind": "port",
                          "sample": f"{sample} elements per step ({cores} procs x 64 rows x 2 x 4096),"
-                                   " numpy restatement of rng.py + engine.k_dropout_apply"},
+                                   " numpy restatement of rng.py + engine.k_dropout_apply",
+                         "host": cpu_info()},
         "e2e": {"value": round(gbs, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -209,6 +265,9 @@ def run_ours(a):
         if share:
             dist.init_process_group("gloo")
         else:
+            # communicator init lines (rank / nRanks per comm) on stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
 
     from paper_2509_07003_b200 import _lib, create_mesh, ops, rng as R
@@ -241,7 +300,10 @@ def run_ours(a):
     stream = torch.cuda.current_stream(dev)
     state = R.RngState(SEED, 0, 65536)
 
+    last = {}
+
     def step(i):
+        last["i"], last["offset"] = i, state.offset  # which buffer / offset the parity check reads
         ops.dropout_apply(xs[i % nbuf], P_DROP, state, view, out=ys[i % nbuf])
         state.advance(math.prod(SHAPE))  # every rank, no communication (rng.py:95-98)
 
@@ -276,7 +338,8 @@ def run_ours(a):
             dist.barrier()
     ms_local = t0.elapsed_time(t1) / a.steps
     clocks = clk.summary()
-    y = ys[0]
+    # parity of the last timed step's output (every rank checks its own shard)
+    par = parity_check(ys[last["i"] % nbuf], xs[last["i"] % nbuf], view, SEED, last["offset"])
 
     # --- e2e through the public API with host buffers -------------------------
     # Every step copies its input x from pinned host memory to the GPU and its
@@ -322,6 +385,12 @@ def run_ours(a):
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, e2e_ms, e2e_sync_ms = t.tolist()
+    pt = torch.tensor([par["checked"], par["mismatches"]], dtype=torch.int64,
+                      device="cpu" if share else dev)
+    if ws > 1:
+        dist.all_reduce(pt, op=dist.ReduceOp.SUM)
+    par["checked"], par["mismatches"] = (int(v) for v in pt.tolist())
+    par["ranks"] = ws
     total_elems = math.prod(SHAPE)
     gbs = total_elems * BYTES_PER_ELEM / (ms * 1e-3) / 1e9
     e2e_gbs = total_elems * BYTES_PER_ELEM / (e2e_ms * 1e-3) / 1e9
@@ -344,6 +413,13 @@ def run_ours(a):
     # counter word per-thread varying and all four words consumed (nothing to
     # hoist), x 80 INT32 ops per block.
     int_peak_tops = PHILOX_OPS * phx.value / 1e12
+    # Issue ceiling of the fma-heavy pipe: IMAD.WIDE.U32 issues at 32 per SM per
+    # clock (4 cycles per warp per SMSP), a Philox block is
+    # 20 of them -> SMs x 32 x f_max / 20 blocks/s.
+    sm_max_hz = (clocks.get("sm_max_mhz") or 1965.0) * 1e6
+    n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    ceil_blocks = n_sms * 32 * sm_max_hz / 20
+    ceil_tops = PHILOX_OPS * ceil_blocks / 1e12
     achieved_tops = n_local / (ms_local * 1e-3) * PHILOX_OPS / 1e12
     achieved_gbs_local = local_bytes / (ms_local * 1e-3) / 1e9
 
@@ -362,7 +438,7 @@ def run_ours(a):
             sample = 12 * 1024 * SHAPE[2]  # 50 M elements, 1 core, ~15 s of compute
             rate, secs, elems = cpu_measure(sample, 1)
             cpu = {"value": round(rate * BYTES_PER_ELEM / 1e9, 6), "unit": "GB/s", "cores": 1,
-                   "kind": "port",
+                   "kind": "port", "host": cpu_info(),
                    "sample": f"{elems} elements (rows 0-12287 x 4096 of batch 0, 6 pieces), numpy "
                              f"restatement of rng.py:185-242 + engine.py:80-81, {secs:.1f}s of compute"}
         line = {
@@ -385,7 +461,11 @@ def run_ours(a):
                                                     "algorithmic bytes per launch = %d" % local_bytes,
                 "int32_probe": {"imad_wide_per_s": imad.value, "lop3_per_s": lop3.value,
                                 "philox_blocks_per_s_no_hoist": phx.value,
-                                "how": "sdr_probe_int32 live: peak = 80 x philox_blocks_per_s_no_hoist"},
+                                "how": "sdr_probe_int32 live: peak = 80 x philox_blocks_per_s_no_hoist; "
+                                       "imad_wide/lop3 = independent non-foldable chains (probe.cu)"},
+                "pipe_ceiling": {"peak": round(ceil_tops, 3), "frac": round(achieved_tops / ceil_tops, 4),
+                                 "how": f"{n_sms} SMs x 32 IMAD.WIDE/clk x {sm_max_hz / 1e6:.0f} MHz / "
+                                        "20 per block x 80 ops"},
                 "hbm": {"achieved": round(achieved_gbs_local, 1), "peak": hbm_peak, "unit": "GB/s",
                         "frac": round(achieved_gbs_local / hbm_peak, 4), "peak_source": hbm_src},
                 "kernel": "k_dropout_fast<BF16,BF16,-1> (one launch per step)",
@@ -400,13 +480,21 @@ def run_ours(a):
                            "after every step"},
             "gpu_launches": a.steps,
             "clocks": clocks,
+            "parity": par,
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
-        print(json.dumps(line), flush=True)
     if ws > 1:
+        # second north-star target: cfg5 fused redistribute busBW (after the headline timing)
+        from tools.bench_extra import cfg5_redistribute
+        red = cfg5_redistribute(10, 3, dev, ws, rank, share)
+        if rank == 0:
+            line["redistribute"] = red
+            print(json.dumps(line), flush=True)
         dist.barrier()
         dist.destroy_process_group()
+    elif line is not None:
+        print(json.dumps(line), flush=True)
     return line
 
 

@@ -99,13 +99,51 @@ class PeerHeap:
         votes = [None] * self.P
         dist.all_gather_object(votes, bool(reach), group=group)
         self.ok = all(votes)
+        self._flags = (C.c_void_p * self.P)(*self.bases) if self.ok else None
+        if self.ok and os.environ.get("SDR_PEER_SELFCHECK", "1") != "0":
+            # Known-answer check of the whole protocol (pack, barrier, reduce
+            # pull, barrier, gather pull) before any user data uses it; a
+            # mismatch on any rank sends the fiber to NCCL.
+            good = self._self_check()
+            dist.all_gather_object(votes, bool(good), group=group)
+            if not all(votes):
+                import warnings
+                warnings.warn(f"peer transport self-check failed on fiber {fiber}: using NCCL")
+                STATS["selfcheck_failed"] = STATS.get("selfcheck_failed", 0) + 1
+                self.ok = False
         if not self.ok:  # give everything back: this fiber uses NCCL
+            if opened:
+                torch.cuda.synchronize(dev)
             for p in opened:
                 _lib.LIB.sdr_peer_heap_close(p)
+            dist.barrier(group=group)  # every importer closed before the owners free
             _lib.LIB.sdr_peer_heap_free(self.own)
             self.own = None
             self.bases = [None] * self.P
-        self._flags = (C.c_void_p * self.P)(*self.bases) if self.ok else None
+            self._flags = None
+
+    def _self_check(self) -> bool:
+        """All-reduce of rank-specific int32 data (ragged length, so the last
+        rank's chunk is short) through this heap, compared with the sum every
+        rank can compute locally.  Uses a short device-barrier timeout."""
+        per = min(4099, self.half // (self.P + 1) // 4 - 8)  # fits the all-reduce's P+1 segments
+        if per < 2:
+            return True  # heap too small to hold a check; nothing to verify it with
+        n = per * self.P - 1
+        i = torch.arange(n, dtype=torch.int64, device=self.dev)
+        mine = ((i * 2654435761 + 97 * self.rank) % 1000003).to(torch.int32)
+        want = sum(((i * 2654435761 + 97 * q) % 1000003) for q in range(self.P)).to(torch.int32)
+        out = torch.empty_like(mine)
+        global _TIMEOUT_NS
+        saved, _TIMEOUT_NS = _TIMEOUT_NS, min(_TIMEOUT_NS, int(60e9))
+        try:
+            if not self.all_reduce([mine], [out]):
+                return False
+        finally:
+            _TIMEOUT_NS = saved
+        torch.cuda.synchronize(self.dev)
+        STATS["all_reduce"] -= 1  # not a user collective
+        return bool(torch.equal(out, want))
 
     def _order(self):
         """All work on the heap must run in call order: the one-barrier-per-call

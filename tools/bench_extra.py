@@ -213,3 +213,122 @@ def run(a):
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# cfg5 summary for the headline line at WORLD_SIZE > 1 (bench.py).
+# ---------------------------------------------------------------------------
+def cfg5_redistribute(steps: int, warmup: int, dev, ws: int, rank: int, share: bool) -> dict:
+    """One LLaMA-3-8B layer's 9 params on a DP x TP mesh (DP = 2): the fused
+    S->R all-gather over DP (`redistribute_many`) and the fused P->S
+    reduce-scatter of same-shaped grads, each through the peer transport and
+    through NCCL, against per-tensor `redistribute` calls and ONE
+    single-buffer NCCL collective of the same bytes (the busBW ceiling of the
+    >= 80% target).  busBW = S (P-1)/P / t, S = gathered bytes per DP fiber
+    (NCCL-tests convention = the reference ledger's, comm.py:45-62).  Values:
+    params Uniform(-1,1) and integer-valued grads (RandInt, so any summation
+    order is exact) drawn from the parity-tested RNG by global index, so every
+    expected output is computable on each rank: `bit_exact` compares every
+    measured variant's outputs with it, bit for bit."""
+    import math
+    from paper_2509_07003_b200 import create_mesh, peer, rng as R
+    from paper_2509_07003_b200 import dtensor as DT
+    from paper_2509_07003_b200.comm import fiber_group
+    from paper_2509_07003_b200.placement import ShardSpec, local_shape_and_offset, parse_placements
+    if ws % 2:
+        return {"skipped": "odd world size: no DP=2 fiber"}
+    dp, tp = 2, ws // 2
+    mesh = create_mesh([("dp", dp), ("tp", tp)])
+    coord = mesh.coords_of_rank(rank)
+    d, ff, kv = 4096, 14336, 1024
+    layer = {"q": ((d, d), "S(1),S(0)"), "k": ((kv, d), "S(1),S(0)"), "v": ((kv, d), "S(1),S(0)"),
+             "o": ((d, d), "S(0),S(1)"), "gate": ((ff, d), "S(1),S(0)"), "up": ((ff, d), "S(1),S(0)"),
+             "down": ((d, ff), "S(0),S(1)"), "n1": ((d,), "S(0),R"), "n2": ((d,), "S(0),R")}
+    xs, dsts, grads, gdst, exp_ag, exp_rs = [], [], [], [], [], []
+    for i, (name, (shape, pl)) in enumerate(layer.items()):
+        spec = ShardSpec(mesh, parse_placements(pl))
+        dst_pl = ["R"] + [str(p) for p in spec.placements[1:]]
+        dspec = ShardSpec(mesh, parse_placements(",".join(dst_pl)))
+        gspec = ShardSpec(mesh, parse_placements(",".join(["P"] + dst_pl[1:])))
+        st = R.RngState(1000 + i)
+        u = R.Uniform(-1.0, 1.0)
+        xs.append(DT.from_local(R.fill_random(local_shape_and_offset(spec, shape, coord), st, u, "bfloat16",
+                                              device=dev), spec, shape, coord))
+        dsts.append(dspec)
+        exp_ag.append(R.fill_random(local_shape_and_offset(dspec, shape, coord), st, u, "bfloat16", device=dev))
+        # rank-dependent Partial grads: dp index k draws with seed 2000 + 16 i + k
+        ri = R.RandInt(-8, 8)
+        gv = local_shape_and_offset(gspec, shape, coord)
+        g = R.fill_random(gv, R.RngState(2000 + 16 * i + coord[0]), ri, np.float32, device=dev)
+        grads.append(DT.from_local(g.to(torch.bfloat16), gspec, shape, coord))
+        gdst.append(spec)
+        pv = local_shape_and_offset(spec, shape, coord)
+        acc = sum(R.fill_random(pv, R.RngState(2000 + 16 * i + k), ri, np.float32, device=dev)
+                  for k in range(dp))
+        exp_rs.append(acc.to(torch.bfloat16))
+    S = sum(x.numel() * 2 for x in exp_ag)  # gathered bytes per rank (= per DP fiber member)
+    busbw = lambda ms: round(S / ms / 1e6 * (dp - 1) / dp, 2)
+
+    def same(outs, exp):
+        return all(torch.equal(o.to_local().view(torch.int16), e.view(torch.int16)) for o, e in zip(outs, exp))
+
+    env0 = {k: os.environ.get(k) for k in ("SDR_TRANSPORT", "SDR_COMM_CPU_STAGING")}
+    res, exact = {}, {}
+    try:
+        for tname in ("peer", "nccl"):
+            os.environ["SDR_TRANSPORT"] = tname
+            if share and tname == "nccl":
+                os.environ["SDR_COMM_CPU_STAGING"] = "1"  # gloo stand-in: NCCL refuses 2 ranks on 1 GPU
+            n0 = dict(peer.STATS)
+            ag = DT.redistribute_many(xs, dsts)
+            rs = DT.redistribute_many(grads, gdst)
+            torch.cuda.synchronize(dev)
+            exact[f"fused_{tname}"] = bool(same(ag, exp_ag) and same(rs, exp_rs))
+            used_peer = peer.STATS["all_gather"] > n0["all_gather"]
+            if tname == "peer" and not used_peer:
+                res["fused_peer"] = {"unavailable": "peer memory not reachable on this fiber"}
+                continue
+            ms_ag = _time(lambda: DT.redistribute_many(xs, dsts), steps, warmup, dev, ws)
+            ms_rs = _time(lambda: DT.redistribute_many(grads, gdst), steps, warmup, dev, ws)
+            res[f"fused_{tname}"] = {"ag_ms": round(ms_ag, 4), "ag_busbw": busbw(ms_ag),
+                                     "rs_ms": round(ms_rs, 4), "rs_busbw": busbw(ms_rs),
+                                     **({"via": "gloo host staging (ranks share one GPU)"}
+                                        if share and tname == "nccl" else {})}
+        # per-tensor redistribute calls over NCCL (9 collectives per direction)
+        os.environ["SDR_TRANSPORT"] = "nccl"
+        ag1 = [DT.redistribute(x, dd) for x, dd in zip(xs, dsts)]
+        rs1 = [DT.redistribute(g, dd) for g, dd in zip(grads, gdst)]
+        torch.cuda.synchronize(dev)
+        exact["per_tensor_nccl"] = bool(same(ag1, exp_ag) and same(rs1, exp_rs))
+        ms_ag = _time(lambda: [DT.redistribute(x, dd) for x, dd in zip(xs, dsts)], steps, warmup, dev, ws)
+        ms_rs = _time(lambda: [DT.redistribute(g, dd) for g, dd in zip(grads, gdst)], steps, warmup, dev, ws)
+        res["per_tensor_nccl"] = {"ag_ms": round(ms_ag, 4), "ag_busbw": busbw(ms_ag),
+                                  "rs_ms": round(ms_rs, 4), "rs_busbw": busbw(ms_rs)}
+        # one single-buffer collective of the same bytes on the DP fiber group
+        if share:
+            res["single_buffer_nccl"] = {"unavailable": "ranks share one GPU (NCCL: duplicate GPU)"}
+        else:
+            group, _ = fiber_group(mesh, (0,))
+            send = torch.empty(S // dp // 2, dtype=torch.bfloat16, device=dev)
+            recv = torch.empty(S // 2, dtype=torch.bfloat16, device=dev)
+            ms_ag = _time(lambda: dist.all_gather_into_tensor(recv, send, group=group), steps, warmup, dev, ws)
+            ms_rs = _time(lambda: dist.reduce_scatter_tensor(send, recv, group=group), steps, warmup, dev, ws)
+            res["single_buffer_nccl"] = {"ag_ms": round(ms_ag, 4), "ag_busbw": busbw(ms_ag),
+                                         "rs_ms": round(ms_rs, 4), "rs_busbw": busbw(ms_rs)}
+    finally:
+        for k, v in env0.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    out = {"workload": "cfg5: one LLaMA-3-8B layer (9 params), fused S->R all-gather over DP and P->S "
+                       "reduce-scatter of same-shaped grads", "mesh": f"dp{dp}xtp{tp}",
+           "gathered_bytes_per_rank": S, "unit": "GB/s busBW (S (P-1)/P / t)", **res,
+           "bit_exact": exact, "steps": steps}
+    ceil = res.get("single_buffer_nccl", {})
+    for tname in ("fused_peer", "fused_nccl"):
+        r = res.get(tname, {})
+        if "ag_busbw" in r and "ag_busbw" in ceil:
+            r["ag_frac_of_single_buffer"] = round(r["ag_busbw"] / ceil["ag_busbw"], 3)
+            r["rs_frac_of_single_buffer"] = round(r["rs_busbw"] / ceil["rs_busbw"], 3)
+    return out
