@@ -128,13 +128,21 @@ int32_t sdr_dropout(const void* x, int32_t x_dtype, void* y, int32_t y_dtype, vo
                     void* stream);
 
 /* NumPy transcendental mirror for Normal (rng.py:154-155): the float64 tables
- * r[k] = sqrt(-2*log1p(-k*2^-24)) and c[k] = cos(2*pi*(k*2^-24)) for
- * k in [0, 2^24), computed by the host's NumPy (host pointers).  Uploads them
- * to `device`, calibrates the device fast path against them exhaustively and
- * reports the max errors (relative for r, absolute for c). */
-int32_t sdr_normal_tables_load(int32_t device, const double* r_table, const double* c_table,
+ * L[k] = log1p(-k*2^-24) and c[k] = cos((2*pi)*(k*2^-24)) for k in [0, 2^24),
+ * computed by the host's NumPy (host pointers; r = sqrt(-2 L) is correctly
+ * rounded on both sides).  The tables are uploaded to `device` only while the
+ * mirror is built: 2-bit ulp corrections of the device libm's log1p / cos
+ * (8 MiB) plus a sorted exception list, verified bit for bit on all 2^24
+ * points of both functions (if that ever fails, the full tables stay resident
+ * instead).  Also calibrates the fast paths exhaustively and reports their max
+ * errors (relative for r, absolute for c).  Reloading replaces the mirror. */
+int32_t sdr_normal_tables_load(int32_t device, const double* log1p_table, const double* c_table,
                                double* max_rel_err_r, double* max_abs_err_c);
 int32_t sdr_normal_tables_loaded(int32_t device);
+/* Resident mirror bytes on `device`, exception count, 1 if the compact mirror
+ * is in use (0: full tables), and the build time of the last load. */
+int32_t sdr_normal_mirror_info(int32_t device, uint64_t* device_bytes, uint64_t* exceptions,
+                               int32_t* compact, double* build_ms);
 /* Count of elements that took the exact (table) fallback since load. */
 int32_t sdr_normal_fallback_count(int32_t device, uint64_t* count);
 
@@ -173,6 +181,13 @@ int32_t sdr_pack_scatter(const sdr_pack_member* members, int32_t n, void* packed
 int32_t sdr_pack_local(const sdr_pack_member* members, int32_t n, void* segment, void* stream);
 int32_t sdr_unpack_local(const sdr_pack_member* members, int32_t n, const void* segment,
                          void* stream);
+/* Replicate->Shard local slice (dtensor.py:247-251 via _local_slice,
+ * dtensor.py:286-298): full[i] describes a tensor holding the whole split
+ * extent (rows = extent, chunk_rows = ceil(extent/nranks)); piece[i].data
+ * receives rank `rank`'s ceil-block rows (piece[i].rows = that row count,
+ * same outer/inner/elem_bytes).  Also the slice step of Shard->Shard. */
+int32_t sdr_slice_local(const sdr_pack_member* full, const sdr_pack_member* piece, int32_t n,
+                        int32_t rank, int32_t nranks, void* stream);
 
 /* ---- peer-memory collectives over NVLink / NVSwitch (CUDA IPC) ----------
  *
@@ -207,9 +222,14 @@ int32_t sdr_peer_heap_free(void* base);   /* free this process's own heap */
  * scope) into slot `rank` of every rank's flags, then waits (acquire) until
  * every slot of flags[rank] >= epoch.  flags: host array of nranks device
  * pointers (each rank's heap base).  A wait longer than timeout_ns traps (the
- * call fails loudly instead of hanging). */
+ * call fails loudly instead of hanging).  timeout_ns < 0 is the soft mode of
+ * the transport's self-check: after |timeout_ns| the kernel sets flag word
+ * SDR_MAX_PEERS of this rank's own heap to 1 and returns (no trap). */
 int32_t sdr_peer_barrier(void* const* flags, int32_t rank, int32_t nranks, uint64_t epoch,
                          int64_t timeout_ns, void* stream);
+/* Synchronous read of flag word `index` of a heap (e.g. the soft-timeout word
+ * SDR_MAX_PEERS after a self-check). */
+int32_t sdr_peer_flag_read(const void* base, int32_t index, uint64_t* value);
 /* S->R pull: segment r of the gathered layout (sdr_unpack_gathered) is read
  * from segs[r] (rank r's packed shard, usually in its peer heap). */
 int32_t sdr_unpack_gathered_peers(const sdr_pack_member* members, int32_t n,

@@ -15,6 +15,8 @@ int philox_blocks(const uint64_t* tau, const uint64_t* beta, int64_t n, uint64_t
 int normal_tables_load(int device, const double* r_host, const double* c_host, double* er,
                        double* ec);
 int normal_tables_loaded(int device);
+int normal_mirror_info(int device, uint64_t* device_bytes, uint64_t* exceptions, int32_t* compact,
+                       double* build_ms);
 int normal_fallback_count(int device, uint64_t* count);
 int probe_int32(int device, double* imad_per_s, double* lop3_per_s, double* philox_per_s);
 const char* last_cuda_error();
@@ -24,12 +26,15 @@ int pack_scatter(const sdr_pack_member* m, int n, void* packed, int64_t seg_byte
                  cudaStream_t s);
 int pack_local(const sdr_pack_member* m, int n, void* seg, cudaStream_t s);
 int unpack_local(const sdr_pack_member* m, int n, const void* seg, cudaStream_t s);
+int slice_local(const sdr_pack_member* full, const sdr_pack_member* piece, int n, int rank, int nranks,
+                cudaStream_t s);
 int unpack_gathered_peers(const sdr_pack_member* m, int n, const void* const* segs, int nranks,
                           cudaStream_t s);
 int reduce_scatter_peers(const sdr_pack_member* m, int n, const void* const* packed,
                          int64_t seg_bytes, int nranks, int rank, int dtype, cudaStream_t s);
 int peer_barrier(void* const* flags, int rank, int nranks, uint64_t epoch, int64_t timeout_ns,
                  cudaStream_t s);
+int peer_flag_read(const void* base, int index, uint64_t* value);
 int peer_heap_alloc(int device, int64_t bytes, void** base, sdr_ipc_handle* handle);
 int peer_heap_open(int device, const sdr_ipc_handle* handle, void** base);
 int peer_heap_close(void* base);
@@ -93,12 +98,17 @@ int32_t sdr_dropout(const void* x, int32_t x_dtype, void* y, int32_t y_dtype, vo
   return sdr::dropout(x, x_dtype, y, y_dtype, mask, mask_dtype, p, *rng, *view, as_stream(stream));
 }
 
-int32_t sdr_normal_tables_load(int32_t device, const double* r_table, const double* c_table,
+int32_t sdr_normal_tables_load(int32_t device, const double* log1p_table, const double* c_table,
                                double* max_rel_err_r, double* max_abs_err_c) {
-  return sdr::normal_tables_load(device, r_table, c_table, max_rel_err_r, max_abs_err_c);
+  return sdr::normal_tables_load(device, log1p_table, c_table, max_rel_err_r, max_abs_err_c);
 }
 
 int32_t sdr_normal_tables_loaded(int32_t device) { return sdr::normal_tables_loaded(device); }
+
+int32_t sdr_normal_mirror_info(int32_t device, uint64_t* device_bytes, uint64_t* exceptions,
+                               int32_t* compact, double* build_ms) {
+  return sdr::normal_mirror_info(device, device_bytes, exceptions, compact, build_ms);
+}
 
 int32_t sdr_normal_fallback_count(int32_t device, uint64_t* count) {
   return sdr::normal_fallback_count(device, count);
@@ -123,6 +133,11 @@ int32_t sdr_unpack_local(const sdr_pack_member* members, int32_t n, const void* 
   return sdr::unpack_local(members, n, segment, as_stream(stream));
 }
 
+int32_t sdr_slice_local(const sdr_pack_member* full, const sdr_pack_member* piece, int32_t n,
+                        int32_t rank, int32_t nranks, void* stream) {
+  return sdr::slice_local(full, piece, n, rank, nranks, as_stream(stream));
+}
+
 int32_t sdr_peer_heap_alloc(int32_t device, int64_t bytes, void** base, sdr_ipc_handle* handle) {
   return sdr::peer_heap_alloc(device, bytes, base, handle);
 }
@@ -138,6 +153,10 @@ int32_t sdr_peer_heap_free(void* base) { return sdr::peer_heap_free(base); }
 int32_t sdr_peer_barrier(void* const* flags, int32_t rank, int32_t nranks, uint64_t epoch,
                          int64_t timeout_ns, void* stream) {
   return sdr::peer_barrier(flags, rank, nranks, epoch, timeout_ns, as_stream(stream));
+}
+
+int32_t sdr_peer_flag_read(const void* base, int32_t index, uint64_t* value) {
+  return sdr::peer_flag_read(base, index, value);
 }
 
 int32_t sdr_unpack_gathered_peers(const sdr_pack_member* members, int32_t n,

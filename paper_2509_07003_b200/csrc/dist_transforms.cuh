@@ -40,11 +40,57 @@ struct NormalLut32 {
   float2 trig_lo[4096];  // (cos, sin)(2 pi lo / 2^24)
 };
 
+// Tables of the float64-precision fast path of float32 / float16 outputs
+// (160 KiB, staged in dynamic shared memory by 512-thread CTAs, one per SM).
+// With n = 2^24 - k, nf = float(n) = 2^E m (exact, m in [1, 2)), j = the top
+// 11 fraction bits of m:
+//   X = -2 ln(n 2^-24) = (24 - E) 2ln2 + T_j - 2 log1p(s),  s = m inv_j - 1,
+// inv_j ~ 1/m_j a multiple of 2^-12 (so s is an exact float32 FFMA, |s| <
+// 2^-11), T_j = 2 ln(inv_j) in float64.  Buckets with m >= 1.5 use inv_j ~
+// 1/m_j in (1/2, 2/3] and T_j = 2 ln(2 inv_j) - C2 (C2 = RN(2 ln 2), the
+// constant the (24 - E) term is multiplied by), so the top bucket (inv = 1/2,
+// T = -C2, E = 23) gives A = 0 exactly and X near 0 keeps full relative
+// precision.  The cosine is two-level: cos(2 pi k2 / 2^24) = C_i C_b - S_i S_b
+// with k2 = 4096 i + b.
+struct __align__(16) LogEnt2 {
+  float inv;
+  float pad;
+  double T;
+};
+struct NormalLut2 {
+  LogEnt2 logt[2048];
+#if SDR_N2_COS2
+  double2 cos_hi[4096];  // (cos, sin)(2 pi i / 4096)
+  double2 cos_lo[4096];  // (cos, sin)(2 pi b / 2^24)
+#else
+  double2 trig[2048];    // (cos, sin)(i pi/1024), as NormalLut::trig (c_fast)
+#endif
+};
+
+// The exact mirror of NumPy's two transcendentals (rng.py:154-155) in 2-bit
+// ulp corrections against the device's own libm: for k in [0, 2^24)
+//   L(k) = log1p(-k 2^-24),  C(k) = cos((2 pi) (k 2^-24)),
+// code = bits(NumPy) - bits(CUDA) in {0, +1, -1}, 3 = exception (exact value
+// in a sorted (key, value) list).  8 MiB per device instead of 2 x 128 MiB of
+// float64 tables; r = sqrt(-2 L) is correctly rounded on both sides.
+struct ExactMirror {
+  const uint32_t* code_l;  // 16 codes per word
+  const uint32_t* code_c;
+  const uint32_t* xk_l;    // exceptions: sorted keys, values
+  const double* xv_l;
+  const uint32_t* xk_c;
+  const double* xv_c;
+  int32_t nx_l, nx_c;
+};
+
 struct NormalMirror {
-  const double* rtab;   // NumPy r[k] = sqrt(-2*log1p(-k*2^-24))
-  const double* ctab;   // NumPy c[k] = cos(2*pi*(k*2^-24))
+  const double* rtab;   // full NumPy r[k] table, only when the compact mirror failed verification
+  const double* ctab;   // full NumPy c[k] table (same)
+  ExactMirror em;
   const NormalLut* lut; // device copy of the fast-path tables
   const NormalLut32* lut32;
+  const NormalLut2* lut2;
+  double kr2, k02;      // certification bound of the NormalLut2 path
   double nh, th;        // -0.5*std, 1.5*std: the Newton step of r_fast returns std*r
   double kr, k0;        // certification bound B = (std r) kr + k0
   // float32 fast path (bfloat16 outputs): calibrated errors and bound terms
@@ -82,6 +128,9 @@ __constant__ double c_npoly[9] = {
 #ifndef SDR_NORMAL_SPLIT
 #define SDR_NORMAL_SPLIT 1  // float64 phases of a chunk in SPLIT passes (register pressure)
 #endif
+#ifndef SDR_R_SEED32
+#define SDR_R_SEED32 1    // r_fast: float32 rsqrt seed (1) or MUFU.RSQ64H (0)
+#endif
 #ifndef SDR_R_NEWTON2
 #define SDR_R_NEWTON2 0   // second Newton step for r (fewer certification fallbacks)
 #endif
@@ -94,6 +143,45 @@ __constant__ double c_npoly[9] = {
 #ifndef SDR_FILL_MINB
 #define SDR_FILL_MINB 2   // CTAs/SM the register budget of the fill kernels is sized for
 #endif
+#ifndef SDR_NORMAL_N2
+#define SDR_NORMAL_N2 0   // float32/float16 normals on the NormalLut2 tables (else NormalLut)
+#endif
+#ifndef SDR_FILL_PIPE
+#define SDR_FILL_PIPE 0   // software-pipelined Normal walk loop (next chunk's Philox beside this transform)
+#endif
+#ifndef SDR_NSPLIT
+#define SDR_NSPLIT 1      // Normal chunks in NSPLIT parts (Philox + transform per part: fewer live registers)
+#endif
+#ifndef SDR_BF16_MINB
+#define SDR_BF16_MINB SDR_FILL_MINB  // CTAs/SM for the bfloat16 Normal kernels' register budget
+#endif
+#ifndef SDR_N2_MINB
+#define SDR_N2_MINB 2     // CTAs/SM the NormalLut2 kernels' register budget is sized for (256 threads)
+#endif
+#ifndef SDR_R2_SEED
+#define SDR_R2_SEED 1     // r_fast2 rsqrt seed: 0 MUFU.RSQ64H, 1 float32 MUFU.RSQ, 2 RSQ64H + 2nd Newton
+#endif
+#ifndef SDR_N2_COS2
+#define SDR_N2_COS2 0     // NormalLut2 cosine: two-level table (1) or c_fast's table + polynomial (0)
+#endif
+#ifndef SDR_N2_THREADS
+#define SDR_N2_THREADS 256  // CTA size of the NormalLut2 kernels (smem allows 2-3 CTAs/SM without COS2)
+#endif
+
+// Kernels drawing float32 / float16 normals stage NormalLut2 (64 KiB; 160 KiB
+// with SDR_N2_COS2, then one 512-thread CTA per SM).  Everything else:
+// 256-thread CTAs, SDR_FILL_MINB per SM.
+template <int DIST, int DT>
+constexpr bool uses_lut2() {
+  return SDR_NORMAL_N2 && DIST == SDR_NORMAL && (DT == SDR_F32 || DT == SDR_F16);
+}
+template <int DIST, int DT>
+constexpr int fill_threads() { return uses_lut2<DIST, DT>() ? SDR_N2_THREADS : 256; }
+template <int DIST, int DT>
+constexpr int fill_minb() {
+  return uses_lut2<DIST, DT>() ? SDR_N2_MINB * 256 / SDR_N2_THREADS
+         : (DIST == SDR_NORMAL && DT == SDR_BF16) ? SDR_BF16_MINB : SDR_FILL_MINB;
+}
 
 __host__ __device__ __forceinline__ double hilo(uint32_t hi, uint32_t lo) {
 #ifdef __CUDA_ARCH__
@@ -150,7 +238,14 @@ __device__ __forceinline__ double r_fast(uint32_t w0, const NormalLut* L, double
   const double g = fma(s * s, p, s);                                     // -2 log1p(t)
   const double ne = kTwo52p1047 - hilo(0x43300000u, (hw + 0x80000u) >> 20);  // -e, exact
   const double X = fma(ne, C[8], tb.y + g);                              // -2 ln w
+#if SDR_R_SEED32
+  // float32 MUFU.RSQ seed (~2^-23 vs ~2^-20 for MUFU.RSQ64H): after the one
+  // Newton step r is good to ~2^-45, so ~8x fewer elements miss
+  // certification; the clamp keeps k = 0 (X ~ 2^-1000) finite.
+  double h = static_cast<double>(rsqrtf(fmaxf(__double2float_rn(X), 0x1p-126f)));
+#else
   double h = rsqrt_seed(X);
+#endif
 #if SDR_R_NEWTON2
   h = h * fma(X * h, h * -0.5, 1.5);                                     // seed to ~2^-40
 #endif
@@ -159,16 +254,17 @@ __device__ __forceinline__ double r_fast(uint32_t w0, const NormalLut* L, double
 }
 
 // cos(2*pi*k*2^-24), k = w1 >> 8: nearest pi/1024 table point + residual.
-__device__ __forceinline__ double c_fast(uint32_t w1, const NormalLut* L) {
+__device__ __forceinline__ double c_fast_trig(uint32_t w1, const double2* trig) {
   const double* C = c_npoly;
   const uint32_t u = w1 + 0x100000u;                                     // (k + 4096) << 8
-  const double2 cs = lut_at(L->trig, (u >> 17) & 0x7FF0u);               // i = u >> 21
+  const double2 cs = lut_at(trig, (u >> 17) & 0x7FF0u);                  // i = u >> 21
   const double d = hilo(0x43300000u, (u >> 8) & 0x1FFFu) - kTwo52p4096;  // k - 8192 i, exact
   const double d2 = d * d;
   const double cm = d2 * fma(d2, C[4], C[5]);                            // cos(K d) - 1
   const double sd = d * fma(d2, C[6], C[7]);                             // sin(K d)
   return fma(-cs.y, sd, fma(cs.x, cm, cs.x));
 }
+__device__ __forceinline__ double c_fast(uint32_t w1, const NormalLut* L) { return c_fast_trig(w1, L->trig); }
 
 // float32 fast functions for the bfloat16 path: the same reductions as
 // r_fast / c_fast in float32 arithmetic (~2^-21), calibrated exhaustively like
@@ -195,6 +291,67 @@ __device__ __forceinline__ float c32_fast(uint32_t w1, const NormalLut32* L) {
   const float2 a = lut_at(L->trig_hi, (w1 >> 17) & 0x7FF8u);  // hi = k >> 12
   const float2 b = lut_at(L->trig_lo, (w1 >> 5) & 0x7FF8u);   // lo = k & 4095
   return fmaf(a.x, b.x, -a.y * b.y);
+}
+
+// std * r(k) from NormalLut2 (see there): s and t = s (s/2 - 2/3) in float32
+// (s exact, t to 2^-24 relative), X = (A - 2s) + s^2 (1 + t) in float64, one
+// Newton step on the MUFU.RSQ64H seed with std folded in (nh = -std/2,
+// th = 3 std/2).  13 float64 operations fewer than r_fast + c_fast.  k = 0:
+// T_0 carries 2^-1000 so X > 0 (r ~ 2^-500, never certified).
+constexpr double kTwoLn2 = 0x1.62e42fefa39efp0;  // RN(2 ln 2)
+__device__ __forceinline__ double r_fast2(uint32_t w0, const NormalLut2* L, double nh, double th) {
+  const uint32_t hw = __float_as_uint(__uint2float_rn(0x1000000u - (w0 >> 8)));  // n, exact
+  const LogEnt2 tb = lut_at(L->logt, (hw >> 8) & 0x7FF0u);                         // j = hw[22:12]
+  const float m = __uint_as_float((hw & 0x007FFFFFu) | 0x3F800000u);
+  const float s = fmaf(m, tb.inv, -1.0f);                                          // exact
+  const float t = s * fmaf(s, 0.5f, -0.666666686534881591796875f);
+  const double sd = static_cast<double>(s);
+  const double A = fma(__uint2double_rn(151u - (hw >> 23)), kTwoLn2, tb.T);        // (24-E) 2ln2 + T_j
+  const double s2 = sd * sd;                                                       // exact
+  const double X = fma(sd, -2.0, A) + fma(s2, static_cast<double>(t), s2);        // -2 ln w
+#if SDR_R2_SEED == 1
+  // float32 MUFU.RSQ seed (~2^-23; the f64 MUFU.RSQ64H seed is ~2^-20): one
+  // Newton step then leaves ~2^-45 instead of ~2^-39.5, so ~64x fewer
+  // elements miss certification.  The clamp keeps k = 0 (X = 2^-1000) finite.
+  const double h = static_cast<double>(rsqrtf(fmaxf(__double2float_rn(X), 0x1p-126f)));
+#else
+  double h = rsqrt_seed(X);
+#if SDR_R2_SEED == 2
+  h = fma(h, 0.5 * fma(-(X * h), h, 1.0), h);  // second Newton step on 1/sqrt(X)
+#endif
+#endif
+  const double gx = X * h;
+  return gx * fma(gx * h, nh, th);                                                 // std * sqrt(X)
+}
+
+// cos(2*pi*k2*2^-24), k2 = w1 >> 8.  SDR_N2_COS2: two-level table, k2 =
+// 4096 i + b, C_i C_b - S_i S_b (2 float64 ops, 32 B of random shared-memory
+// reads); else c_fast's pi/1024 table + residual polynomial (16 B, 8 ops).
+// Random 16 B shared loads cost ~12 wavefronts per warp (bank conflicts), so
+// the bytes per element bound the kernel as much as the float64 ops do.
+__device__ __forceinline__ double c_fast2(uint32_t w1, const NormalLut2* L) {
+#if SDR_N2_COS2
+  const double2 a = lut_at(L->cos_hi, (w1 >> 16) & 0xFFF0u);
+  const double2 b = lut_at(L->cos_lo, (w1 >> 4) & 0xFFF0u);
+  return fma(a.x, b.x, -(a.y * b.y));
+#else
+  return c_fast_trig(w1, L->trig);
+#endif
+}
+
+// Every double within B of v rounds (RN) to the same float32 as v.  Checked on
+// v's bits: d = distance of v to the nearest float32 rounding midpoint in ulps
+// of v (low 29 mantissa bits against 2^28), against 2^sh > B / ulp(v) from the
+// exponent fields (B >= |v| 2^-51 keeps sh >= 1).  Normal float32 range only:
+// zero, subnormal and overflowing v are never certified.
+__device__ __forceinline__ bool f32_round_certified(double v, double B) {
+  const uint32_t vh = dhi(v);
+  const uint32_t ev = (vh >> 20) & 0x7FFu;
+  const uint32_t sh = (dhi(B) >> 20) + 53u - ev;  // B < 2^(eB+1), ulp(v) = 2^(ev-1075)
+  const int32_t t = static_cast<int32_t>(dlo(v) & 0x1FFFFFFFu) - 0x10000000;
+  uint32_t q;
+  asm("shf.r.clamp.b32 %0, %1, 0, %2;" : "=r"(q) : "r"(static_cast<uint32_t>(abs(t))), "r"(sh));
+  return (ev - 897u) <= 253u && q != 0u;
 }
 
 template <int DT>
@@ -229,11 +386,47 @@ __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLu
   }
 }
 
-// Exact Normal (rng.py:150-156) from the NumPy tables: float64 Box-Muller with
-// the reference's own r[k1], c[k2], then one cast.
+// CUDA libm value d of table point k corrected to NumPy's (ExactMirror).
+__device__ __noinline__ double mirror_fix(double d, const uint32_t* code, uint32_t k, const uint32_t* xk,
+                                          const double* xv, int32_t nx) {
+  const uint32_t c = (__ldg(code + (k >> 4)) >> ((k & 15u) * 2u)) & 3u;
+  if (c == 3u) {  // exception: binary search of the sorted keys
+    int lo = 0, hi = nx - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(xk + mid) < k) lo = mid + 1;
+      else hi = mid;
+    }
+    return __ldg(xv + lo);
+  }
+  const long long b = __double_as_longlong(d);
+  return c == 0u ? d : __longlong_as_double(c == 1u ? b + 1 : b - 1);
+}
+
+// NumPy's r[k1] and c[k2] (rng.py:154-155): the device's log1p / cos of the
+// same float64 arguments, corrected by the mirror; sqrt is correctly rounded.
+__device__ __forceinline__ double mirror_r(const ExactMirror& M, uint32_t k) {
+  const double L = mirror_fix(log1p(-static_cast<double>(k) * 0x1p-24), M.code_l, k, M.xk_l, M.xv_l, M.nx_l);
+  return __dsqrt_rn(-2.0 * L);
+}
+__device__ __forceinline__ double mirror_c(const ExactMirror& M, uint32_t k) {
+  const double arg = __dmul_rn(6.283185307179586, static_cast<double>(k) * 0x1p-24);  // (2.0*pi)*u2
+  return mirror_fix(cos(arg), M.code_c, k, M.xk_c, M.xv_c, M.nx_c);
+}
+
+// Exact Normal (rng.py:150-156): float64 Box-Muller with the reference's own
+// r[k1], c[k2] (compact mirror, or the full tables if it failed verification),
+// then one cast.
 template <int DT>
-__device__ __forceinline__ typename St<DT>::T normal_exact(const DistP& P, uint32_t w0, uint32_t w1) {
-  const double r = __ldg(P.nm.rtab + (w0 >> 8)), c = __ldg(P.nm.ctab + (w1 >> 8));
+__device__ __noinline__ typename St<DT>::T normal_exact(const DistP& P, uint32_t w0, uint32_t w1) {
+  double r, c;
+  if (P.nm.rtab != nullptr) {
+    r = __ldg(P.nm.rtab + (w0 >> 8));
+    c = __ldg(P.nm.ctab + (w1 >> 8));
+  } else {
+    r = mirror_r(P.nm.em, w0 >> 8);
+    c = mirror_c(P.nm.em, w1 >> 8);
+  }
   return from_f64<DT>(__dadd_rn(P.mean, __dmul_rn(P.stdv, __dmul_rn(r, c))));
 }
 
@@ -294,6 +487,42 @@ __device__ __forceinline__ void normal_chunk(const DistP& P, const NormalLut* L,
     }
   }
 }
+// A chunk of float32 / float16 normals on the NormalLut2 tables: all r, all c,
+// combine, certify (float32: on the bits of v; float16: by rounding v +- B),
+// one branch for the rare uncertified elements (exact NumPy tables).
+template <int DT, int NE>
+__device__ __forceinline__ void normal_chunk2(const DistP& P, const NormalLut2* L, const uint32_t* w0,
+                                              const uint32_t* w1, typename St<DT>::T* out) {
+  double rs[NE], c[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) rs[e] = r_fast2(w0[e], L, P.nm.nh, P.nm.th);
+#pragma unroll
+  for (int e = 0; e < NE; ++e) c[e] = c_fast2(w1[e], L);
+  uint32_t badmask = 0;
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const double v = fma(rs[e], c[e], P.mean);
+    const double B = fma(rs[e], P.nm.kr2, P.nm.k02);
+    if constexpr (DT == SDR_F32) {
+      out[e] = __double2float_rn(v);
+      badmask |= f32_round_certified(v, B) ? 0u : (1u << e);
+    } else {
+      const auto lo = from_f64<DT>(v - B), hi = from_f64<DT>(v + B);
+      out[e] = lo;
+      badmask |= lo == hi ? 0u : (1u << e);
+    }
+  }
+  if (__builtin_expect(badmask != 0, 0)) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      if (badmask & (1u << e)) {
+        atomicAdd(P.nm.fallbacks, 1ull);
+        out[e] = normal_exact<DT>(P, w0[e], w1[e]);
+      }
+    }
+  }
+}
+
 // Stage the Normal tables in shared memory: one elected thread issues a TMA
 // bulk copy (cp.async.bulk global -> shared, completion on an mbarrier) and the
 // CTA waits on the barrier -- one 20-40 KiB transfer instead of a loop of

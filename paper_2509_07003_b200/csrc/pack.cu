@@ -168,6 +168,31 @@ int unpack_local(const sdr_pack_member* M, int n, const void* seg, cudaStream_t 
   return run_jobs(jobs, s);
 }
 
+// Replicate -> Shard local slice (dtensor.py:247-251, _local_slice
+// dtensor.py:286-298): rank `rank`'s ceil-block rows of each full member into
+// its piece tensor, one batched 2-D copy job per member.
+int slice_local(const sdr_pack_member* F, const sdr_pack_member* Pc, int n, int rank, int nranks,
+                cudaStream_t s) {
+  if (n < 0 || nranks < 1 || rank < 0 || rank >= nranks || (n > 0 && (F == nullptr || Pc == nullptr)))
+    return SDR_E_INVALID;
+  std::vector<CopyJob> jobs;
+  for (int i = 0; i < n; ++i) {
+    const sdr_pack_member& f = F[i];
+    const sdr_pack_member& p = Pc[i];
+    if (!member_ok(f) || f.chunk_rows * nranks < f.rows) return SDR_E_INVALID;
+    int64_t lo, len;
+    rank_rows(f.rows, f.chunk_rows, rank, lo, len);
+    if (p.outer != f.outer || p.inner != f.inner || p.elem_bytes != f.elem_bytes || p.rows != len)
+      return SDR_E_INVALID;
+    if (len == 0 || f.outer == 0 || f.inner == 0) continue;
+    if (p.data == nullptr) return SDR_E_INVALID;
+    const int64_t row_b = f.inner * f.elem_bytes;
+    add_job(jobs, static_cast<const unsigned char*>(f.data) + lo * row_b, p.data, f.outer, len * row_b,
+            f.rows * row_b, len * row_b);
+  }
+  return run_jobs(jobs, s);
+}
+
 // Force-load the copy kernels (CUDA lazy loading loads a kernel at its first
 // launch, and that load waits for running kernels: a host thread that launches
 // a not-yet-loaded kernel behind a spinning peer barrier would stall).

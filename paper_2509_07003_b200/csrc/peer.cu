@@ -263,7 +263,11 @@ __global__ void k_peer_barrier(const __grid_constant__ PeerFlags F, int rank, in
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
     if (v >= epoch) break;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-    if (static_cast<long long>(now - t0) > timeout_ns) {
+    if (static_cast<long long>(now - t0) > (timeout_ns < 0 ? -timeout_ns : timeout_ns)) {
+      if (timeout_ns < 0) {  // soft mode: record the timeout in my own flag word SDR_MAX_PEERS, return
+        atomicMax(F.p[rank] + SDR_MAX_PEERS, 1ull);
+        return;
+      }
       printf("sdr_peer_barrier: rank %d timed out waiting for fiber rank %d (epoch %llu, saw %llu)\n",
              rank, t, epoch, v);
       __trap();
@@ -388,7 +392,7 @@ int reduce_scatter_peers(const sdr_pack_member* M, int n, const void* const* pac
 int peer_barrier(void* const* flags, int rank, int nranks, uint64_t epoch, int64_t timeout_ns,
                  cudaStream_t s) {
   if (flags == nullptr || nranks < 1 || nranks > SDR_MAX_PEERS || rank < 0 || rank >= nranks ||
-      timeout_ns <= 0)
+      timeout_ns == 0)
     return SDR_E_INVALID;
   PeerFlags F;
   memset(&F, 0, sizeof(F));
@@ -420,6 +424,13 @@ static int cuda_status(cudaError_t e) {
   set_cuda_error(e);
   return SDR_E_CUDA;
 }
+
+int peer_flag_read(const void* base, int index, uint64_t* value) {
+  if (base == nullptr || value == nullptr || index < 0 || index >= SDR_PEER_FLAG_BYTES / 8)
+    return SDR_E_INVALID;
+  return cuda_status(cudaMemcpy(value, static_cast<const uint64_t*>(base) + index, 8, cudaMemcpyDeviceToHost));
+}
+
 
 int preload_copy_kernels();
 

@@ -135,6 +135,43 @@ __device__ __forceinline__ void chunk_words_aligned(const Gen& g, uint64_t j0, u
   }
 }
 
+// chunk_words_aligned in parts: the chunk-uniform values once (hoist_chunk),
+// then words of elements E0 .. E0+NE-1 (words_part), so a caller can finish
+// the transform of one part before the Philox registers of the next are live.
+struct ChunkHoist {
+  uint32_t bhi, y3, hq, z1;
+  uint64_t pb0;
+};
+__device__ __forceinline__ ChunkHoist hoist_chunk(const Gen& g, uint64_t j0) {
+  const uint64_t beta = (j0 >> g.div_theta.s) + g.offset;
+  const uint64_t t = j0 & (g.theta - 1);
+  const uint64_t pa = mul_wide(lo32(beta), kM0);
+  const uint32_t y2 = hi32(pa) ^ hi32(t) ^ g.keys.k1[0];
+  const uint64_t pq = mul_wide(y2, kM1);
+  return ChunkHoist{hi32(beta), lo32(pa), hi32(pq), lo32(pq), mul_wide(lo32(t), kM1)};
+}
+template <int NE, int E0>
+__device__ __forceinline__ void words_part(const RoundKeys& K, const ChunkHoist& H, uint32_t (&w0)[NE],
+                                           uint32_t (&w1)[NE]) {
+  uint32_t x0[NE], x1[NE], x2[NE], x3[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const uint64_t pb = H.pb0 + static_cast<uint64_t>(E0 + e) * kM1;
+    const uint32_t y0 = hi32(pb) ^ H.bhi ^ K.k0[0];
+    const uint64_t pa2 = mul_wide(y0, kM0);
+    x0[e] = H.hq ^ lo32(pb) ^ K.k0[1];
+    x1[e] = H.z1;
+    x2[e] = hi32(pa2) ^ H.y3 ^ K.k1[1];
+    x3[e] = lo32(pa2);
+  }
+  rounds_from<2, NE>(K, x0, x1, x2, x3);
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    w0[e] = x0[e];
+    w1[e] = x1[e];
+  }
+}
+
 // Word 1 only, for a keep/drop decision (dropout): the last two rounds need
 // just hi(M0*x0) of round 9 and lo(M1*x2) of round 10.  Same preconditions as
 // chunk_words_aligned.  A tie on the high threshold word (p = 2^-32) is
@@ -354,11 +391,12 @@ inline void setup_chunks(const CanonView& cv, bool fast, uint64_t& nchunks, uint
 
 // 256-thread launch with programmatic stream serialization (PDL) when SDR_PDL.
 template <typename K, typename Args>
-inline void launch_pdl(K kernel, int grid, cudaStream_t s, const Args& A, size_t dyn_smem = 0) {
+inline void launch_pdl(K kernel, int grid, cudaStream_t s, const Args& A, size_t dyn_smem = 0,
+                       int threads = 256) {
 #if SDR_PDL
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(static_cast<unsigned>(threads));
   cfg.dynamicSmemBytes = dyn_smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -368,7 +406,7 @@ inline void launch_pdl(K kernel, int grid, cudaStream_t s, const Args& A, size_t
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kernel, A);
 #else
-  kernel<<<grid, 256, dyn_smem, s>>>(A);
+  kernel<<<grid, threads, dyn_smem, s>>>(A);
 #endif
 }
 

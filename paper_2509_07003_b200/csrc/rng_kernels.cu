@@ -21,6 +21,7 @@
 // error is measured exhaustively at load, a rigorous bound, and the exact
 // NumPy tables for the few elements the bound cannot certify.
 // The SDR_* macros below are A/B knobs; their defaults are the measured best.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -116,12 +117,43 @@ __device__ __forceinline__ void fill_words(const FillArgs& A, uint64_t j0, uint3
   else chunk_words<kV>(A.g, j0, w0, w1);
 }
 
+// Transform of elements E0 .. E0+3 of a chunk from their words (the half-chunk
+// pipeline of k_fill_fast).
+template <int DT, int E0>
+__device__ __forceinline__ void normal_half(const FillArgs& A, const NormalLut* L, const uint32_t (&w0)[4],
+                                            const uint32_t (&w1)[4], typename St<DT>::T (&v)[kV]) {
+  if constexpr (uses_lut2<SDR_NORMAL, DT>())
+    normal_chunk2<DT, 4>(A.d, reinterpret_cast<const NormalLut2*>(L), w0, w1, v + E0);
+  else
+    normal_chunk_bf16<4>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v + E0);
+}
+
+// Normal values of a chunk in SDR_NSPLIT parts (Philox words of a part, then
+// its transform) so the peak register set is one part's, not the chunk's.
+template <int DT, int NE, int E0>
+__device__ __forceinline__ void normal_part(const FillArgs& A, const NormalLut* L, const ChunkHoist& H,
+                                            typename St<DT>::T (&v)[kV]) {
+  uint32_t w0[NE], w1[NE];
+  words_part<NE, E0>(A.g.keys, H, w0, w1);
+  if constexpr (uses_lut2<SDR_NORMAL, DT>())
+    normal_chunk2<DT, NE>(A.d, reinterpret_cast<const NormalLut2*>(L), w0, w1, v + E0);
+  else
+    normal_chunk_bf16<NE>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v + E0);
+  if constexpr (E0 + NE < kV) normal_part<DT, NE, E0 + NE>(A, L, H, v);
+}
+
 template <int DIST, int DT, bool ALIGNED>
 __device__ __forceinline__ void chunk_values(const FillArgs& A, const NormalLut* L, uint64_t j0,
                                              typename St<DT>::T (&v)[kV]) {
-  uint32_t w0[kV], w1[kV];
-  fill_words<ALIGNED>(A, j0, w0, w1);
-  values_from_words<DIST, DT>(A, L, w0, w1, v);
+  if constexpr (ALIGNED && SDR_NSPLIT > 1 && DIST == SDR_NORMAL &&
+                (uses_lut2<DIST, DT>() || (DT == SDR_BF16 && SDR_NORMAL_BF16_F32))) {
+    const ChunkHoist H = hoist_chunk(A.g, j0);
+    normal_part<DT, kV / SDR_NSPLIT, 0>(A, L, H, v);
+  } else {
+    uint32_t w0[kV], w1[kV];
+    fill_words<ALIGNED>(A, j0, w0, w1);
+    values_from_words<DIST, DT>(A, L, w0, w1, v);
+  }
 }
 
 template <int DIST, int DT>
@@ -130,6 +162,8 @@ __device__ __forceinline__ void values_from_words(const FillArgs& A, const Norma
                                                   typename St<DT>::T (&v)[kV]) {
   if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
     normal_chunk_bf16<kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v);
+  } else if constexpr (uses_lut2<DIST, DT>()) {
+    normal_chunk2<DT, kV>(A.d, reinterpret_cast<const NormalLut2*>(L), w0, w1, v);
   } else if constexpr (DIST == SDR_NORMAL && DT != SDR_F64) {
     constexpr int NS = SDR_NORMAL_SPLIT;
 #pragma unroll
@@ -189,13 +223,19 @@ __device__ __forceinline__ void fill_elem(const FillArgs& A, const NormalLut* L,
 }
 
 template <int DIST, int DT, bool ALIGNED>
-__global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_fast(const __grid_constant__ FillArgs A) {
+__global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>())
+    k_fill_fast(const __grid_constant__ FillArgs A) {
 #if SDR_PDL
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
   const NormalLut* L = nullptr;
   uint32_t bar = 0;  // Normal: tables arriving by TMA (waited on before first use)
-  if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
+  if constexpr (uses_lut2<DIST, DT>()) {
+    extern __shared__ __align__(16) unsigned char s_dyn[];  // sizeof(NormalLut2), set at launch
+    NormalLut2* s_lut2 = reinterpret_cast<NormalLut2*>(s_dyn);
+    bar = stage_lut_begin(s_lut2, A.d.nm.lut2);
+    L = reinterpret_cast<const NormalLut*>(s_lut2);
+  } else if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
     extern __shared__ __align__(16) unsigned char s_dyn[];  // sizeof(NormalLut32), set at launch
     NormalLut32* s_lut32 = reinterpret_cast<NormalLut32*>(s_dyn);
     bar = stage_lut_begin(s_lut32, A.d.nm.lut32);
@@ -215,7 +255,58 @@ __global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_fast(const __grid_c
   if (A.walk.on) {
     uint64_t cq;
     uint64_t j = walk_start(A.ix, A.div_cpr, q, kV, cq);
-    if constexpr (DIST == SDR_NORMAL) {
+    if constexpr (DIST == SDR_NORMAL && SDR_FILL_PIPE == 2 && ALIGNED &&
+                  (uses_lut2<DIST, DT>() || (DT == SDR_BF16 && SDR_NORMAL_BF16_F32))) {
+      // Half-chunk software pipeline: every step computes the Philox words of
+      // the NEXT half chunk (4 elements; pure arithmetic, computed past the end
+      // too and discarded) in the same basic block as the transform of the
+      // current half, so the fma-heavy IMAD.WIDE stream and the transform's
+      // ALU / FP32 / shared / XU work interleave inside each warp.
+      using T = typename St<DT>::T;
+      ChunkHoist H = hoist_chunk(A.g, j);
+      uint32_t a0[4], a1[4], b0[4], b1[4];
+      words_part<4, 0>(A.g.keys, H, a0, a1);
+      stage_lut_wait(bar);
+      for (; q < A.nchunks; q += stride) {
+        T v[kV];
+        words_part<4, 4>(A.g.keys, H, b0, b1);
+        normal_half<DT, 0>(A, L, a0, a1, v);
+        uint64_t jn = j, cqn = cq;
+        walk_next(A.walk, A.chunks_per_row, jn, cqn);
+        H = hoist_chunk(A.g, jn);
+        words_part<4, 0>(A.g.keys, H, a0, a1);
+        normal_half<DT, 4>(A, L, b0, b1, v);
+        store_chunk(static_cast<T*>(A.out) + q * kV, v);
+        j = jn;
+        cq = cqn;
+      }
+    } else if constexpr (DIST == SDR_NORMAL && SDR_FILL_PIPE == 1) {
+      // Software pipeline: the Philox words of the thread's next chunk are
+      // computed (unconditionally: pure arithmetic, discarded past the end)
+      // in the same basic block as the transform of the current chunk, so the
+      // fma-heavy IMAD.WIDE stream interleaves with the transform's ALU /
+      // shared / XU work instead of alternating phases.
+      using T = typename St<DT>::T;
+      uint32_t w0[kV], w1[kV];
+      fill_words<ALIGNED>(A, j, w0, w1);
+      stage_lut_wait(bar);
+      for (; q < A.nchunks; q += stride) {
+        uint64_t jn = j, cqn = cq;
+        walk_next(A.walk, A.chunks_per_row, jn, cqn);
+        uint32_t n0[kV], n1[kV];
+        fill_words<ALIGNED>(A, jn, n0, n1);
+        T v[kV];
+        values_from_words<DIST, DT>(A, L, w0, w1, v);
+        store_chunk(static_cast<T*>(A.out) + q * kV, v);
+#pragma unroll
+        for (int e = 0; e < kV; ++e) {
+          w0[e] = n0[e];
+          w1[e] = n1[e];
+        }
+        j = jn;
+        cq = cqn;
+      }
+    } else if constexpr (DIST == SDR_NORMAL) {
       // first chunk peeled: its Philox words overlap the table transfer
       if (q < A.nchunks) {
         using T = typename St<DT>::T;
@@ -269,13 +360,18 @@ __global__ void __launch_bounds__(256) k_fill_generic(const __grid_constant__ Fi
 constexpr uint64_t kTileElems = SDR_TILE_ELEMS;
 
 template <int DIST, int DT>
-__global__ void __launch_bounds__(256, SDR_FILL_MINB) k_fill_batch(const FillArgs* __restrict__ descs,
-                                                    const uint64_t* __restrict__ tile_prefix,
-                                                    int n, uint64_t ntiles) {
+__global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>())
+    k_fill_batch(const FillArgs* __restrict__ descs, const uint64_t* __restrict__ tile_prefix, int n,
+                 uint64_t ntiles) {
   __shared__ __align__(16) unsigned char smem[sizeof(FillArgs)];
   FillArgs& A = *reinterpret_cast<FillArgs*>(smem);
   const NormalLut* L = nullptr;
-  if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
+  if constexpr (uses_lut2<DIST, DT>()) {
+    extern __shared__ __align__(16) unsigned char s_dyn[];  // sizeof(NormalLut2), set at launch
+    NormalLut2* s_lut2 = reinterpret_cast<NormalLut2*>(s_dyn);
+    stage_lut(s_lut2, descs[0].d.nm.lut2);
+    L = reinterpret_cast<const NormalLut*>(s_lut2);
+  } else if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
     extern __shared__ __align__(16) unsigned char s_dyn[];  // sizeof(NormalLut32), set at launch
     NormalLut32* s_lut32 = reinterpret_cast<NormalLut32*>(s_dyn);
     stage_lut(s_lut32, descs[0].d.nm.lut32);
@@ -356,15 +452,15 @@ __global__ void __launch_bounds__(256) k_transform(const uint32_t* __restrict__ 
 // Exhaustive calibration of the Normal fast path against the NumPy tables:
 // max relative error of r_fast (k >= 1; k = 0 must give r <= 2^-490), max
 // absolute error of c_fast, and the same for the float32 functions.
-__global__ void k_normal_calibrate(const double* rtab, const double* ctab, const NormalLut* lut,
-                                   const NormalLut32* lut32, unsigned long long* max_r_bits,
-                                   unsigned long long* max_c_bits) {
+__global__ void k_normal_calibrate(const double* ltab, const double* ctab, const NormalLut* lut,
+                                   const NormalLut32* lut32, const NormalLut2* lut2,
+                                   unsigned long long* max_r_bits, unsigned long long* max_c_bits) {
   __shared__ __align__(16) NormalLut s_lut;
   stage_lut(&s_lut, lut);  // the float32 tables are read from global memory here
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= (1u << 24)) return;
   const double inf = __longlong_as_double(0x7FF0000000000000ll);
-  const double rg = r_fast(k << 8, &s_lut, -0.5, 1.5), rn = rtab[k];
+  const double rg = r_fast(k << 8, &s_lut, -0.5, 1.5), rn = __dsqrt_rn(-2.0 * ltab[k]);  // NumPy's r
   double er;
   if (k == 0) er = (rn == 0.0 && rg >= 0.0 && rg <= 0x1p-490) ? 0.0 : inf;
   else er = (rg > 0.0 && rn > 0.0) ? fabs(rg - rn) / rg : inf;
@@ -374,13 +470,21 @@ __global__ void k_normal_calibrate(const double* rtab, const double* ctab, const
   if (k == 0) er32 = (r32 >= 0.0 && r32 <= 0x1p-49) ? 0.0 : inf;
   else er32 = (r32 > 0.0 && rn > 0.0) ? fabs(r32 - rn) / r32 : inf;
   const double ec32 = fabs(static_cast<double>(c32_fast(k << 8, lut32)) - ctab[k]);  // absolute
-  unsigned long long b[4] = {static_cast<unsigned long long>(__double_as_longlong(er)),
+  // NormalLut2 functions (tables read from global memory here)
+  const double r2 = r_fast2(k << 8, lut2, -0.5, 1.5);
+  double er2;
+  if (k == 0) er2 = (r2 >= 0.0 && r2 <= 0x1p-490) ? 0.0 : inf;
+  else er2 = (r2 > 0.0 && rn > 0.0) ? fabs(r2 - rn) / r2 : inf;
+  const double ec2 = fabs(c_fast2(k << 8, lut2) - ctab[k]);
+  unsigned long long b[6] = {static_cast<unsigned long long>(__double_as_longlong(er)),
                              static_cast<unsigned long long>(__double_as_longlong(ec)),
                              static_cast<unsigned long long>(__double_as_longlong(er32)),
-                             static_cast<unsigned long long>(__double_as_longlong(ec32))};
+                             static_cast<unsigned long long>(__double_as_longlong(ec32)),
+                             static_cast<unsigned long long>(__double_as_longlong(er2)),
+                             static_cast<unsigned long long>(__double_as_longlong(ec2))};
   // Non-negative doubles order like their bit patterns (NaN above inf); reduce per warp first.
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 6; ++i) {
     for (int o = 16; o > 0; o >>= 1) b[i] = max(b[i], __shfl_xor_sync(0xffffffffu, b[i], o));
   }
   if ((threadIdx.x & 31) == 0) {
@@ -388,7 +492,65 @@ __global__ void k_normal_calibrate(const double* rtab, const double* ctab, const
     atomicMax(max_c_bits, b[1]);
     atomicMax(max_r_bits + 2, b[2]);
     atomicMax(max_c_bits + 2, b[3]);
+    atomicMax(max_r_bits + 4, b[4]);
+    atomicMax(max_c_bits + 4, b[5]);
   }
+}
+
+// ExactMirror construction: thread t owns table points 16t .. 16t+15 (one code
+// word per function); exceptions are appended to unsorted lists.
+__device__ __forceinline__ uint32_t mirror_code(double np, double cu) {
+  const long long a = __double_as_longlong(np), b = __double_as_longlong(cu);
+  if ((a ^ b) < 0) return a == b ? 0u : 3u;  // sign differs (only near a zero crossing)
+  const long long d = a - b;
+  return d == 0 ? 0u : d == 1 ? 1u : d == -1 ? 2u : 3u;
+}
+__global__ void k_mirror_codes(const double* __restrict__ ltab, const double* __restrict__ ctab,
+                               uint32_t* code_l, uint32_t* code_c, uint32_t* xk_l, double* xv_l,
+                               uint32_t* xk_c, double* xv_c, unsigned int* counts, unsigned int cap) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (1u << 20)) return;
+  uint32_t wl = 0, wc = 0;
+  for (uint32_t i = 0; i < 16; ++i) {
+    const uint32_t k = 16u * t + i;
+    const double cl = log1p(-static_cast<double>(k) * 0x1p-24);
+    const double cc = cos(__dmul_rn(6.283185307179586, static_cast<double>(k) * 0x1p-24));
+    const uint32_t a = mirror_code(ltab[k], cl), b = mirror_code(ctab[k], cc);
+    wl |= a << (2 * i);
+    wc |= b << (2 * i);
+    if (a == 3u) {
+      const unsigned int n = atomicAdd(counts, 1u);
+      if (n < cap) {
+        xk_l[n] = k;
+        xv_l[n] = ltab[k];
+      }
+    }
+    if (b == 3u) {
+      const unsigned int n = atomicAdd(counts + 1, 1u);
+      if (n < cap) {
+        xk_c[n] = k;
+        xv_c[n] = ctab[k];
+      }
+    }
+  }
+  code_l[t] = wl;
+  code_c[t] = wc;
+}
+
+// Every table point through the compact mirror against NumPy's values, bit for bit.
+__global__ void k_mirror_verify(const ExactMirror M, const double* __restrict__ ltab,
+                                const double* __restrict__ ctab, unsigned long long* bad) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (1u << 24)) return;
+  const bool ok = __double_as_longlong(mirror_r(M, k)) == __double_as_longlong(__dsqrt_rn(-2.0 * ltab[k])) &&
+                  __double_as_longlong(mirror_c(M, k)) == __double_as_longlong(ctab[k]);
+  if (!ok) atomicAdd(bad, 1ull);
+}
+
+// Full-table fallback: r[k] = sqrt(-2 L[k]) in place.
+__global__ void k_r_from_l(double* t) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < (1u << 24)) t[k] = __dsqrt_rn(-2.0 * t[k]);
 }
 
 // ---------------------------------------------------------------------------
@@ -486,12 +648,19 @@ int canonicalize(const sdr_view& v, CanonView& cv) {
 
 // Per-device Normal mirror tables.
 struct NormalState {
-  double* rtab = nullptr;
+  double* rtab = nullptr;  // full tables: only if the compact mirror failed verification
   double* ctab = nullptr;
+  uint32_t* code = nullptr;  // 2 x 2^20 code words
+  uint32_t* xk = nullptr;    // exception keys (l then c)
+  double* xv = nullptr;      // exception values
+  int nx_l = 0, nx_c = 0;
+  uint64_t device_bytes = 0;  // mirror bytes resident on the device
+  double build_ms = 0;
   NormalLut* lut = nullptr;
   NormalLut32* lut32 = nullptr;
+  NormalLut2* lut2 = nullptr;
   unsigned long long* fallbacks = nullptr;
-  double err_r = 0, err_c = 0, err_r32 = 0, err_c32 = 0;
+  double err_r = 0, err_c = 0, err_r32 = 0, err_c32 = 0, err_r2 = 0, err_c2 = 0;
   bool loaded = false;
 };
 static std::mutex g_nm_mu;
@@ -552,6 +721,36 @@ static void build_normal_lut32(const NormalLut& h, NormalLut32& L) {
   L.trig_hi[2048] = make_float2(-1.0f, 0.0f);
   L.trig_hi[3072] = make_float2(0.0f, -1.0f);
 }
+// NormalLut2 (see dist_transforms.cuh), long double arithmetic.
+static void build_normal_lut2(NormalLut2& L) {
+  const long double C2 = static_cast<long double>(kTwoLn2);
+  for (int j = 0; j < 2048; ++j) {
+    const long double mc = 1.0L + (j + 0.5L) / 2048.0L;     // bucket centre of m
+    long double inv = nearbyintl(4096.0L / mc) / 4096.0L;    // multiple of 2^-12
+    if (j == 0) inv = 1.0L;                                  // n = 2^24 (k = 0): s = 0, A = 0
+    const long double T = (j < 1024) ? 2.0L * logl(inv) : 2.0L * logl(2.0L * inv) - C2;
+    L.logt[j].inv = static_cast<float>(inv);
+    L.logt[j].pad = 0.0f;
+    L.logt[j].T = static_cast<double>(T);
+  }
+  L.logt[0].T = 0x1p-1000;  // X > 0 at k = 0
+#if SDR_N2_COS2
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int i = 0; i < 4096; ++i) {
+    const long double a = 2.0L * pi * i / 4096.0L, b = 2.0L * pi * i / 16777216.0L;
+    L.cos_hi[i] = make_double2(static_cast<double>(cosl(a)), static_cast<double>(sinl(a)));
+    L.cos_lo[i] = make_double2(static_cast<double>(cosl(b)), static_cast<double>(sinl(b)));
+  }
+  L.cos_hi[0] = make_double2(1.0, 0.0);
+  L.cos_hi[1024] = make_double2(0.0, 1.0);
+  L.cos_hi[2048] = make_double2(-1.0, 0.0);
+  L.cos_hi[3072] = make_double2(0.0, -1.0);
+#else
+  NormalLut h;
+  build_normal_lut(h);
+  memcpy(L.trig, h.trig, sizeof(L.trig));
+#endif
+}
 static NormalState g_nm[64];
 
 static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) {
@@ -582,8 +781,20 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
       if (device < 0 || device >= 64 || !g_nm[device].loaded) return SDR_E_NOTABLES;
       P.nm.rtab = g_nm[device].rtab;
       P.nm.ctab = g_nm[device].ctab;
+      {
+        const NormalState& S = g_nm[device];
+        P.nm.em.code_l = S.code;
+        P.nm.em.code_c = S.code ? S.code + (1u << 20) : nullptr;
+        P.nm.em.xk_l = S.xk;
+        P.nm.em.xv_l = S.xv;
+        P.nm.em.xk_c = S.xk ? S.xk + S.nx_l : nullptr;
+        P.nm.em.xv_c = S.xv ? S.xv + S.nx_l : nullptr;
+        P.nm.em.nx_l = S.nx_l;
+        P.nm.em.nx_c = S.nx_c;
+      }
       P.nm.lut = g_nm[device].lut;
       P.nm.lut32 = g_nm[device].lut32;
+      P.nm.lut2 = g_nm[device].lut2;
       {
         // float64 fast path (see normal_certified): with Er, Ec the calibrated
         // errors of r_fast / c_fast and u = 2^-53,
@@ -600,6 +811,14 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
         P.nm.kr += 0x1p-51 * (1.0 + 0x1p-40);
         P.nm.k0 += fabs(P.mean) * 0x1p-51 * (1.0 + 0x1p-40);
         if (!(Er < 0x1p-20) || !(Ec < 0x1p-20)) P.nm.kr = INFINITY;  // calibration failed: exact path
+        {  // the same bound for the NormalLut2 functions (r_fast2 / c_fast2)
+          const double Er2 = g_nm[device].err_r2, Ec2 = g_nm[device].err_c2;
+          const double Erp2 = (Er2 / (1.0 - Er2) + 8.0 * u) * (1.0 + 0x1p-30);
+          P.nm.kr2 = 2.0 * (Erp2 + Ec2 * (1.0 + Erp2) + 2.01 * u) / (1.0 - Erp2) * (1.0 + 0x1p-30) +
+                     0x1p-51 * (1.0 + 0x1p-40);
+          P.nm.k02 = P.nm.k0;
+          if (!(Er2 < 0x1p-20) || !(Ec2 < 0x1p-20)) P.nm.kr2 = INFINITY;
+        }
         // float32 path (bfloat16 outputs): Er32, Ec32 the calibrated errors of
         // r32_fast / c32_fast;  |v32 - v_np| <= |std| r (Er32 + Ec32(1+Er32) + 2^-23)
         // + 2^-24 (|v32| + |mean|) + |std| 2^-49 (k = 0), doubled.
@@ -617,7 +836,7 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
         // Test hook: SDR_NORMAL_PATH=exact sends every element through the NumPy
         // tables, =f64 skips the float32 path (results must be identical).
         if (const char* path = getenv("SDR_NORMAL_PATH")) {
-          if (strcmp(path, "exact") == 0) P.nm.kr = P.nm.b32_r = INFINITY;
+          if (strcmp(path, "exact") == 0) P.nm.kr = P.nm.kr2 = P.nm.b32_r = INFINITY;
           if (strcmp(path, "f64") == 0) P.nm.b32_r = INFINITY;
         }
       }
@@ -652,7 +871,8 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
 // the 48 KiB static limit), with the opt-in attribute set before each launch.
 template <int DIST, int DT>
 static constexpr size_t fill_dyn_smem() {
-  return (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) ? sizeof(NormalLut32) : 0;
+  return uses_lut2<DIST, DT>() ? sizeof(NormalLut2)
+         : (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) ? sizeof(NormalLut32) : 0;
 }
 template <typename K>
 static void allow_dyn_smem(K kernel, size_t bytes) {
@@ -663,16 +883,17 @@ template <int DIST, int DT>
 static void launch_fill(const FillArgs& A0, bool fast, cudaStream_t s) {
   FillArgs A = A0;
   constexpr size_t dsm = fill_dyn_smem<DIST, DT>();
+  constexpr int nt = fill_threads<DIST, DT>();
   if (fast && A.aligned) {
     allow_dyn_smem(k_fill_fast<DIST, DT, true>, dsm);
-    const int grid = grid_for(k_fill_fast<DIST, DT, true>, A.nchunks, 256, dsm);
-    set_walk(A.walk, A.ix.cv, A.chunks_per_row, static_cast<uint64_t>(grid) * 256, kV);
-    launch_pdl(k_fill_fast<DIST, DT, true>, grid, s, A, dsm);
+    const int grid = grid_for(k_fill_fast<DIST, DT, true>, A.nchunks, nt, dsm);
+    set_walk(A.walk, A.ix.cv, A.chunks_per_row, static_cast<uint64_t>(grid) * nt, kV);
+    launch_pdl(k_fill_fast<DIST, DT, true>, grid, s, A, dsm, nt);
   } else if (fast) {
     allow_dyn_smem(k_fill_fast<DIST, DT, false>, dsm);
-    const int grid = grid_for(k_fill_fast<DIST, DT, false>, A.nchunks, 256, dsm);
-    set_walk(A.walk, A.ix.cv, A.chunks_per_row, static_cast<uint64_t>(grid) * 256, kV);
-    launch_pdl(k_fill_fast<DIST, DT, false>, grid, s, A, dsm);
+    const int grid = grid_for(k_fill_fast<DIST, DT, false>, A.nchunks, nt, dsm);
+    set_walk(A.walk, A.ix.cv, A.chunks_per_row, static_cast<uint64_t>(grid) * nt, kV);
+    launch_pdl(k_fill_fast<DIST, DT, false>, grid, s, A, dsm, nt);
   } else {
     k_fill_generic<DIST, DT><<<grid_for(k_fill_generic<DIST, DT>, A.ix.cv.numel, 256), 256, 0, s>>>(A);
   }
@@ -816,42 +1037,147 @@ int philox_blocks(const uint64_t* tau, const uint64_t* beta, int64_t n, uint64_t
   return check_launch();
 }
 
-int normal_tables_load(int device, const double* r_host, const double* c_host, double* er,
+// Build the per-device Normal mirror from the host NumPy tables L[k] =
+// log1p(-k 2^-24) and C[k] = cos((2 pi)(k 2^-24)): the full tables are
+// uploaded only transiently, to (1) derive the 2-bit corrections against the
+// device libm (ExactMirror), (2) verify that mirror on all 2^24 points of both
+// functions, and (3) calibrate the fast paths exhaustively.  Resident after
+// load: the 8 MiB of codes + exceptions (or, if verification failed, the full
+// tables as before) and the small fast-path LUTs.
+int normal_tables_load(int device, const double* l_host, const double* c_host, double* er,
                        double* ec) {
-  if (device < 0 || device >= 64 || r_host == nullptr || c_host == nullptr) return SDR_E_INVALID;
+  if (device < 0 || device >= 64 || l_host == nullptr || c_host == nullptr) return SDR_E_INVALID;
   std::lock_guard<std::mutex> lk(g_nm_mu);
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
   NormalState& S = g_nm[device];
   const size_t bytes = sizeof(double) << 24;
+  const unsigned int cap = 1u << 20;  // exception capacity per function
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  cudaEventRecord(t0);
   cudaError_t e = cudaSuccess;
-  if (S.rtab == nullptr) {
-    e = cudaMalloc(&S.rtab, bytes);
-    if (e == cudaSuccess) e = cudaMalloc(&S.ctab, bytes);
-    if (e == cudaSuccess) e = cudaMalloc(&S.fallbacks, 5 * sizeof(unsigned long long));
+  if (S.lut == nullptr) {
+    e = cudaMalloc(&S.fallbacks, 7 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMalloc(&S.lut, sizeof(NormalLut));
     if (e == cudaSuccess) e = cudaMalloc(&S.lut32, sizeof(NormalLut32));
+    if (e == cudaSuccess) e = cudaMalloc(&S.lut2, sizeof(NormalLut2));
     if (e == cudaSuccess) {
       NormalLut h;
       build_normal_lut(h);
       NormalLut32 h32;
       build_normal_lut32(h, h32);
+      std::vector<NormalLut2> h2(1);
+      build_normal_lut2(h2[0]);
       e = cudaMemcpy(S.lut, &h, sizeof(NormalLut), cudaMemcpyHostToDevice);
       if (e == cudaSuccess) e = cudaMemcpy(S.lut32, &h32, sizeof(NormalLut32), cudaMemcpyHostToDevice);
+      if (e == cudaSuccess) e = cudaMemcpy(S.lut2, h2.data(), sizeof(NormalLut2), cudaMemcpyHostToDevice);
     }
   }
-  if (e == cudaSuccess) e = cudaMemcpy(S.rtab, r_host, bytes, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(S.ctab, c_host, bytes, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemset(S.fallbacks, 0, 5 * sizeof(unsigned long long));
+  // a reload replaces the previous mirror
+  cudaFree(S.rtab);
+  cudaFree(S.ctab);
+  cudaFree(S.code);
+  cudaFree(S.xk);
+  cudaFree(S.xv);
+  S.rtab = S.ctab = nullptr;
+  S.code = S.xk = nullptr;
+  S.xv = nullptr;
+  S.nx_l = S.nx_c = 0;
+  S.loaded = false;
+  double *dl = nullptr, *dc = nullptr, *xv = nullptr;
+  uint32_t* xk = nullptr;
+  unsigned int* counts = nullptr;
+  if (e == cudaSuccess) e = cudaMalloc(&dl, bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&dc, bytes);
+  if (e == cudaSuccess) e = cudaMemcpy(dl, l_host, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dc, c_host, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(S.fallbacks, 0, 7 * sizeof(unsigned long long));
+  // (3) calibration of the fast paths against the full tables
   if (e == cudaSuccess) {
-    k_normal_calibrate<<<(1u << 24) / 256, 256>>>(S.rtab, S.ctab, S.lut, S.lut32, S.fallbacks + 1,
+    k_normal_calibrate<<<(1u << 24) / 256, 256>>>(dl, dc, S.lut, S.lut32, S.lut2, S.fallbacks + 1,
                                                   S.fallbacks + 2);
     e = cudaGetLastError();
   }
-  // fallbacks[1..4] = max err of r, c (float64 path) and r32, c32 (float32 path)
-  unsigned long long bits[4] = {0, 0, 0, 0};
-  if (e == cudaSuccess) e = cudaMemcpy(bits, S.fallbacks + 1, 4 * sizeof(bits[0]), cudaMemcpyDeviceToHost);
+  // (1) codes + unsorted exceptions
+  if (e == cudaSuccess) e = cudaMalloc(&S.code, 2 * sizeof(uint32_t) << 20);
+  if (e == cudaSuccess) e = cudaMalloc(&xk, 2 * sizeof(uint32_t) * cap);
+  if (e == cudaSuccess) e = cudaMalloc(&xv, 2 * sizeof(double) * cap);
+  if (e == cudaSuccess) e = cudaMalloc(&counts, 2 * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(counts, 0, 2 * sizeof(unsigned int));
+  if (e == cudaSuccess) {
+    k_mirror_codes<<<(1u << 20) / 256, 256>>>(dl, dc, S.code, S.code + (1u << 20), xk, xv, xk + cap,
+                                              xv + cap, counts, cap);
+    e = cudaGetLastError();
+  }
+  unsigned int nx[2] = {0, 0};
+  if (e == cudaSuccess) e = cudaMemcpy(nx, counts, sizeof(nx), cudaMemcpyDeviceToHost);
+  bool compact = e == cudaSuccess && nx[0] <= cap && nx[1] <= cap;
+  if (compact && nx[0] + nx[1] > 0) {  // sort each list by key on the host, upload packed
+    std::vector<uint32_t> hk(2 * cap);
+    std::vector<double> hv(2 * cap);
+    e = cudaMemcpy(hk.data(), xk, 2 * sizeof(uint32_t) * cap, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(hv.data(), xv, 2 * sizeof(double) * cap, cudaMemcpyDeviceToHost);
+    std::vector<uint32_t> sk;
+    std::vector<double> sv;
+    for (int f = 0; f < 2 && e == cudaSuccess; ++f) {
+      std::vector<std::pair<uint32_t, double>> kv(nx[f]);
+      for (unsigned int i = 0; i < nx[f]; ++i) kv[i] = {hk[f * cap + i], hv[f * cap + i]};
+      std::sort(kv.begin(), kv.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      for (const auto& p : kv) {
+        sk.push_back(p.first);
+        sv.push_back(p.second);
+      }
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&S.xk, sk.size() * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&S.xv, sv.size() * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpy(S.xk, sk.data(), sk.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(S.xv, sv.data(), sv.size() * sizeof(double), cudaMemcpyHostToDevice);
+  }
+  S.nx_l = static_cast<int>(nx[0]);
+  S.nx_c = static_cast<int>(nx[1]);
+  // (2) exhaustive verification of the compact mirror
+  unsigned long long bad = ~0ull;
+  if (compact && e == cudaSuccess) {
+    ExactMirror M{S.code, S.code + (1u << 20), S.xk, S.xv, S.xk ? S.xk + S.nx_l : nullptr,
+                  S.xv ? S.xv + S.nx_l : nullptr, S.nx_l, S.nx_c};
+    e = cudaMemset(S.fallbacks, 0, sizeof(unsigned long long));
+    if (e == cudaSuccess) {
+      k_mirror_verify<<<(1u << 24) / 256, 256>>>(M, dl, dc, S.fallbacks);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(&bad, S.fallbacks, sizeof(bad), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemset(S.fallbacks, 0, sizeof(unsigned long long));
+  }
+  compact = compact && bad == 0;
+  if (e == cudaSuccess && !compact) {  // keep the full tables (r derived from L on the device)
+    k_r_from_l<<<(1u << 24) / 256, 256>>>(dl);
+    e = cudaGetLastError();
+    S.rtab = dl;
+    S.ctab = dc;
+    dl = dc = nullptr;
+    cudaFree(S.code);
+    cudaFree(S.xk);
+    cudaFree(S.xv);
+    S.code = S.xk = nullptr;
+    S.xv = nullptr;
+  }
+  // fallbacks[1..6] = max err of r, c (NormalLut), r32, c32 (float32 path), r2, c2 (NormalLut2)
+  unsigned long long bits[6] = {0, 0, 0, 0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpy(bits, S.fallbacks + 1, 6 * sizeof(bits[0]), cudaMemcpyDeviceToHost);
+  cudaFree(dl);
+  cudaFree(dc);
+  cudaFree(xk);
+  cudaFree(xv);
+  cudaFree(counts);
+  cudaEventRecord(t1);
+  cudaEventSynchronize(t1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
   cudaSetDevice(prev);
   if (e != cudaSuccess) {
     set_cuda_error(e);
@@ -861,9 +1187,33 @@ int normal_tables_load(int device, const double* r_host, const double* c_host, d
   memcpy(&S.err_c, &bits[1], 8);
   memcpy(&S.err_r32, &bits[2], 8);
   memcpy(&S.err_c32, &bits[3], 8);
+  memcpy(&S.err_r2, &bits[4], 8);
+  memcpy(&S.err_c2, &bits[5], 8);
+  S.build_ms = ms;
+  S.device_bytes = compact ? (2 * sizeof(uint32_t) << 20) + (S.nx_l + S.nx_c) * (sizeof(uint32_t) + sizeof(double))
+                           : 2 * bytes;
+  S.device_bytes += sizeof(NormalLut) + sizeof(NormalLut32) + sizeof(NormalLut2) + 7 * sizeof(unsigned long long);
+  if (getenv("SDR_NORMAL_DEBUG"))
+    fprintf(stderr,
+            "sdr normal mirror: %s, exceptions log1p %d cos %d, verify-mismatch %llu, %.1f ms, %.2f MiB resident;"
+            " calibration r %.3g c %.3g r32 %.3g c32 %.3g r2 %.3g c2 %.3g\n",
+            compact ? "compact" : "full tables", S.nx_l, S.nx_c, bad, ms, S.device_bytes / 1048576.0, S.err_r,
+            S.err_c, S.err_r32, S.err_c32, S.err_r2, S.err_c2);
   S.loaded = true;
   if (er) *er = S.err_r;
   if (ec) *ec = S.err_c;
+  return SDR_OK;
+}
+
+int normal_mirror_info(int device, uint64_t* device_bytes, uint64_t* exceptions, int32_t* compact,
+                       double* build_ms) {
+  std::lock_guard<std::mutex> lk(g_nm_mu);
+  if (device < 0 || device >= 64 || !g_nm[device].loaded) return SDR_E_NOTABLES;
+  const NormalState& S = g_nm[device];
+  if (device_bytes) *device_bytes = S.device_bytes;
+  if (exceptions) *exceptions = static_cast<uint64_t>(S.nx_l + S.nx_c);
+  if (compact) *compact = S.rtab == nullptr ? 1 : 0;
+  if (build_ms) *build_ms = S.build_ms;
   return SDR_OK;
 }
 
@@ -889,8 +1239,11 @@ template <int DIST, int DT>
 static void launch_batch(const FillArgs* d_descs, const uint64_t* d_prefix, int n, uint64_t ntiles,
                          cudaStream_t s) {
   constexpr size_t dsm = fill_dyn_smem<DIST, DT>();
+  constexpr int nt = fill_threads<DIST, DT>();
   allow_dyn_smem(k_fill_batch<DIST, DT>, dsm);
-  k_fill_batch<DIST, DT><<<launch_grid(ntiles * 256, 256), 256, dsm, s>>>(d_descs, d_prefix, n, ntiles);
+  const int grid = uses_lut2<DIST, DT>() ? grid_for(k_fill_batch<DIST, DT>, ntiles * nt, nt, dsm)
+                                         : launch_grid(ntiles * nt, nt);
+  k_fill_batch<DIST, DT><<<grid, nt, dsm, s>>>(d_descs, d_prefix, n, ntiles);
 }
 
 template <int DIST>

@@ -205,32 +205,20 @@ def _check_transition(src: Placement, dst: Placement):
         raise RedistributeError(f"public transition into Partial is unsupported ({src}->{dst})")
 
 
-def _local_slice(t: torch.Tensor, tdim: int, placement: Placement, full_extent: int, P: int,
-                 k: int) -> torch.Tensor:
-    """Rank k's piece along tdim of a tensor holding the full extent."""
-    if isinstance(placement, InterleavedShard):
-        m = placement.interleaved_size
-        glen = full_extent // m
-        per = glen // P
-        shp = list(t.shape)
-        v = t.reshape(shp[:tdim] + [m, glen] + shp[tdim + 1:])
-        v = v.narrow(tdim + 1, k * per, per)
-        return v.reshape(shp[:tdim] + [m * per] + shp[tdim + 1:]).contiguous()
-    chunk = -(-full_extent // P)
-    lo = min(full_extent, k * chunk)
-    hi = min(full_extent, lo + chunk)
-    return t.narrow(tdim, lo, hi - lo).contiguous()
-
-
 def redistribute_many(xs: list[DTensor], dsts: list[ShardSpec],
                       ledger: comm.CollectiveLedger | None = None, *, mover=None) -> list[DTensor]:
     """Redistribute many DTensors at once.  Mesh dims are processed left to
     right for all tensors together; at each step the tensors that need a
     gather (resp. reduce-scatter / all-reduce) on the same fiber group are
-    coalesced into ONE collective."""
+    coalesced into ONE collective.  Calls whose every step runs on the peer
+    transport replay a cached plan (_Plan) instead of re-deriving it."""
     mover = DEFAULT_MOVER if mover is None else mover
     if len(xs) != len(dsts):
         raise ValueError("one destination spec per tensor")
+    if mover is DEFAULT_MOVER and xs and all(x.local.is_cuda for x in xs):
+        plan = _plan_for(xs, dsts)
+        if plan is not None:
+            return plan.run(xs, ledger)
     cur = []
     for x, d in zip(xs, dsts):
         if d.mesh != x.mesh:
@@ -269,17 +257,247 @@ def redistribute_many(xs: list[DTensor], dsts: list[ShardSpec],
             _fused_all_reduce(mesh, (md,), [(xs[i], cur[i]) for i in idxs], ledger, mover)
             for i in idxs:
                 cur[i][0] = cur[i][0].with_placement(md, Replicate())
-        for i in slices:
-            x, d = xs[i], dsts[i]
-            spec, loc = cur[i]
-            dst_p = d.placements[md]
-            P, k = x.mesh.sizes[md], x.coord[md]
-            cur[i] = [spec.with_placement(md, dst_p),
-                      _local_slice(loc, dst_p.dim, dst_p, x.shape[dst_p.dim], P, k)]
+        if slices:
+            _fused_slice(md, [(xs[i], dsts[i], cur[i]) for i in slices], mover)
     out = []
     for x, (spec, loc) in zip(xs, cur):
         out.append(DTensor(replace(x.meta, spec=spec), loc, x.coord))
     return out
+
+
+# ---------------------------------------------------------------------------
+# Plan cache: the host work of a peer-transport redistribute_many (placement
+# walk, geometry, bucket layout, heap lookup, ctypes member tables) depends only
+# on the tensors' metadata, so it is derived once per (shapes, dtypes, specs,
+# destinations, coordinate, transport) and replayed: per call only the outputs
+# are allocated, the data pointers patched and the launches issued.  Plans
+# exist for calls whose every step is a peer-transport gather / reduce-scatter
+# or a local slice; anything else (NCCL, all-reduce, graph capture, a regrown
+# heap) takes the general path below.
+# ---------------------------------------------------------------------------
+_PLANS: dict = {}
+_NO_PLAN = object()
+
+
+class _Plan:
+    def __init__(self, steps, metas, heaps):
+        self.steps = steps      # [(kind, data)] in execution order
+        self.metas = metas      # output DTensorMeta per tensor
+        self.heaps = heaps      # [(heap key, PeerHeap)] the steps use
+
+    def valid(self) -> bool:
+        return all(peer._HEAPS.get(k) is hp and hp.ok for k, hp in self.heaps)
+
+    def run(self, xs, ledger):
+        from . import _lib
+        cur = [x.local for x in xs]
+        if not all(t.is_contiguous() for t in cur):
+            raise ValueError("members must be contiguous")
+        dev = cur[0].device
+        with torch.cuda.device(dev):
+            s = _lib.stream_handle(dev)
+            for kind, d in self.steps:
+                if kind == "slice":
+                    idxs, shapes, full_arr, piece_arr, k, P = d
+                    outs = [torch.empty(shp, dtype=cur[i].dtype, device=dev) for i, shp in zip(idxs, shapes)]
+                    for j, i in enumerate(idxs):
+                        full_arr[j].data = cur[i].data_ptr() if cur[i].numel() else None
+                        piece_arr[j].data = outs[j].data_ptr() if outs[j].numel() else None
+                    _lib.check(_lib.LIB.sdr_slice_local(full_arr, piece_arr, len(idxs), k, P, s), "sdr_slice_local")
+                else:
+                    idxs, shapes, hp, buckets, led = d
+                    outs = [torch.empty(shp, dtype=cur[i].dtype, device=dev) for i, shp in zip(idxs, shapes)]
+                    for bidx, seg, a_in, a_out, dcode, nbytes in buckets:
+                        for j, b in enumerate(bidx):
+                            t_in, t_out = cur[idxs[b]], outs[b]
+                            a_in[j].data = t_in.data_ptr() if t_in.numel() else None
+                            a_out[j].data = t_out.data_ptr() if t_out.numel() else None
+                        if kind == "gather":
+                            hp.all_gather_arrays(a_in, a_out, len(bidx), s)
+                        else:
+                            hp.reduce_scatter_arrays(a_in, a_out, len(bidx), seg, dcode, s)
+                        if ledger is not None:
+                            ledger.record("all_gather" if kind == "gather" else "reduce_scatter", nbytes, *led)
+                for i, o in zip(idxs, outs):
+                    cur[i] = o
+        return [DTensor(m, loc, x.coord) for m, loc, x in zip(self.metas, cur, xs)]
+
+
+def _plan_key(xs, dsts):
+    return (tuple((x.meta.global_shape, x.meta.spec, x.meta.dtype, x.coord, tuple(x.local.shape)) for x in xs),
+            tuple(dsts), peer.transport(), xs[0].local.device.index)
+
+
+def _plan_for(xs, dsts):
+    if torch.cuda.is_current_stream_capturing():
+        return None
+    key = _plan_key(xs, dsts)
+    plan = _PLANS.get(key)
+    if plan is None:
+        plan = _build_plan(xs, dsts)
+        _PLANS[key] = plan
+        if len(_PLANS) > 4096:
+            _PLANS.pop(next(iter(_PLANS)))
+    if plan is _NO_PLAN:
+        return None
+    if not plan.valid():
+        _PLANS.pop(key, None)
+        return None
+    return plan
+
+
+def _build_plan(xs, dsts):
+    """Walk the transitions like redistribute_many, on metadata only; return
+    _NO_PLAN unless every collective step fits the peer transport.  The heap
+    lookups are the same collective calls the general path makes, in the same
+    order on every rank."""
+    from . import _lib
+    for x, d in zip(xs, dsts):
+        if d.mesh != x.mesh:
+            raise RedistributeError("redistribute requires the same mesh")
+        d.validate_for_shape(x.shape)
+        for md in range(x.mesh.ndim):
+            _check_transition(x.placements[md], d.placements[md])
+    if any(x.mesh != xs[0].mesh for x in xs):
+        return _NO_PLAN
+    mesh = xs[0].mesh
+    dev = xs[0].local.device
+    specs = [x.meta.spec for x in xs]
+    shapes = [tuple(x.local.shape) for x in xs]
+    steps, heaps = [], []
+    for md in range(mesh.ndim):
+        gathers, reduces, slices = [], {}, []
+        for i, (x, d) in enumerate(zip(xs, dsts)):
+            src_p, dst_p = specs[i].placements[md], d.placements[md]
+            if src_p == dst_p:
+                continue
+            if src_p.is_shard_like():
+                gathers.append(i)
+                if dst_p.is_shard_like():
+                    slices.append(i)
+            elif isinstance(src_p, Partial) and isinstance(dst_p, Replicate):
+                return _NO_PLAN  # all-reduce: general path
+            elif isinstance(src_p, Partial):
+                reduces.setdefault(x.dtype, []).append(i)
+            else:
+                slices.append(i)
+        P = mesh.sizes[md]
+        if (gathers or reduces) and P == 1:
+            return _NO_PLAN
+        if gathers or reduces:
+            group, fiber = comm.fiber_group(mesh, (md,))
+            k = fiber.index(comm.my_rank())
+        if gathers:
+            send, recv, outs = [], [], []
+            for i in gathers:
+                p = specs[i].placements[md]
+                E = xs[i].shape[p.dim]
+                shp = list(shapes[i])
+                o, rows_full, inner, chunk = _split_geometry(shp, p.dim, p, E, P)
+                n_loc = math.prod(shp)
+                es = xs[i].local.element_size()
+                send.append(Member(_Meta(es), o, n_loc // max(1, o * inner) if o * inner else 0, inner, chunk))
+                recv.append(Member(_Meta(es), o, rows_full, inner, chunk))
+                outs.append(tuple(shp[:p.dim] + [E] + shp[p.dim + 1:]))
+            sizes = _padded_bytes(send)
+            hp = peer.heap_for(group, fiber, dev, need_half=max(sizes, default=0))
+            if hp is None or max(sizes, default=0) > hp.half:
+                return _NO_PLAN
+            heaps.append(((tuple(fiber), dev.index), hp))
+            buckets = []
+            for bidx in _buckets(sizes, cap=hp.half):
+                sm, rm = [send[b] for b in bidx], [recv[b] for b in bidx]
+                seg = layout(sm)
+                for a, b_ in zip(sm, rm):
+                    b_.seg_off = a.seg_off
+                nbytes = sum(math.prod(outs[b]) * recv[b].tensor.element_size() for b in bidx)
+                buckets.append((bidx, seg, _template(sm), _template(rm), 0, nbytes))
+            steps.append(("gather", (gathers, outs, hp, buckets, (P, mesh.name, mesh.dim_names[md]))))
+            for i, shp in zip(gathers, outs):
+                specs[i] = specs[i].with_placement(md, Replicate())
+                shapes[i] = shp
+        for dt, idxs in reduces.items():
+            if not peer.reducible(dt):
+                return _NO_PLAN
+            full, piece, outs = [], [], []
+            for i in idxs:
+                dst_p = dsts[i].placements[md]
+                E = xs[i].shape[dst_p.dim]
+                shp = list(shapes[i])
+                o, rows_full, inner, chunk = _split_geometry(shp, dst_p.dim, dst_p, E, P)
+                pc = _piece_shape(shp, dst_p, E, P, k)
+                es = xs[i].local.element_size()
+                full.append(Member(_Meta(es), o, rows_full, inner, chunk))
+                piece.append(Member(_Meta(es), o, math.prod(pc) // max(1, o * inner) if o * inner else 0,
+                                    inner, chunk))
+                outs.append(tuple(pc))
+            sizes = _padded_bytes(full)
+            hp = peer.heap_for(group, fiber, dev, need_half=max(sizes, default=0) * P + 256 * P)
+            if hp is None:
+                return _NO_PLAN
+            cap = hp.half // P // 256 * 256
+            if max(sizes, default=0) > cap:
+                return _NO_PLAN
+            heaps.append(((tuple(fiber), dev.index), hp))
+            buckets = []
+            for bidx in _buckets(sizes, cap=cap):
+                fm, pm = [full[b] for b in bidx], [piece[b] for b in bidx]
+                seg = layout(fm, align=16)
+                for f, q in zip(fm, pm):
+                    q.seg_off = f.seg_off
+                nbytes = sum(math.prod(shapes[idxs[b]]) * full[b].tensor.element_size() for b in bidx)
+                buckets.append((bidx, seg, _template(fm), _template(pm), peer._SDR_DTYPE[dt], nbytes))
+            steps.append(("reduce", (idxs, outs, hp, buckets, (P, mesh.name, mesh.dim_names[md]))))
+            for i, shp in zip(idxs, outs):
+                specs[i] = specs[i].with_placement(md, dsts[i].placements[md])
+                shapes[i] = shp
+        if slices:
+            by_rank: dict = {}
+            for i in slices:
+                by_rank.setdefault((mesh.sizes[md], xs[i].coord[md]), []).append(i)
+            for (Ps, ks), idxs in by_rank.items():
+                full, piece, outs = [], [], []
+                for i in idxs:
+                    dst_p = dsts[i].placements[md]
+                    E = xs[i].shape[dst_p.dim]
+                    shp = list(shapes[i])
+                    o, rows_full, inner, chunk = _split_geometry(shp, dst_p.dim, dst_p, E, Ps)
+                    pc = _piece_shape(shp, dst_p, E, Ps, ks)
+                    es = xs[i].local.element_size()
+                    full.append(Member(_Meta(es), o, rows_full, inner, chunk))
+                    piece.append(Member(_Meta(es), o, math.prod(pc) // max(1, o * inner) if o * inner else 0,
+                                        inner, chunk))
+                    outs.append(tuple(pc))
+                steps.append(("slice", (idxs, outs, _template(full), _template(piece), ks, Ps)))
+                for i, shp in zip(idxs, outs):
+                    specs[i] = specs[i].with_placement(md, dsts[i].placements[md])
+                    shapes[i] = shp
+    metas = [replace(x.meta, spec=sp) for x, sp in zip(xs, specs)]
+    return _Plan(steps, metas, heaps)
+
+
+class _Meta:
+    """Stand-in for a member tensor while a plan is built (element size only)."""
+
+    def __init__(self, es):
+        self.es = es
+
+    def element_size(self):
+        return self.es
+
+
+def _template(members):
+    """sdr_pack_member array of `members` with null data pointers (patched per call)."""
+    from . import _lib
+    import ctypes as C
+    arr = (_lib.SdrPackMember * max(1, len(members)))()
+    for j, m in enumerate(members):
+        arr[j].data = None
+        arr[j].outer, arr[j].rows, arr[j].inner = m.outer, m.rows, m.inner
+        arr[j].chunk_rows, arr[j].seg_off = m.chunk, m.seg_off
+        arr[j].elem_bytes = m.tensor.element_size()
+    del C
+    return arr
 
 
 # Coalesced collectives are cut into buckets of about this many send bytes
@@ -525,6 +743,42 @@ def _peer_reduce_scatter(group, fiber, t, full_members, piece_members, ledger, m
         if ledger is not None:
             ledger.record("reduce_scatter", _real_bytes(fm), P, mesh.name, mesh.dim_names[md])
     return True
+
+
+def _fused_slice(md, items, mover):
+    """Replicate -> Shard (and the slice after a Shard -> Shard gather) on mesh
+    dim md for every item at once: rank k's ceil-block rows of each local
+    (dtensor.py:247-256, _local_slice :286-298) in ONE copy launch
+    (sdr_slice_local).  items: (x, dst spec, [spec, local])."""
+    full, piece, slots = [], [], []
+    for x, d, slot in items:
+        spec, loc = slot
+        dst_p = d.placements[md]
+        P, k = x.mesh.sizes[md], x.coord[md]
+        E = x.shape[dst_p.dim]
+        loc = loc.contiguous()
+        shp = list(loc.shape)
+        o, rows_full, inner, chunk = _split_geometry(shp, dst_p.dim, dst_p, E, P)
+        out = torch.empty(_piece_shape(shp, dst_p, E, P, k), dtype=loc.dtype, device=loc.device)
+        rows_k = out.numel() // max(1, o * inner) if o * inner else 0
+        full.append(Member(loc, o, rows_full, inner, chunk))
+        piece.append(Member(out, o, rows_k, inner, chunk))
+        slots.append((slot, spec.with_placement(md, dst_p), out, P, k))
+    by_rank = {}
+    for i, (_, _, _, P, k) in enumerate(slots):
+        by_rank.setdefault((P, k), []).append(i)
+    for (P, k), idx in by_rank.items():
+        cuda = [i for i in idx if full[i].tensor.is_cuda]
+        if cuda:
+            mover.slice_local([full[i] for i in cuda], [piece[i] for i in cuda], k, P)
+        for i in idx:  # host tensors (CPU DTensors, e.g. gloo runs): a plain view copy
+            if not full[i].tensor.is_cuda and piece[i].tensor.numel():
+                f, q = full[i], piece[i]
+                lo = min(f.rows, k * f.chunk)
+                q.tensor.view(f.outer, q.rows, f.inner).copy_(
+                    f.tensor.view(f.outer, f.rows, f.inner)[:, lo:lo + q.rows])
+    for slot, spec, out, _, _ in slots:
+        slot[0], slot[1] = spec, out
 
 
 def _piece_shape(shp, dst_p, E, P, k):

@@ -97,4 +97,14 @@ class CudaMover:
         _lib.check(st, "sdr_unpack_gathered")
 
 
+    def slice_local(self, full_members, piece_members, rank: int, nranks: int):
+        """Rank `rank`'s ceil-block rows of each full member into its piece
+        (Replicate -> Shard, dtensor.py:247-251)."""
+        fa, pa = self._arr(full_members), self._arr(piece_members)
+        dev = full_members[0].tensor.device
+        with torch.cuda.device(dev):
+            st = _lib.LIB.sdr_slice_local(fa, pa, len(full_members), rank, nranks, _lib.stream_handle(dev))
+        _lib.check(st, "sdr_slice_local")
+
+
 DEFAULT_MOVER = CudaMover()

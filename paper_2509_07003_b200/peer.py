@@ -135,7 +135,9 @@ class PeerHeap:
         want = sum(((i * 2654435761 + 97 * q) % 1000003) for q in range(self.P)).to(torch.int32)
         out = torch.empty_like(mine)
         global _TIMEOUT_NS
-        saved, _TIMEOUT_NS = _TIMEOUT_NS, min(_TIMEOUT_NS, int(60e9))
+        # soft barriers: a peer that never arrives sets this rank's timeout
+        # word and the check fails (NCCL fallback) instead of trapping
+        saved, _TIMEOUT_NS = _TIMEOUT_NS, -min(_TIMEOUT_NS, int(60e9))
         try:
             if not self.all_reduce([mine], [out]):
                 return False
@@ -143,7 +145,11 @@ class PeerHeap:
             _TIMEOUT_NS = saved
         torch.cuda.synchronize(self.dev)
         STATS["all_reduce"] -= 1  # not a user collective
-        return bool(torch.equal(out, want))
+        word = C.c_uint64()
+        with torch.cuda.device(self.dev):
+            _lib.check(_lib.LIB.sdr_peer_flag_read(self.own, _lib.MAX_PEERS, C.byref(word)),
+                       "sdr_peer_flag_read")
+        return bool(torch.equal(out, want)) and word.value == 0
 
     def _order(self):
         """All work on the heap must run in call order: the one-barrier-per-call
@@ -163,10 +169,10 @@ class PeerHeap:
         off = _lib.PEER_FLAG_BYTES + h * self.half
         return (C.c_void_p * self.P)(*[b + off for b in self.bases])
 
-    def _barrier(self):
+    def _barrier(self, stream=None):
         self.epoch += 1
         st = _lib.LIB.sdr_peer_barrier(self._flags, self.rank, self.P, self.epoch, _TIMEOUT_NS,
-                                       _stream(self.dev))
+                                       _stream(self.dev) if stream is None else stream)
         _lib.check(st, "sdr_peer_barrier")
 
     def _next_half(self) -> int:
@@ -180,19 +186,32 @@ class PeerHeap:
         from .movers import CudaMover
         if seg_bytes > self.half:
             raise ValueError("bucket larger than the peer heap half")
-        self._order()
-        h = self._next_half()
-        segs = self._half_ptrs(h)
-        arr = CudaMover._arr(send_members)
         with torch.cuda.device(self.dev):
-            st = _lib.LIB.sdr_pack_local(arr, len(send_members), segs[self.rank], _stream(self.dev))
-            _lib.check(st, "sdr_pack_local")
-            self._barrier()
-            arr = CudaMover._arr(recv_members)
-            st = _lib.LIB.sdr_unpack_gathered_peers(arr, len(recv_members), segs, self.P,
-                                                    _stream(self.dev))
-        _lib.check(st, "sdr_unpack_gathered_peers")
+            self.all_gather_arrays(CudaMover._arr(send_members), CudaMover._arr(recv_members),
+                                   len(send_members), _stream(self.dev))
+
+    def all_gather_arrays(self, send_arr, recv_arr, n: int, stream: int):
+        """all_gather on prebuilt sdr_pack_member arrays (the redistribute plan
+        cache patches their data pointers per call); device already current."""
+        self._order()
+        segs = self._half_ptrs(self._next_half())
+        _lib.check(_lib.LIB.sdr_pack_local(send_arr, n, segs[self.rank], stream), "sdr_pack_local")
+        self._barrier(stream)
+        _lib.check(_lib.LIB.sdr_unpack_gathered_peers(recv_arr, n, segs, self.P, stream),
+                   "sdr_unpack_gathered_peers")
         STATS["all_gather"] += 1
+
+    def reduce_scatter_arrays(self, full_arr, piece_arr, n: int, seg_bytes: int, dtype_code: int,
+                              stream: int):
+        """reduce_scatter on prebuilt member arrays (plan cache); device current."""
+        self._order()
+        bufs = self._half_ptrs(self._next_half())
+        _lib.check(_lib.LIB.sdr_pack_scatter(full_arr, n, bufs[self.rank], seg_bytes, self.P, stream),
+                   "sdr_pack_scatter")
+        self._barrier(stream)
+        _lib.check(_lib.LIB.sdr_reduce_scatter_peers(piece_arr, n, bufs, seg_bytes, self.P, self.rank,
+                                                     dtype_code, stream), "sdr_reduce_scatter_peers")
+        STATS["reduce_scatter"] += 1
 
     def reduce_scatter(self, full_members, piece_members, seg_bytes: int, dtype: torch.dtype):
         """P->S: pack my Partial tensors rank-major into my half, barrier, sum

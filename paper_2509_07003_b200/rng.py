@@ -218,12 +218,13 @@ _TABLE_ERRORS: dict[int, tuple[float, float]] = {}
 
 
 def numpy_normal_tables() -> tuple[np.ndarray, np.ndarray]:
-    """r[k] = sqrt(-2*log1p(-u)), c[k] = cos(2*pi*u), u = k*2^-24, k < 2^24,
-    evaluated with the same NumPy expressions as rng.py:152-155 on this host."""
+    """L[k] = log1p(-u), c[k] = cos(2*pi*u), u = k*2^-24, k < 2^24, evaluated
+    with the same NumPy expressions as rng.py:152-155 on this host (the
+    reference's r is sqrt(-2.0 * L), correctly rounded, so L pins it)."""
     u = np.arange(1 << 24, dtype=np.uint32).astype(np.float64) * 2.0 ** -24
-    r = np.sqrt(-2.0 * np.log1p(-u))
+    L = np.log1p(-u)
     c = np.cos(2.0 * np.pi * u)
-    return np.ascontiguousarray(r), np.ascontiguousarray(c)
+    return np.ascontiguousarray(L), np.ascontiguousarray(c)
 
 
 def ensure_normal_tables(device=None) -> tuple[float, float]:
@@ -234,12 +235,25 @@ def ensure_normal_tables(device=None) -> tuple[float, float]:
     with _TABLES_LOCK:
         if idx in _TABLE_ERRORS and _lib.LIB.sdr_normal_tables_loaded(idx):
             return _TABLE_ERRORS[idx]
-        r, c = numpy_normal_tables()
+        L, c = numpy_normal_tables()
         er, ec = C.c_double(), C.c_double()
-        st = _lib.LIB.sdr_normal_tables_load(idx, r.ctypes.data, c.ctypes.data, C.byref(er), C.byref(ec))
+        st = _lib.LIB.sdr_normal_tables_load(idx, L.ctypes.data, c.ctypes.data, C.byref(er), C.byref(ec))
         _lib.check(st, "sdr_normal_tables_load")
         _TABLE_ERRORS[idx] = (er.value, ec.value)
         return _TABLE_ERRORS[idx]
+
+
+def normal_mirror_info(device=None) -> dict:
+    """Resident bytes of the Normal mirror on `device`, its exception count,
+    whether the compact (2-bit correction) form is in use, and the build time
+    of the device part of the last load (ms)."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    nb, nx, cp, ms = C.c_uint64(), C.c_uint64(), C.c_int32(), C.c_double()
+    _lib.check(_lib.LIB.sdr_normal_mirror_info(idx, C.byref(nb), C.byref(nx), C.byref(cp), C.byref(ms)),
+               "sdr_normal_mirror_info")
+    return {"device_bytes": nb.value, "exceptions": nx.value, "compact": bool(cp.value),
+            "build_ms": ms.value}
 
 
 def normal_fallback_count(device=None) -> int:

@@ -60,3 +60,12 @@ class TorchCpuMover:
                 base = r * seg_bytes + m.seg_off
                 src = packed[base:base + m.seg_bytes].view(m.outer, m.chunk, m.inner * es)
                 full[:, lo:lo + n] = src[:, :n]
+
+    def slice_local(self, full_members, piece_members, rank, nranks):
+        for f, q in zip(full_members, piece_members):
+            if q.tensor.numel() == 0:
+                continue
+            es = f.tensor.element_size()
+            lo, n = _rank_rows(f.rows, f.chunk, rank)
+            src = f.tensor.contiguous().view(torch.uint8).reshape(f.outer, f.rows, f.inner * es)
+            q.tensor.view(torch.uint8).reshape(f.outer, n, f.inner * es).copy_(src[:, lo:lo + n])

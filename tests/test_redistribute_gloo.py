@@ -217,11 +217,23 @@ def _worker_golden_cuda(rank, ws, mesh_sizes, bucket_bytes=None, transport="nccl
         xs.append(x)
         dsts.append(dst)
         wants.append(want)
-    ys = redistribute_many(xs, dsts, comm.CollectiveLedger(), mover=mover)
+    led_general = comm.CollectiveLedger()
+    ys = redistribute_many(xs, dsts, led_general, mover=mover)
     for y, want, c in zip(ys, wants, cases):
         assert y.local.cpu().numpy().tobytes() == np.ascontiguousarray(want).tobytes(), ("many", c)
     from paper_2509_07003_b200 import peer
     assert (peer.STATS["all_gather"] > 0) == (transport == "peer")
+    # default mover: the plan cache (peer transport) builds on the first call
+    # and replays on the next; same outputs and the same ledger as above
+    for rep in range(3):
+        led = comm.CollectiveLedger()
+        ys = redistribute_many(xs, dsts, led)
+        for y, want, c in zip(ys, wants, cases):
+            assert y.local.cpu().numpy().tobytes() == np.ascontiguousarray(want).tobytes(), ("plan", rep, c)
+            assert y.placements == dsts[cases.index(c)].placements
+        assert led.entries == led_general.entries, rep
+    if transport == "peer":
+        assert any(p is not DT._NO_PLAN for p in DT._PLANS.values())
 
 
 @pytest.mark.gpu

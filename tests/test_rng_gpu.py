@@ -270,6 +270,30 @@ def test_normal_mirror_calibration_and_large_parity():
     assert after >= before
 
 
+def test_normal_mirror_is_compact_and_verified():
+    """The exact NumPy mirror is 2-bit ulp corrections of the device libm's
+    log1p / cos (8 MiB) plus an exception list, verified bit for bit on all
+    2^24 points of both functions at load (the load keeps the full 256 MiB
+    tables only if that verification fails).  A reload replaces it without
+    growing device memory."""
+    R.ensure_normal_tables()
+    info = R.normal_mirror_info()
+    assert info["compact"], info
+    assert info["device_bytes"] <= 8 * 2 ** 20 + 512 * 1024, info  # codes + exceptions + fast-path LUTs
+    idx = torch.cuda.current_device()
+    free0 = torch.cuda.mem_get_info()[0]
+    R._TABLE_ERRORS.pop(idx, None)  # force a rebuild from the host's NumPy
+    R.ensure_normal_tables()
+    torch.cuda.synchronize()
+    assert abs(torch.cuda.mem_get_info()[0] - free0) <= 16 * 2 ** 20
+    assert R.normal_mirror_info()["compact"]
+    # every element through the exact path (float64 output) vs the oracle
+    shape = (1 << 20,)
+    g = R.generate_global(shape, R.RngState(4242, 9), R.Normal(0.5, 3.0), np.float64)
+    ref = O.fill_global(shape, 4242, 9, 65536, "normal", (0.5, 3.0), np.float64)
+    assert _same(g, torch.from_numpy(ref))
+
+
 def test_64bit_indexing_beyond_2p32_elements():
     """One launch over > 2^32 elements (u8 Bernoulli, 4.3 GB) and a small
     window at the end of a 2^40-element tensor: 64-bit j, beta and chunk math."""
