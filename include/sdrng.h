@@ -111,9 +111,13 @@ int32_t sdr_fill(void* out, int32_t out_dtype, const sdr_dist* dist, const sdr_r
 int32_t sdr_transform(const uint32_t* w0, const uint32_t* w1, int64_t n, const sdr_dist* dist,
                       void* out, int32_t out_dtype, void* stream);
 
-/* Multi-tensor fill: n independent fills in ONE launch (Module.materialize,
- * model.py:121-132 -> generate_distributed, rng.py:220-235).  Each fill has
- * its own dist/rng/view/dtype.  Table arrays are host memory. */
+/* Multi-tensor fill: n independent fills in ONE launch per (distribution,
+ * dtype) group (Module.materialize, model.py:121-132 -> generate_distributed,
+ * rng.py:220-235).  Each fill has its own dist/rng/view/dtype -- every dtype
+ * sdr_fill accepts for that distribution (float for all five, int64/int32
+ * for RandInt, int/uint8/bool for Bernoulli).  Table arrays are host memory;
+ * the descriptors reach the device as kernel parameters (no host copy), so
+ * the call is stream-ordered end to end and may be captured in a CUDA graph. */
 int32_t sdr_fill_batch(void* const* outs, const int32_t* out_dtypes, const sdr_dist* dists,
                        const sdr_rng* rngs, const sdr_view* views, int32_t n, void* stream);
 

@@ -200,7 +200,44 @@ def _group_by_partial(grads):
     return groups, untouched
 
 
-def _reduce_buckets(members, dims, bucket_bytes, ledger, mover, rounds, label):
+REDUCE_MODES = ("exact", "switch")
+
+
+def reduce_mode(mode: str | None = None) -> str:
+    """How the P->R all-reduces of the gradient reductions sum.
+
+    "exact" (default): the peer-memory pull, ascending fiber-rank order --
+    bit-identical to the reference's `acc += b` loop (comm.py:91-101) for every
+    dtype.  "switch" (opt-in; argument or SDR_PR_REDUCE=switch): one NCCL
+    all-reduce per bucket over the flattened fiber communicator, which NCCL
+    runs as NVLS -- the reduction inside the NVSwitch (multimem ld_reduce) --
+    on nodes whose fabric supports it (NCCL_ALGO=NVLS forces it).  The
+    switch's summation order is not the ascending rank order, so float
+    results differ from the reference within `switch_sum_tolerance`;
+    integer sums stay exact."""
+    m = os.environ.get("SDR_PR_REDUCE", "exact") if mode is None else mode
+    if m not in REDUCE_MODES:
+        raise CommError(f"reduce mode must be one of {REDUCE_MODES}, not {m!r}")
+    return m
+
+
+def switch_sum_tolerance(abs_sum, P: int, dtype):
+    """Elementwise bound on |s_switch - s_ref| for a sum of P terms whose
+    absolute values sum to `abs_sum`, the two sums taken in any two orders
+    with round-to-nearest in `dtype`: each is within gamma_(P-1) * abs_sum of
+    the exact sum (Higham, Accuracy and Stability, eq. 4.4), so their
+    difference is within 2 gamma_(P-1) abs_sum, gamma_n = n u / (1 - n u),
+    u = 2^-(mantissa bits + 1).  Zero for integer dtypes."""
+    import torch
+    if not dtype.is_floating_point:
+        return 0 * abs_sum
+    u = {torch.float64: 2.0 ** -53, torch.float32: 2.0 ** -24, torch.bfloat16: 2.0 ** -8,
+         torch.float16: 2.0 ** -11}[dtype]
+    n = max(P - 1, 0)
+    return abs_sum * (2.0 * n * u / (1.0 - n * u))
+
+
+def _reduce_buckets(members, dims, bucket_bytes, ledger, mover, rounds, label, mode="exact"):
     from .dtensor import DTensor, _fused_all_reduce
     from .placement import Replicate
     from dataclasses import replace
@@ -208,7 +245,8 @@ def _reduce_buckets(members, dims, bucket_bytes, ledger, mover, rounds, label):
     out = {}
     for bucket in bucketize(members, bucket_bytes):
         slots = [[m.meta.spec, m.local] for m in bucket]
-        _fused_all_reduce(mesh, dims, list(zip(bucket, slots)), ledger, mover, ledger_mesh=label)
+        _fused_all_reduce(mesh, dims, list(zip(bucket, slots)), ledger, mover, ledger_mesh=label,
+                          switch=mode == "switch")
         rounds.append(("all_reduce", label, tuple(mesh.dim_names[d] for d in dims)))
         for m, (spec, loc) in zip(bucket, slots):
             for d in dims:
@@ -218,38 +256,44 @@ def _reduce_buckets(members, dims, bucket_bytes, ledger, mover, rounds, label):
 
 
 def bucketed_grad_reduce(grads, bucket_bytes: int = DEFAULT_BUCKET_BYTES, ledger=None, *,
-                         mover=None):
-    """Per Partial mesh dim, one all-reduce per bucket (comm.py:208-233)."""
+                         mover=None, reduce: str | None = None):
+    """Per Partial mesh dim, one all-reduce per bucket (comm.py:208-233).
+    `reduce`: "exact" (default) or "switch" (see reduce_mode)."""
     from .movers import DEFAULT_MOVER
     mover = DEFAULT_MOVER if mover is None else mover
+    mode = reduce_mode(reduce)
     groups, skipped = _group_by_partial(grads)
     result = {id(g): g for g in grads}
     rounds: list = []
     for (mesh, pdims, _), members in groups.items():
         current = members
         for d in pdims:
-            upd = _reduce_buckets(current, (d,), bucket_bytes, ledger, mover, rounds, mesh.name)
+            upd = _reduce_buckets(current, (d,), bucket_bytes, ledger, mover, rounds, mesh.name, mode)
             current = [upd[id(m)] for m in current]
         for before, after in zip(members, current):
             result[id(before)] = after
-    return [result[id(g)] for g in grads], {"skipped": skipped, "rounds": rounds}
+    return [result[id(g)] for g in grads], {"skipped": skipped, "rounds": rounds, "reduce": mode}
 
 
 def fused_nd_grad_reduce(grads, bucket_bytes: int = DEFAULT_BUCKET_BYTES, ledger=None, *,
-                         mover=None):
+                         mover=None, reduce: str | None = None):
     """All Partial dims of a group flattened into one fiber: ONE all-reduce
-    per bucket instead of one per dim (comm.py:236-289)."""
+    per bucket instead of one per dim (comm.py:236-289).
+    `reduce="switch"` (or SDR_PR_REDUCE=switch) sends each bucket through
+    NCCL on the flattened communicator -- in-switch NVLS reduction where the
+    fabric has it -- instead of the bit-exact peer pull (reduce_mode)."""
     from .movers import DEFAULT_MOVER
     mover = DEFAULT_MOVER if mover is None else mover
+    mode = reduce_mode(reduce)
     groups, skipped = _group_by_partial(grads)
     result = {id(g): g for g in grads}
     rounds: list = []
     for (mesh, pdims, _), members in groups.items():
         flat = mesh.flatten_dims([mesh.dim_names[d] for d in pdims])
-        upd = _reduce_buckets(members, tuple(pdims), bucket_bytes, ledger, mover, rounds, flat.name)
+        upd = _reduce_buckets(members, tuple(pdims), bucket_bytes, ledger, mover, rounds, flat.name, mode)
         for m in members:
             result[id(m)] = upd[id(m)]
-    return [result[id(g)] for g in grads], {"skipped": skipped, "rounds": rounds}
+    return [result[id(g)] for g in grads], {"skipped": skipped, "rounds": rounds, "reduce": mode}
 
 
 @dataclass(frozen=True)

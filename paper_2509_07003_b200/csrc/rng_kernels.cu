@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <type_traits>
 #include <vector>
@@ -1235,6 +1236,29 @@ int normal_fallback_count(int device, uint64_t* count) {
   return SDR_OK;
 }
 
+// Descriptor upload: the batch's FillArgs travel as kernel parameters (up to
+// kUploadN per launch, 29 KB) and are copied into the stream-ordered device
+// table by a tiny kernel, so the whole batched fill -- allocation, upload,
+// fill, free -- is stream-ordered and can be captured in a CUDA graph (no
+// pageable host copy).
+constexpr int kUploadN = 24;
+struct UploadArgs {
+  FillArgs a[kUploadN];
+  uint64_t prefix[kUploadN];
+  FillArgs* dst;
+  uint64_t* dst_prefix;
+  int n;
+};
+static_assert(sizeof(UploadArgs) <= 32000, "kernel parameter limit");
+
+__global__ void __launch_bounds__(256) k_upload_descs(const __grid_constant__ UploadArgs U) {
+  const int words = U.n * static_cast<int>(sizeof(FillArgs) / 16);
+  const uint4* src = reinterpret_cast<const uint4*>(U.a);
+  uint4* dst = reinterpret_cast<uint4*>(U.dst);
+  for (int w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
+  if (threadIdx.x < U.n) U.dst_prefix[threadIdx.x] = U.prefix[threadIdx.x];
+}
+
 template <int DIST, int DT>
 static void launch_batch(const FillArgs* d_descs, const uint64_t* d_prefix, int n, uint64_t ntiles,
                          cudaStream_t s) {
@@ -1246,24 +1270,10 @@ static void launch_batch(const FillArgs* d_descs, const uint64_t* d_prefix, int 
   k_fill_batch<DIST, DT><<<grid, nt, dsm, s>>>(d_descs, d_prefix, n, ntiles);
 }
 
-template <int DIST>
-static int dispatch_batch_dt(int dt, const FillArgs* d, const uint64_t* p, int n, uint64_t nt,
-                             cudaStream_t s) {
-  switch (dt) {
-    case SDR_F32: launch_batch<DIST, SDR_F32>(d, p, n, nt, s); break;
-    case SDR_F64: launch_batch<DIST, SDR_F64>(d, p, n, nt, s); break;
-    case SDR_BF16:
-      if constexpr (DIST != SDR_UNIFORM01 && DIST != SDR_RANDINT) launch_batch<DIST, SDR_BF16>(d, p, n, nt, s);
-      else return SDR_E_DTYPE;
-      break;
-    case SDR_F16:
-      if constexpr (DIST != SDR_UNIFORM01 && DIST != SDR_RANDINT) launch_batch<DIST, SDR_F16>(d, p, n, nt, s);
-      else return SDR_E_DTYPE;
-      break;
-    default:
-      return SDR_E_DTYPE;
-  }
-  return check_launch();
+// SDR_OK when distribution `kind` can produce dtype `dt` (the reference's
+// NumPy / ml_dtypes casts), else SDR_E_DTYPE / SDR_E_DIST.
+static int dist_dtype_ok(int kind, int dt) {
+  return with_dist(kind, [&](auto D) { return with_dtype<decltype(D)::value>(dt, [](auto) { return SDR_OK; }); });
 }
 
 int fill_batch(void* const* outs, const int32_t* dts, const sdr_dist* dists, const sdr_rng* rngs,
@@ -1280,14 +1290,15 @@ int fill_batch(void* const* outs, const int32_t* dts, const sdr_dist* dists, con
     if (rngs[i].theta < 1) return SDR_E_INVALID;
     const int dt = dts[i];
     if (dtype_size(dt) == 0 || dists[i].kind < 0 || dists[i].kind > 4) return SDR_E_DTYPE;
+    int st = dist_dtype_ok(dists[i].kind, dt);
+    if (st != SDR_OK) return st;
     CanonView cv;
-    int st = canonicalize(views[i], cv);
+    st = canonicalize(views[i], cv);
     if (st != SDR_OK) return st;
     Member m;
     memset(static_cast<void*>(&m), 0, sizeof(m));
     st = fill_dist_params(dists[i], dt, m.a.d, dev);
     if (st != SDR_OK) return st;
-    if (dt != SDR_F32 && dt != SDR_F64 && dt != SDR_BF16 && dt != SDR_F16) return SDR_E_DTYPE;
     if (cv.numel == 0) continue;
     if (outs[i] == nullptr) return SDR_E_INVALID;
     m.a.g = make_gen(rngs[i]);
@@ -1303,32 +1314,34 @@ int fill_batch(void* const* outs, const int32_t* dts, const sdr_dist* dists, con
     auto& G = groups[gi];
     if (G.empty()) continue;
     const int kind = gi / 8, dt = gi % 8, m = static_cast<int>(G.size());
-    std::vector<FillArgs> descs(m);
-    std::vector<uint64_t> prefix(m);
-    uint64_t tiles = 0;
-    for (int i = 0; i < m; ++i) {
-      descs[i] = G[i].a;
-      prefix[i] = tiles;
-      tiles += G[i].tiles;
-    }
     FillArgs* d_descs = nullptr;
     uint64_t* d_prefix = nullptr;
     cudaError_t e = cudaMallocAsync(&d_descs, sizeof(FillArgs) * m, s);
     if (e == cudaSuccess) e = cudaMallocAsync(&d_prefix, sizeof(uint64_t) * m, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_descs, descs.data(), sizeof(FillArgs) * m, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_prefix, prefix.data(), sizeof(uint64_t) * m, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) {
       set_cuda_error(e);
       return SDR_E_CUDA;
     }
-    int st;
-    switch (kind) {
-      case SDR_UNIFORM01: st = dispatch_batch_dt<SDR_UNIFORM01>(dt, d_descs, d_prefix, m, tiles, s); break;
-      case SDR_UNIFORM: st = dispatch_batch_dt<SDR_UNIFORM>(dt, d_descs, d_prefix, m, tiles, s); break;
-      case SDR_NORMAL: st = dispatch_batch_dt<SDR_NORMAL>(dt, d_descs, d_prefix, m, tiles, s); break;
-      case SDR_RANDINT: st = dispatch_batch_dt<SDR_RANDINT>(dt, d_descs, d_prefix, m, tiles, s); break;
-      default: st = dispatch_batch_dt<SDR_BERNOULLI>(dt, d_descs, d_prefix, m, tiles, s); break;
+    uint64_t tiles = 0;
+    for (int i0 = 0; i0 < m; i0 += kUploadN) {
+      auto U = std::make_unique<UploadArgs>();
+      U->n = std::min(kUploadN, m - i0);
+      U->dst = d_descs + i0;
+      U->dst_prefix = d_prefix + i0;
+      for (int i = 0; i < U->n; ++i) {
+        U->a[i] = G[i0 + i].a;
+        U->prefix[i] = tiles;
+        tiles += G[i0 + i].tiles;
+      }
+      k_upload_descs<<<1, 256, 0, s>>>(*U);
     }
+    int st = with_dist(kind, [&](auto D) {
+      constexpr int DIST = decltype(D)::value;
+      return with_dtype<DIST>(dt, [&](auto T) {
+        launch_batch<DIST, decltype(T)::value>(d_descs, d_prefix, m, tiles, s);
+        return check_launch();
+      });
+    });
     cudaFreeAsync(d_descs, s);
     cudaFreeAsync(d_prefix, s);
     if (st != SDR_OK) return st;

@@ -792,12 +792,14 @@ def _piece_shape(shp, dst_p, E, P, k):
     return out
 
 
-def _fused_all_reduce(mesh, dims, items, ledger, mover, ledger_mesh=None):
+def _fused_all_reduce(mesh, dims, items, ledger, mover, ledger_mesh=None, switch=False):
     """items: (x, [spec, local]); one all-reduce over the fiber spanned by
     `dims` (one dim, or several flattened -- N-d fusion) of all locals packed
     back to back.  Replaces each slot's local with a new reduced tensor (the
     inputs are never modified).  The ledger records the members' bytes under
-    `ledger_mesh` (the flattened mesh's name for N-d fusion, comm.py:270)."""
+    `ledger_mesh` (the flattened mesh's name for N-d fusion, comm.py:270).
+    switch=True skips the bit-exact peer pull: one NCCL all-reduce of the
+    packed bucket (NVLS in-switch reduction where available, comm.reduce_mode)."""
     ledger_mesh = mesh.name if ledger_mesh is None else ledger_mesh
     P = math.prod(mesh.sizes[d] for d in dims)
     if P == 1:
@@ -812,7 +814,7 @@ def _fused_all_reduce(mesh, dims, items, ledger, mover, ledger_mesh=None):
     # rank-chunked segment bytes per member (identical on every rank)
     sizes = [-(-(-(-m.tensor.numel() // P) * es) // 16) * 16 for m in members]
     hp = (peer.heap_for(group, fiber, t0.device, need_half=max(sizes, default=0) * (P + 1) + 256 * (P + 1))
-          if peer.reducible(t0.dtype) else None)
+          if peer.reducible(t0.dtype) and not switch else None)
     if hp is not None:
         # buckets of whole members whose segment fits a half P+1 times
         # (packed input + reduced chunk); all ranks take the same branch

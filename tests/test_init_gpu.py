@@ -294,3 +294,70 @@ def test_deferred_init_allocates_shard_sized_buffers():
     fc2 = torch.cat([shards[(k,)]["fc2.weight"] for k in range(4)], dim=0)
     assert torch.equal(bits(fc1), bits(ref["fc1.weight"].value))
     assert torch.equal(bits(fc2), bits(ref["fc2.weight"].value))
+
+
+def _mixed_params():
+    """Every (distribution, dtype) family the reference's Module.materialize can
+    meet (model.py:21-46): float weights, int / bool buffers; 30 RandInt
+    members cross one descriptor-upload chunk (24)."""
+    ps = {"w": I.Parameter((48, 40), R.Normal(0.0, 0.02), np.float32),
+          "wd": I.Parameter((9, 33), R.Uniform(-0.5, 0.5), np.float64),
+          "mask": I.Parameter((64, 17), R.Bernoulli(0.3), np.bool_),
+          "mask8": I.Parameter((40, 8), R.Bernoulli(0.7), np.uint8),
+          "ids32": I.Parameter((24, 16), R.RandInt(-3, 1000), np.int32)}
+    for i in range(30):
+        ps[f"ids{i}"] = I.Parameter((5 + i, 8), R.RandInt(-(1 << 40), 1 << 41), np.int64)
+    return ps
+
+
+def test_materialize_integer_and_bool_params():
+    """sdr_fill_batch fills int / bool parameters (RandInt, Bernoulli) too, bit
+    for bit equal to the sequential fill_random walk, sharded and unsharded."""
+    mesh = S.create_mesh([("tp", 4)])
+    for coord in [None, (1,), (3,)]:
+        params = _mixed_params()
+        specs = {} if coord is None else {n: ShardSpec(mesh, parse_placements("S(0)")) for n in params
+                                          if n != "wd"}
+        st = R.RngState(123, 0, 64)
+        got = I.materialize(params, st, specs, coord)
+        ref_state = R.RngState(123, 0, 64)
+        for name, p in params.items():
+            spec = specs.get(name)
+            if spec is None:
+                want = R.generate_global(p.shape, ref_state, p.dist, p.dtype)
+            else:
+                want = R.fill_random(local_shape_and_offset(spec, p.shape, coord), ref_state, p.dist, p.dtype)
+                ref_state.advance(int(np.prod(p.shape)))
+            assert got[name].dtype == want.dtype and torch.equal(bits(got[name]), bits(want)), (name, coord)
+        assert st.offset == ref_state.offset
+    # and against the oracle for one int and one bool member
+    out = I.materialize({"a": I.Parameter((7, 9), R.RandInt(5, 77), np.int64),
+                         "b": I.Parameter((13,), R.Bernoulli(0.25), np.bool_)}, R.RngState(9))
+    ref_a = O.fill_global((7, 9), 9, 0, 65536, "randint", (5, 77), np.int64)
+    ref_b = O.fill_global((13,), 9, 1, 65536, "bernoulli", (0.25,), np.bool_)
+    assert out["a"].cpu().numpy().tobytes() == ref_a.tobytes()
+    assert out["b"].cpu().numpy().tobytes() == ref_b.tobytes()
+
+
+def test_materialize_captures_in_cuda_graph():
+    """The batched init is stream-ordered end to end (descriptors as kernel
+    parameters, stream-ordered allocation): captured once, a replay rewrites
+    every parameter with the eager values."""
+    mesh = S.create_mesh([("tp", 2)])
+    specs = {n: ShardSpec(mesh, parse_placements("S(0)")) for n in _mixed_params()}
+    eager = I.materialize(_mixed_params(), R.RngState(31), specs, (1,))
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):  # warm-up off the capture (tables, allocator)
+        I.materialize(_mixed_params(), R.RngState(31), specs, (1,))
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    params = _mixed_params()
+    with torch.cuda.graph(g):
+        got = I.materialize(params, R.RngState(31), specs, (1,))
+    for t in got.values():
+        t.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    for name in eager:
+        assert torch.equal(bits(got[name]), bits(eager[name])), name

@@ -154,6 +154,75 @@ def test_bucketed_and_fused_grad_reduce_gloo():
     _spawn(_worker_fused_grads, 4)
 
 
+def _worker_switch_reduce(rank, ws, cuda=False):
+    """Opt-in reduce="switch" (NCCL / NVLS order, comm.reduce_mode): float
+    sums within comm.switch_sum_tolerance of the ascending-rank float64 sum,
+    integer sums exact, same buckets / rounds / ledger as the exact mode."""
+    from cpu_mover import TorchCpuMover
+    from paper_2509_07003_b200 import comm, create_mesh
+    from paper_2509_07003_b200.dtensor import from_local
+    from paper_2509_07003_b200.placement import ShardSpec, local_shape_and_offset, parse_placements
+    if cuda:  # exact mode on the peer transport (ranks sharing one GPU); switch mode via host-staged gloo
+        os.environ["SDR_COMM_CPU_STAGING"] = "1"
+        os.environ["SDR_TRANSPORT"] = "peer"
+        torch.cuda.set_device(0)
+        from paper_2509_07003_b200.movers import CudaMover
+        mover = CudaMover()
+    else:
+        mover = TorchCpuMover()
+    mesh = create_mesh([("dp", 2), ("tp", 2)])
+    coord = mesh.coords_of_rank(rank)
+    cases = [("P,P", (33, 7), torch.float32), ("P,S(0)", (9, 4), torch.float32), ("P,P", (50,), torch.bfloat16),
+             ("P,P", (6, 6), torch.float64), ("P,P", (5, 3), torch.int64)]
+    grads, parts = [], []
+    for i, (sp, shp, dt) in enumerate(cases):
+        spec = ShardSpec(mesh, parse_placements(sp))
+        v = local_shape_and_offset(spec, shp, coord)
+        g = torch.Generator().manual_seed(7 * i + rank)
+        loc = (torch.randint(-9, 10, v.local_shape, generator=g) if dt == torch.int64
+               else torch.randn(v.local_shape, generator=g) * 10 ** (i % 3)).to(dt)
+        grads.append(from_local(loc.cuda() if cuda else loc, spec, shp, coord))
+        # every fiber rank's local, in ascending fiber order, for the reference sum
+        grp, fib = comm.fiber_group(mesh, spec.partial_mesh_dims())
+        got = [torch.empty_like(loc) for _ in fib]
+        dist.all_gather(got, loc, group=grp)
+        parts.append(got)
+    l_ex, l_sw = comm.CollectiveLedger(), comm.CollectiveLedger()
+    out_e, rep_e = comm.fused_nd_grad_reduce(grads, bucket_bytes=256, ledger=l_ex, mover=mover)
+    out_s, rep_s = comm.fused_nd_grad_reduce(grads, bucket_bytes=256, ledger=l_sw, mover=mover, reduce="switch")
+    assert rep_s["reduce"] == "switch" and rep_e["reduce"] == "exact"
+    assert rep_s["rounds"] == rep_e["rounds"]
+    assert l_sw.entries == l_ex.entries
+    for (sp, shp, dt), got, e, s_ in zip(cases, parts, out_e, out_s):
+        acc = got[0].clone()
+        for b in got[1:]:
+            acc += b  # the reference's ascending loop (comm.py:91-101)
+        tol = comm.switch_sum_tolerance(sum(b.double().abs() for b in got), len(got), dt)
+        if cuda or not dt.is_floating_point:
+            assert torch.equal(e.local.cpu(), acc)  # peer pull (or integers): bit-identical
+        else:  # CPU: gloo's own order stands in for the pull
+            assert bool(((e.local.double() - acc.double()).abs() <= tol).all())
+        err = (s_.local.cpu().double() - acc.double()).abs()
+        assert bool((err <= tol).all()), (sp, dt, float((err - tol).max()))
+        assert s_.meta.spec == e.meta.spec
+    try:
+        comm.fused_nd_grad_reduce(grads, reduce="nvls")
+        raise AssertionError("bad reduce mode accepted")
+    except comm.CommError:
+        pass
+
+
+def test_switch_reduce_mode_tolerance_gloo():
+    _spawn(_worker_switch_reduce, 4)
+
+
+@pytest.mark.gpu
+def test_switch_reduce_mode_vs_peer_pull_multiprocess():
+    """GPU: the exact mode runs the peer pull (bit-identical to the
+    reference's ascending sum); switch mode stays within its tolerance."""
+    _spawn(_worker_switch_reduce, 4, True)
+
+
 def _worker_many_mixed(rank, ws):
     """Mixed dtypes in one coalesced gather; uneven shards padded per rank."""
     from cpu_mover import TorchCpuMover
