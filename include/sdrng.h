@@ -246,6 +246,20 @@ int32_t sdr_reduce_scatter_peers(const sdr_pack_member* members, int32_t n,
                                  const void* const* packed, int64_t seg_bytes, int32_t nranks,
                                  int32_t rank, int32_t dtype, void* stream);
 
+/* One whole peer collective per call (what the redistribute plan replays):
+ * the three launches above behind one entry point, with the segments at
+ * bases[q] + half_offset.  S->R: sdr_pack_local(send -> my segment),
+ * sdr_peer_barrier(epoch), sdr_unpack_gathered_peers(recv). */
+int32_t sdr_peer_all_gather(const sdr_pack_member* send, const sdr_pack_member* recv, int32_t n,
+                            void* const* bases, int32_t nranks, int32_t rank, int64_t half_offset,
+                            uint64_t epoch, int64_t timeout_ns, void* stream);
+/* P->S: sdr_pack_scatter(full -> my half, seg_bytes per rank),
+ * sdr_peer_barrier(epoch), sdr_reduce_scatter_peers(piece). */
+int32_t sdr_peer_reduce_scatter(const sdr_pack_member* full, const sdr_pack_member* piece, int32_t n,
+                                void* const* bases, int32_t nranks, int32_t rank, int64_t half_offset,
+                                int64_t seg_bytes, int32_t dtype, uint64_t epoch, int64_t timeout_ns,
+                                void* stream);
+
 /* INT32 pipe microbenchmark: measured IMAD.WIDE.U32 and LOP3 throughput
  * (ops/s) on `device`, for the roofline denominator. */
 int32_t sdr_probe_int32(int32_t device, double* imad_wide_per_s, double* lop3_per_s,

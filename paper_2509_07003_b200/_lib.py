@@ -118,6 +118,12 @@ def _load():
         "sdr_reduce_scatter_peers": (C.c_int32, [P(SdrPackMember), C.c_int32, P(C.c_void_p),
                                                  C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                                  C.c_void_p]),
+        "sdr_peer_all_gather": (C.c_int32, [P(SdrPackMember), P(SdrPackMember), C.c_int32, P(C.c_void_p),
+                                            C.c_int32, C.c_int32, C.c_int64, C.c_uint64, C.c_int64,
+                                            C.c_void_p]),
+        "sdr_peer_reduce_scatter": (C.c_int32, [P(SdrPackMember), P(SdrPackMember), C.c_int32,
+                                                P(C.c_void_p), C.c_int32, C.c_int32, C.c_int64, C.c_int64,
+                                                C.c_int32, C.c_uint64, C.c_int64, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -135,6 +141,7 @@ EXPORTED = (
     "sdr_pack_scatter", "sdr_pack_local", "sdr_unpack_local", "sdr_slice_local", "sdr_probe_int32",
     "sdr_peer_heap_alloc", "sdr_peer_heap_open", "sdr_peer_heap_close", "sdr_peer_heap_free",
     "sdr_peer_barrier", "sdr_peer_flag_read", "sdr_unpack_gathered_peers", "sdr_reduce_scatter_peers",
+    "sdr_peer_all_gather", "sdr_peer_reduce_scatter",
 )
 
 

@@ -171,6 +171,35 @@ int32_t sdr_reduce_scatter_peers(const sdr_pack_member* members, int32_t n,
                                    as_stream(stream));
 }
 
+int32_t sdr_peer_all_gather(const sdr_pack_member* send, const sdr_pack_member* recv, int32_t n,
+                            void* const* bases, int32_t nranks, int32_t rank, int64_t half_offset,
+                            uint64_t epoch, int64_t timeout_ns, void* stream) {
+  if (bases == nullptr || nranks < 1 || nranks > SDR_MAX_PEERS || rank < 0 || rank >= nranks || half_offset < 0)
+    return SDR_E_INVALID;
+  const void* segs[SDR_MAX_PEERS];
+  for (int q = 0; q < nranks; ++q) segs[q] = static_cast<const char*>(bases[q]) + half_offset;
+  const cudaStream_t s = as_stream(stream);
+  int st = sdr::pack_local(send, n, const_cast<void*>(segs[rank]), s);
+  if (st == SDR_OK) st = sdr::peer_barrier(bases, rank, nranks, epoch, timeout_ns, s);
+  if (st == SDR_OK) st = sdr::unpack_gathered_peers(recv, n, segs, nranks, s);
+  return st;
+}
+
+int32_t sdr_peer_reduce_scatter(const sdr_pack_member* full, const sdr_pack_member* piece, int32_t n,
+                                void* const* bases, int32_t nranks, int32_t rank, int64_t half_offset,
+                                int64_t seg_bytes, int32_t dtype, uint64_t epoch, int64_t timeout_ns,
+                                void* stream) {
+  if (bases == nullptr || nranks < 1 || nranks > SDR_MAX_PEERS || rank < 0 || rank >= nranks || half_offset < 0)
+    return SDR_E_INVALID;
+  const void* segs[SDR_MAX_PEERS];
+  for (int q = 0; q < nranks; ++q) segs[q] = static_cast<const char*>(bases[q]) + half_offset;
+  const cudaStream_t s = as_stream(stream);
+  int st = sdr::pack_scatter(full, n, const_cast<void*>(segs[rank]), seg_bytes, nranks, s);
+  if (st == SDR_OK) st = sdr::peer_barrier(bases, rank, nranks, epoch, timeout_ns, s);
+  if (st == SDR_OK) st = sdr::reduce_scatter_peers(piece, n, segs, seg_bytes, nranks, rank, dtype, s);
+  return st;
+}
+
 int32_t sdr_probe_int32(int32_t device, double* imad_wide_per_s, double* lop3_per_s,
                         double* philox_blocks_per_s) {
   return sdr::probe_int32(device, imad_wide_per_s, lop3_per_s, philox_blocks_per_s);

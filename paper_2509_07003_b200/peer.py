@@ -20,7 +20,8 @@ alternate halves, so one barrier per call is enough (include/sdrng.h).
 Selection (`transport()`): SDR_TRANSPORT=peer|nccl|auto (default auto = peer
 when every fiber rank is on this host and its device can reach ours; the
 decision is agreed by all fiber ranks).  SDR_PEER_HEAP_MB sizes the heap
-(default 256: two 128 MiB halves); buckets larger than a half go to NCCL,
+(default 1024: two 512 MiB halves -- one LLaMA-3-8B layer's S->R or P->S over
+a DP=2 fiber in one call); buckets larger than a half go to NCCL,
 and so do collectives issued while a CUDA graph is being captured.
 """
 
@@ -190,27 +191,30 @@ class PeerHeap:
             self.all_gather_arrays(CudaMover._arr(send_members), CudaMover._arr(recv_members),
                                    len(send_members), _stream(self.dev))
 
-    def all_gather_arrays(self, send_arr, recv_arr, n: int, stream: int):
+    def all_gather_arrays(self, send_arr, recv_arr, n: int, stream: int, ordered: bool = False):
         """all_gather on prebuilt sdr_pack_member arrays (the redistribute plan
-        cache patches their data pointers per call); device already current."""
-        self._order()
-        segs = self._half_ptrs(self._next_half())
-        _lib.check(_lib.LIB.sdr_pack_local(send_arr, n, segs[self.rank], stream), "sdr_pack_local")
-        self._barrier(stream)
-        _lib.check(_lib.LIB.sdr_unpack_gathered_peers(recv_arr, n, segs, self.P, stream),
-                   "sdr_unpack_gathered_peers")
+        cache patches their data pointers per call); device already current.
+        One C call: pack, barrier, pull (sdr_peer_all_gather).  `ordered`:
+        the caller has already run _order() for this stream."""
+        if not ordered:
+            self._order()
+        off = _lib.PEER_FLAG_BYTES + self._next_half() * self.half
+        self.epoch += 1
+        _lib.check(_lib.LIB.sdr_peer_all_gather(send_arr, recv_arr, n, self._flags, self.P, self.rank, off,
+                                                self.epoch, _TIMEOUT_NS, stream), "sdr_peer_all_gather")
         STATS["all_gather"] += 1
 
     def reduce_scatter_arrays(self, full_arr, piece_arr, n: int, seg_bytes: int, dtype_code: int,
-                              stream: int):
-        """reduce_scatter on prebuilt member arrays (plan cache); device current."""
-        self._order()
-        bufs = self._half_ptrs(self._next_half())
-        _lib.check(_lib.LIB.sdr_pack_scatter(full_arr, n, bufs[self.rank], seg_bytes, self.P, stream),
-                   "sdr_pack_scatter")
-        self._barrier(stream)
-        _lib.check(_lib.LIB.sdr_reduce_scatter_peers(piece_arr, n, bufs, seg_bytes, self.P, self.rank,
-                                                     dtype_code, stream), "sdr_reduce_scatter_peers")
+                              stream: int, ordered: bool = False):
+        """reduce_scatter on prebuilt member arrays (plan cache); device current.
+        One C call: pack, barrier, reduce pull (sdr_peer_reduce_scatter)."""
+        if not ordered:
+            self._order()
+        off = _lib.PEER_FLAG_BYTES + self._next_half() * self.half
+        self.epoch += 1
+        _lib.check(_lib.LIB.sdr_peer_reduce_scatter(full_arr, piece_arr, n, self._flags, self.P, self.rank, off,
+                                                    seg_bytes, dtype_code, self.epoch, _TIMEOUT_NS, stream),
+                   "sdr_peer_reduce_scatter")
         STATS["reduce_scatter"] += 1
 
     def reduce_scatter(self, full_members, piece_members, seg_bytes: int, dtype: torch.dtype):
@@ -306,7 +310,7 @@ def heap_for(group, fiber, dev: torch.device, need_half: int = 0):
     key = (tuple(fiber), dev.index)
     hp = _HEAPS.get(key)
     if hp is None:
-        half = int(float(os.environ.get("SDR_PEER_HEAP_MB", "256")) * (1 << 20)) // 2
+        half = int(float(os.environ.get("SDR_PEER_HEAP_MB", "1024")) * (1 << 20)) // 2
         hp = _HEAPS[key] = PeerHeap(group, fiber, dev, max(half, min(need_half, _max_half())))
         if not hp.ok and transport() == "peer":
             raise RuntimeError(f"SDR_TRANSPORT=peer but fiber {fiber} cannot map peer memory")

@@ -35,6 +35,29 @@ for _ in range(20):
     torch.cuda.synchronize()
     dist.barrier()
 ts.sort()
+# breakdown: the peer C call (pack + barrier + pull launches) and the output allocation
+from paper_2509_07003_b200 import peer as _peer, dtensor as _dt
+acc = {"c_call": 0.0, "alloc": 0.0, "n": 0}
+_ag, _al = _peer.PeerHeap.all_gather_arrays, _dt._alloc_outputs
+def _ag_t(self, *a, **k):
+    t = time.perf_counter(); r = _ag(self, *a, **k); acc["c_call"] += time.perf_counter() - t; return r
+def _al_t(*a, **k):
+    t = time.perf_counter(); r = _al(*a, **k); acc["alloc"] += time.perf_counter() - t; return r
+_peer.PeerHeap.all_gather_arrays, _dt._alloc_outputs = _ag_t, _al_t
+t_all = 0.0
+for _ in range(20):
+    t0 = time.perf_counter()
+    redistribute_many(xs, dsts)
+    t_all += time.perf_counter() - t0
+    acc["n"] += 1
+    torch.cuda.synchronize()
+    dist.barrier()
+_peer.PeerHeap.all_gather_arrays, _dt._alloc_outputs = _ag, _al
+if rank == 0:
+    n = acc["n"]
+    print(f"breakdown per call: total {t_all/n*1e6:.0f} us = peer C call(s) {acc['c_call']/n*1e6:.0f} us "
+          f"+ output allocation {acc['alloc']/n*1e6:.0f} us + the rest (plan lookup, pointer patching) "
+          f"{(t_all-acc['c_call']-acc['alloc'])/n*1e6:.0f} us", flush=True)
 if rank == 0:
     print(f"host time per redistribute_many (9 members, peer): median {ts[len(ts)//2]*1e6:.0f} us, "
           f"min {ts[0]*1e6:.0f} us", flush=True)
@@ -42,11 +65,11 @@ if os.environ.get("SDR_PROFILE_HOST") == "1":
     import cProfile, pstats
     pr = cProfile.Profile()
     pr.enable()
-    for _ in range(20):
+    for _ in range(200):
         redistribute_many(xs, dsts)
     pr.disable()
     torch.cuda.synchronize()
     if rank == 0:
-        pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+        pstats.Stats(pr).sort_stats("tottime").print_stats(25)
 dist.barrier()
 dist.destroy_process_group()
