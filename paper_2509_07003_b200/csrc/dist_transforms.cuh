@@ -212,6 +212,13 @@ __host__ __device__ __forceinline__ uint32_t dlo(double d) {
 #endif
 }
 
+// MUFU.RSQ without the denormal fix-up rsqrtf() adds (callers clamp x >= 2^-126).
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ double rsqrt_seed(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -242,7 +249,7 @@ __device__ __forceinline__ double r_fast(uint32_t w0, const NormalLut* L, double
   // float32 MUFU.RSQ seed (~2^-23 vs ~2^-20 for MUFU.RSQ64H): after the one
   // Newton step r is good to ~2^-45, so ~8x fewer elements miss
   // certification; the clamp keeps k = 0 (X ~ 2^-1000) finite.
-  double h = static_cast<double>(rsqrtf(fmaxf(__double2float_rn(X), 0x1p-126f)));
+  double h = static_cast<double>(rsqrt_ftz(fmaxf(__double2float_rn(X), 0x1p-126f)));
 #else
   double h = rsqrt_seed(X);
 #endif
@@ -313,7 +320,7 @@ __device__ __forceinline__ double r_fast2(uint32_t w0, const NormalLut2* L, doub
   // float32 MUFU.RSQ seed (~2^-23; the f64 MUFU.RSQ64H seed is ~2^-20): one
   // Newton step then leaves ~2^-45 instead of ~2^-39.5, so ~64x fewer
   // elements miss certification.  The clamp keeps k = 0 (X = 2^-1000) finite.
-  const double h = static_cast<double>(rsqrtf(fmaxf(__double2float_rn(X), 0x1p-126f)));
+  const double h = static_cast<double>(rsqrt_ftz(fmaxf(__double2float_rn(X), 0x1p-126f)));
 #else
   double h = rsqrt_seed(X);
 #if SDR_R2_SEED == 2
