@@ -38,22 +38,27 @@ template <int XT> struct DropT { using T = typename St<XT>::T; };
 template <int XT, int YT>
 __device__ __forceinline__ typename St<YT>::T drop_apply(const DropArgs& A, typename St<XT>::T x,
                                                          bool keep, bool& nan) {
+  // (x * m) * scale == x * (m ? scale : 0) bit for bit: x * 1 is exact, and
+  // (x * 0) * scale == x * 0 (a signed zero, or NaN for NaN / inf x) since the
+  // float32 / float64 scale is positive and finite (1/(1-p) <= 2^53 for any
+  // double p < 1) -- one multiply per element less.
   if constexpr (XT == SDR_F32) {
-    const float y = __fmul_rn(__fmul_rn(x, keep ? 1.0f : 0.0f), A.scale32);
+    const float y = __fmul_rn(x, keep ? A.scale32 : 0.0f);
     nan = y != y;
     return y;
   } else if constexpr (XT == SDR_F64) {
-    const double y = __dmul_rn(__dmul_rn(x, keep ? 1.0 : 0.0), A.scale64);
+    const double y = __dmul_rn(x, keep ? A.scale64 : 0.0);
     nan = y != y;
     return y;
   } else if constexpr (XT == SDR_BF16) {
     const float xf = __uint_as_float(static_cast<uint32_t>(x) << 16);
-    const float y = __fmul_rn(__fmul_rn(xf, keep ? 1.0f : 0.0f), A.scale32);
+    const float y = __fmul_rn(xf, keep ? A.scale32 : 0.0f);
     nan = y != y;
     if constexpr (YT == SDR_F32) return y;
     else return bf16_bits(y);
   } else {  // SDR_F16: x*m exact in f16, then RNE(x16 * scale16)
     const __half xh = __ushort_as_half(x);
+    // (no folding here: scale16 overflows to inf for p > 1 - 2^-16, and (x * 0) * inf is NaN)
     const __half xm = __hmul(xh, keep ? __ushort_as_half(0x3C00) : __ushort_as_half(0));
     const uint16_t y = __half_as_ushort(__hmul(xm, __ushort_as_half(A.scale16)));
     nan = (y & 0x7FFFu) > 0x7C00u;
@@ -204,7 +209,7 @@ __global__ void __launch_bounds__(256, SDR_DROP_MINB) k_dropout_fast(const __gri
           uint32_t wd;
           memcpy(&wd, &xv[e & ~1], 4);
           const float xf = (e & 1) ? bf16_hi(wd) : bf16_lo(wd);
-          const float r = __fmul_rn(__fmul_rn(xf, keep[e] ? 1.0f : 0.0f), A.scale32);
+          const float r = __fmul_rn(xf, keep[e] ? A.scale32 : 0.0f);  // == (x * m) * scale (drop_apply)
           nan[e] = r != r;
           if constexpr (YT == SDR_F32) yv[e] = r;
           else yv[e] = bf16_bits(r);

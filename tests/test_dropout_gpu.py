@@ -53,7 +53,7 @@ def test_golden_dropout(golden):
 
 
 @pytest.mark.parametrize("dt", ["float32", "bfloat16", "float16", "float64"])
-@pytest.mark.parametrize("p", [0.1, 0.5, 0.999])
+@pytest.mark.parametrize("p", [0.1, 0.5, 0.999, 0.99999])  # 0.99999: float16 scale overflows to inf
 def test_sharded_dropout_matches_oracle(dt, p):
     shape = (4, 96, 80)
     g = torch.Generator().manual_seed(5)
