@@ -278,11 +278,13 @@ __device__ __forceinline__ double c_fast(uint32_t w1, const NormalLut* L) { retu
 // the float64 ones.  Tables (NormalLut32): logt[j] = (-2 mult_j 2^-23,
 // 2 ln(inv_j)) (+2^-100 at j = 0), trig[i] = (cos, sin)(i pi/1024).
 __device__ __forceinline__ float r32_fast(uint32_t w0, const NormalLut32* L) {
-  const uint32_t hw = __float_as_uint(__uint2float_rn(0x1000000u - (w0 >> 8)));  // n, exact
+  // n = 2^24 - k by a float add (exact; one integer op less than the integer
+  // subtract), e via a shift-add the compiler can fuse (LEA.HI)
+  const uint32_t hw = __float_as_uint(16777216.0f - __uint2float_rn(w0 >> 8));    // n, exact
   const float2 tb = lut_at(L->logt, (hw >> 11) & 0xFF8u);                         // j = hw[22:14]
   const float s = fmaf(__uint_as_float((hw & 0x007FFFFFu) | 0x4B000000u), tb.x, 2.0f);  // -2t
   const float g = fmaf(s * s, fmaf(s, 1.0f / 12.0f, 0.25f), s);                   // -2 log1p(t)
-  const float e = __uint_as_float(0x4B000000u | ((hw + 0x400000u) >> 23)) - 8388759.0f;  // e, exact
+  const float e = __uint_as_float(((hw + 0x400000u) >> 23) + 0x4B000000u) - 8388759.0f;  // e, exact
   const float X = fmaf(e, -1.38629436f, tb.y + g);                                // -2 ln w
   float h;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(h) : "f"(X));
@@ -307,13 +309,16 @@ __device__ __forceinline__ float c32_fast(uint32_t w1, const NormalLut32* L) {
 // T_0 carries 2^-1000 so X > 0 (r ~ 2^-500, never certified).
 constexpr double kTwoLn2 = 0x1.62e42fefa39efp0;  // RN(2 ln 2)
 __device__ __forceinline__ double r_fast2(uint32_t w0, const NormalLut2* L, double nh, double th) {
-  const uint32_t hw = __float_as_uint(__uint2float_rn(0x1000000u - (w0 >> 8)));  // n, exact
+  const uint32_t hw = __float_as_uint(16777216.0f - __uint2float_rn(w0 >> 8));    // n, exact
   const LogEnt2 tb = lut_at(L->logt, (hw >> 8) & 0x7FF0u);                         // j = hw[22:12]
   const float m = __uint_as_float((hw & 0x007FFFFFu) | 0x3F800000u);
   const float s = fmaf(m, tb.inv, -1.0f);                                          // exact
   const float t = s * fmaf(s, 0.5f, -0.666666686534881591796875f);
   const double sd = static_cast<double>(s);
-  const double A = fma(__uint2double_rn(151u - (hw >> 23)), kTwoLn2, tb.T);        // (24-E) 2ln2 + T_j
+  // 24 - E = (2^23 + 151) - float(2^23 + biased E), exact in float32 (a
+  // shift-add and an FADD instead of an integer subtract and I2F.F64)
+  const float em = 8388759.0f - __uint_as_float((hw >> 23) + 0x4B000000u);
+  const double A = fma(static_cast<double>(em), kTwoLn2, tb.T);                  // (24-E) 2ln2 + T_j
   const double s2 = sd * sd;                                                       // exact
   const double X = fma(sd, -2.0, A) + fma(s2, static_cast<double>(t), s2);        // -2 ln w
 #if SDR_R2_SEED == 1
@@ -346,50 +351,53 @@ __device__ __forceinline__ double c_fast2(uint32_t w1, const NormalLut2* L) {
 #endif
 }
 
-// Every double within B of v rounds (RN) to the same float32 as v.  Checked on
-// v's bits: d = distance of v to the nearest float32 rounding midpoint in ulps
-// of v (low 29 mantissa bits against 2^28), against 2^sh > B / ulp(v) from the
-// exponent fields (B >= |v| 2^-51 keeps sh >= 1).  Normal float32 range only:
-// zero, subnormal and overflowing v are never certified.
-__device__ __forceinline__ bool f32_round_certified(double v, double B) {
-  const uint32_t vh = dhi(v);
-  const uint32_t ev = (vh >> 20) & 0x7FFu;
-  const uint32_t sh = (dhi(B) >> 20) + 53u - ev;  // B < 2^(eB+1), ulp(v) = 2^(ev-1075)
-  const int32_t t = static_cast<int32_t>(dlo(v) & 0x1FFFFFFFu) - 0x10000000;
-  uint32_t q;
-  asm("shf.r.clamp.b32 %0, %1, 0, %2;" : "=r"(q) : "r"(static_cast<uint32_t>(abs(t))), "r"(sh));
-  return (ev - 897u) <= 253u && q != 0u;
-}
-
 template <int DT>
 __device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, const NormalLut* L,
                                                            uint32_t w0, uint32_t w1);
 
+// A chunk of bfloat16 normals on the float32 path.  Elements go in pairs: one
+// F2FP packs the two lower ends RD(v - B) and one the two upper ends RU(v + B)
+// (bf16(RN32(.)) is monotone, so an element is certified iff both ends round
+// to the same bfloat16); the lower pack is the output word, and the XOR of the
+// two packs is OR-accumulated (one LOP3 per pair).  Only the rare branch looks
+// at which element differs; those take the float64 path, then the exact one.
 template <int NE>
 __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLut32* L32,
                                                   const uint32_t* w0, const uint32_t* w1, uint16_t* out) {
-  uint32_t badmask = 0;
+  static_assert(NE % 2 == 0, "elements go in pairs");
+  uint32_t diff = 0, hiw[NE / 2];
 #pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    const float r = r32_fast(w0[e], L32), c = c32_fast(w1[e], L32);
-    const float v = fmaf(P.nm.std32, r * c, P.nm.mean32);
-    // |v - v_numpy| <= r*b32_r + b32_c   (host: bound terms)
-    const float B = fmaf(r, P.nm.b32_r, P.nm.b32_c);  // |v| term folded (host)
-    // bf16(RN32(.)) is monotone: [v-B, v+B] rounds to one bfloat16 iff both ends do
-    const __nv_bfloat162 pk = __floats2bfloat162_rn(__fsub_rd(v, B), __fadd_ru(v, B));
-    uint32_t lh;
-    memcpy(&lh, &pk, 4);
-    out[e] = static_cast<uint16_t>(lh);
-    badmask |= ((lh ^ (lh >> 16)) & 0xFFFFu) ? (1u << e) : 0u;
+  for (int e = 0; e < NE; e += 2) {
+    float lo[2], hi[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float r = r32_fast(w0[e + i], L32), c = c32_fast(w1[e + i], L32);
+      const float v = fmaf(P.nm.std32, r * c, P.nm.mean32);
+      // |v - v_numpy| <= r*b32_r + b32_c   (host: bound terms; |v| term folded)
+      const float B = fmaf(r, P.nm.b32_r, P.nm.b32_c);
+      lo[i] = __fsub_rd(v, B);
+      hi[i] = __fadd_ru(v, B);
+    }
+    const __nv_bfloat162 pl = __floats2bfloat162_rn(lo[0], lo[1]), ph = __floats2bfloat162_rn(hi[0], hi[1]);
+    uint32_t l32, h32;
+    memcpy(&l32, &pl, 4);
+    memcpy(&h32, &ph, 4);
+    out[e] = static_cast<uint16_t>(l32);
+    out[e + 1] = static_cast<uint16_t>(l32 >> 16);
+    diff |= l32 ^ h32;
+    hiw[e / 2] = h32;
   }
-  if (__builtin_expect(badmask != 0, 0)) {
-#if SDR_COUNT_F32_MISS
-    atomicAdd(P.nm.fallbacks, static_cast<unsigned long long>(__popc(badmask)));
-#endif
-    // float64 certified path (tables read through L1/L2), then the exact NumPy tables
+  if (__builtin_expect(diff != 0, 0)) {
 #pragma unroll
-    for (int e = 0; e < NE; ++e)
-      if (badmask & (1u << e)) out[e] = normal_value<SDR_BF16>(P, P.nm.lut, w0[e], w1[e]);
+    for (int e = 0; e < NE; ++e) {
+      if (out[e] != static_cast<uint16_t>(hiw[e / 2] >> (16 * (e & 1)))) {
+#if SDR_COUNT_F32_MISS
+        atomicAdd(P.nm.fallbacks, 1ull);
+#endif
+        // float64 certified path (tables read through L1/L2), then the exact mirror
+        out[e] = normal_value<SDR_BF16>(P, P.nm.lut, w0[e], w1[e]);
+      }
+    }
   }
 }
 
@@ -495,34 +503,46 @@ __device__ __forceinline__ void normal_chunk(const DistP& P, const NormalLut* L,
   }
 }
 // A chunk of float32 / float16 normals on the NormalLut2 tables: all r, all c,
-// combine, certify (float32: on the bits of v; float16: by rounding v +- B),
-// one branch for the rare uncertified elements (exact NumPy tables).
+// combine, certify by rounding v - B and v + B (the cast is monotone), one
+// branch for the rare uncertified elements (exact NumPy mirror).  The
+// certification test costs one LOP3 per element: the XOR of the two roundings
+// is OR-accumulated over the chunk, and only the rare branch looks at which
+// element differs.
 template <int DT, int NE>
 __device__ __forceinline__ void normal_chunk2(const DistP& P, const NormalLut2* L, const uint32_t* w0,
                                               const uint32_t* w1, typename St<DT>::T* out) {
+  using T = typename St<DT>::T;
   double rs[NE], c[NE];
 #pragma unroll
   for (int e = 0; e < NE; ++e) rs[e] = r_fast2(w0[e], L, P.nm.nh, P.nm.th);
 #pragma unroll
   for (int e = 0; e < NE; ++e) c[e] = c_fast2(w1[e], L);
-  uint32_t badmask = 0;
+  uint32_t diff = 0;
+  T hib[NE];
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
     const double v = fma(rs[e], c[e], P.mean);
     const double B = fma(rs[e], P.nm.kr2, P.nm.k02);
+    const T lo = from_f64<DT>(v - B), hi = from_f64<DT>(v + B);
+    out[e] = lo;
+    hib[e] = hi;
+    uint32_t a, b;
     if constexpr (DT == SDR_F32) {
-      out[e] = __double2float_rn(v);
-      badmask |= f32_round_certified(v, B) ? 0u : (1u << e);
+      a = __float_as_uint(lo);
+      b = __float_as_uint(hi);
     } else {
-      const auto lo = from_f64<DT>(v - B), hi = from_f64<DT>(v + B);
-      out[e] = lo;
-      badmask |= lo == hi ? 0u : (1u << e);
+      a = lo;
+      b = hi;
     }
+    diff |= a ^ b;
   }
-  if (__builtin_expect(badmask != 0, 0)) {
+  if (__builtin_expect(diff != 0, 0)) {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
-      if (badmask & (1u << e)) {
+      bool same;
+      if constexpr (DT == SDR_F32) same = __float_as_uint(out[e]) == __float_as_uint(hib[e]);
+      else same = out[e] == hib[e];
+      if (!same) {
         atomicAdd(P.nm.fallbacks, 1ull);
         out[e] = normal_exact<DT>(P, w0[e], w1[e]);
       }
