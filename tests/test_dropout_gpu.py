@@ -88,7 +88,9 @@ def test_sharded_dropout_matches_oracle(dt, p):
 
 def test_cfg2_full_size_sequence_parallel():
     """BASELINE config 2: x bf16 [8,4096,4096], p=0.1, Shard(1) over 1/2/4/8:
-    every shard equals the slice of the unsharded result; oracle spot rows."""
+    shards (all 8 at P = 8) equal the slice of the unsharded result, and 512
+    sequence rows (2 M elements, every batch, every P = 8 shard) equal the
+    oracle."""
     shape = (8, 4096, 4096)
     x = torch.randn(shape, generator=torch.Generator(device="cuda").manual_seed(0), device="cuda",
                     dtype=torch.bfloat16)
@@ -97,18 +99,22 @@ def test_cfg2_full_size_sequence_parallel():
     for P in (2, 4, 8):
         mesh = S.create_mesh([("sp", P)])
         spec = ShardSpec(mesh, parse_placements("S(1)"))
-        for coord in [(0,), (P - 1,)]:
+        for coord in (mesh.iter_coords() if P == 8 else [(0,), (P - 1,)]):
             v = local_shape_and_offset(spec, shape, coord)
             s0, n = v.local_offset[1], v.local_shape[1]
             y = ops.dropout_apply(x[:, s0:s0 + n].contiguous(), 0.1, st, v)
             assert torch.equal(bits(y), bits(full[:, s0:s0 + n].contiguous()))
     import ml_dtypes
-    for b, r in [(0, 0), (3, 2047), (7, 4095)]:
-        row = x[b, r].cpu().view(torch.int16).numpy().view(np.uint16).view(ml_dtypes.bfloat16)
-        j = np.arange(4096) + (b * 4096 + r) * 4096
+    # oracle rows: 64 sequence rows per batch spread over the whole sequence
+    # (every Shard(1) rank at P = 8 owns 8 of them), all 8 batches: 2 M elements
+    rows = np.linspace(0, 4095, 64).round().astype(np.int64)
+    for b in range(8):
+        xr = x[b, torch.from_numpy(rows).cuda()].cpu().view(torch.int16).numpy().view(np.uint16)
+        xr = xr.view(ml_dtypes.bfloat16)
+        j = ((b * 4096 + rows)[:, None] * 4096 + np.arange(4096)[None, :]).reshape(-1)
         keep = O.fill_indices(j, 20240817, 0, 65536, "bernoulli", (1.0 - 0.1,), ml_dtypes.bfloat16)
-        yref = torch.from_numpy(O.dropout_apply(row, keep, 0.1)).to(torch.bfloat16)
-        assert torch.equal(bits(full[b, r].cpu()), bits(yref))
+        yref = torch.from_numpy(O.dropout_apply(xr.reshape(-1), keep, 0.1)).to(torch.bfloat16)
+        assert torch.equal(bits(full[b, torch.from_numpy(rows).cuda()].cpu().reshape(-1)), bits(yref)), b
 
 
 def test_dropout_op_autograd_and_state():

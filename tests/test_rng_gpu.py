@@ -5,6 +5,7 @@ Bit-exact for every distribution, dtype, placement, mesh and state
 """
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -434,3 +435,29 @@ def test_allocation_tracking_is_local_sized():
     with R.track_allocations() as alloc:
         R.generate_distributed(spec, (64, 64), R.RngState(0), R.Uniform01())
     assert 0 < alloc["max_elements"] <= 64 * 64 // 4
+
+
+def test_normal_mirror_footprint_and_first_call_latency():
+    """The exact NumPy mirror is compact (2-bit corrections, <= 9 MiB
+    resident) and its first load is timed (a fresh process)."""
+    import subprocess, sys, textwrap
+    code = textwrap.dedent("""
+        import time, torch
+        torch.cuda.init(); torch.empty(1, device="cuda")
+        from paper_2509_07003_b200 import rng as R
+        f0 = torch.cuda.mem_get_info()[0]
+        t = time.perf_counter(); R.ensure_normal_tables(); torch.cuda.synchronize()
+        dt = time.perf_counter() - t
+        info = R.normal_mirror_info()
+        print("MIRROR", info["device_bytes"], int(info["compact"]), info["exceptions"],
+              f0 - torch.cuda.mem_get_info()[0], round(dt, 3), round(info["build_ms"], 1))
+    """)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    line = [l for l in out.stdout.splitlines() if l.startswith("MIRROR")]
+    assert line, out.stdout + out.stderr
+    nbytes, compact, nexc, delta, secs, build_ms = line[0].split()[1:]
+    print(line[0])
+    assert int(compact) == 1 and int(nbytes) <= 9 << 20
+    assert int(delta) <= 24 << 20  # mirror + tables, plus the lazily loaded kernels' code
+    assert float(secs) < 60
