@@ -205,6 +205,21 @@ def _check_transition(src: Placement, dst: Placement):
         raise RedistributeError(f"public transition into Partial is unsupported ({src}->{dst})")
 
 
+def _check_path(x: DTensor, dst: ShardSpec):
+    """Validate the whole left-to-right walk before any data moves: every
+    intermediate spec must be valid (the reference raises PlacementError at
+    the step that would shard a tensor dim twice, e.g. [P,S(0)] -> [S(0),R]),
+    so a coalesced call fails on every rank before its first collective."""
+    if dst.mesh != x.mesh:
+        raise RedistributeError("redistribute requires the same mesh")
+    dst.validate_for_shape(x.shape)
+    spec = x.meta.spec
+    for md in range(x.mesh.ndim):
+        _check_transition(spec.placements[md], dst.placements[md])
+        if spec.placements[md] != dst.placements[md]:
+            spec = spec.with_placement(md, dst.placements[md])
+
+
 def redistribute_many(xs: list[DTensor], dsts: list[ShardSpec],
                       ledger: comm.CollectiveLedger | None = None, *, mover=None) -> list[DTensor]:
     """Redistribute many DTensors at once.  Mesh dims are processed left to
@@ -215,18 +230,13 @@ def redistribute_many(xs: list[DTensor], dsts: list[ShardSpec],
     mover = DEFAULT_MOVER if mover is None else mover
     if len(xs) != len(dsts):
         raise ValueError("one destination spec per tensor")
+    for x, d in zip(xs, dsts):
+        _check_path(x, d)
     if mover is DEFAULT_MOVER and xs and all(x.local.is_cuda for x in xs):
         plan = _plan_for(xs, dsts)
         if plan is not None:
             return plan.run(xs, ledger)
-    cur = []
-    for x, d in zip(xs, dsts):
-        if d.mesh != x.mesh:
-            raise RedistributeError("redistribute requires the same mesh")
-        d.validate_for_shape(x.shape)
-        for md in range(x.mesh.ndim):
-            _check_transition(x.placements[md], d.placements[md])
-        cur.append([x.meta.spec, x.local])
+    cur = [[x.meta.spec, x.local] for x in xs]
     ndim_max = max((x.mesh.ndim for x in xs), default=0)
     for md in range(ndim_max):
         gathers, reduces, allreds, slices = {}, {}, {}, []

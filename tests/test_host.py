@@ -352,3 +352,21 @@ def test_cost_model_ac07_and_ledger_bytes():
         ledger = CollectiveLedger()
         all_reduce([torch.zeros(128, dtype=torch.float64) for _ in range(P)], ledger)
         assert ledger.entries[0].bytes_per_device == Fraction(2 * 1024 * (P - 1), P)
+
+
+def test_redistribute_rejects_double_sharding_path_like_reference():
+    """The reference raises PlacementError when a left-to-right step would
+    shard a tensor dim by two mesh dims (dtensor.py:208-258), e.g.
+    [S(0),S(1)] -> [S(1),S(0)]; redistribute_many checks the whole walk
+    before any collective, so it raises the same error on every rank."""
+    import torch
+    from paper_2509_07003_b200 import create_mesh
+    from paper_2509_07003_b200.dtensor import from_local, redistribute_many
+    from paper_2509_07003_b200.placement import PlacementError, ShardSpec, local_shape_and_offset, parse_placements
+    mesh = create_mesh([("a", 2), ("b", 2)])
+    for s, d in [("S(0),S(1)", "S(1),S(0)"), ("P,S(0)", "S(0),R"), ("R,S(0)", "S(0),R")]:
+        src = ShardSpec(mesh, parse_placements(s))
+        v = local_shape_and_offset(src, (6, 8), (0, 0))
+        x = from_local(torch.zeros(v.local_shape), src, (6, 8), (0, 0))
+        with pytest.raises(PlacementError):
+            redistribute_many([x], [ShardSpec(mesh, parse_placements(d))])

@@ -549,3 +549,137 @@ def _worker_uneven_rounds(rank, ws):
 
 def test_grad_buckets_use_local_nbytes_max_uneven_gloo():
     _spawn(_worker_uneven_rounds, 4)
+
+
+def _random_cases(seed, mesh_sizes, n=10):
+    """Seeded random redistribute cases (identical on every rank): shapes with
+    uneven and empty shards, source placements S / R / P (a tensor dim
+    sharded by at most one mesh dim), destinations S / R, mixed dtypes."""
+    rs = np.random.default_rng(seed)
+    cases = []
+    for _ in range(n):
+        nd = int(rs.integers(1, 4))
+        shape = tuple(int(v) for v in rs.integers(1, 23, nd))
+
+        def placements(allow_p):
+            out, used = [], set()
+            for _ in mesh_sizes:
+                free = [d for d in range(nd) if d not in used]
+                kind = int(rs.integers(0, 3 if allow_p else 2))
+                if kind == 0 and free:
+                    d = int(rs.choice(free))
+                    used.add(d)
+                    out.append(("S", d))
+                elif kind == 2:
+                    out.append(("P",))
+                else:
+                    out.append(("R",))
+            return tuple(out)
+        src, dst = placements(True), placements(False)
+        has_p = any(p[0] == "P" for p in src)
+        dt = ["float32", "float64", "bfloat16", "int64"][int(rs.integers(0, 4))]
+        cases.append((shape, src, dst, dt, int(rs.integers(0, 1 << 30)), has_p))
+    return cases
+
+
+def _path_valid(shape, src, dst, mesh):
+    """Whether every intermediate spec of the left-to-right walk is valid."""
+    from paper_2509_07003_b200.placement import PlacementError, ShardSpec, parse_placements
+    cur = list(src)
+    try:
+        for md in range(len(src)):
+            if cur[md] != dst[md]:
+                cur[md] = dst[md]
+                ShardSpec(mesh, parse_placements(_pl_text(cur))).validate_for_shape(shape)
+    except PlacementError:
+        return False
+    return True
+
+
+def _local_shape(shape, pl, mesh_sizes, coord):
+    from oracle import rng_oracle as O
+    base = tuple(("R",) if p[0] == "P" else p for p in pl)
+    return tuple(len(i) for i in O.window(shape, base, mesh_sizes, coord))
+
+
+def _pl_text(pl):
+    return ",".join("R" if p[0] == "R" else "P" if p[0] == "P" else f"S({p[1]})" for p in pl)
+
+
+def _worker_random_peer(rank, ws, mesh_sizes, seeds):
+    """Random coalesced redistributes through the peer transport (ranks share
+    one GPU, CUDA IPC heaps): every rank's output equals the oracle's
+    (oracle/redist_oracle.py, pinned by the golden cases) bit for bit, for
+    float data too -- the pulls sum in the reference's ascending order."""
+    os.environ["SDR_COMM_CPU_STAGING"] = "1"
+    os.environ["SDR_TRANSPORT"] = "peer"
+    torch.cuda.set_device(0)
+    import ml_dtypes
+    from oracle import redist_oracle as RO, rng_oracle as O
+    from paper_2509_07003_b200 import create_mesh, peer
+    from paper_2509_07003_b200.dtensor import from_local, redistribute_many
+    from paper_2509_07003_b200.placement import ShardSpec, parse_placements
+    np_dt = {"float32": np.float32, "float64": np.float64, "bfloat16": ml_dtypes.bfloat16, "int64": np.int64}
+    t_dt = {"float32": torch.float32, "float64": torch.float64, "bfloat16": torch.bfloat16, "int64": torch.int64}
+    mesh = create_mesh([(f"m{j}", s) for j, s in enumerate(mesh_sizes)])
+    me = mesh.coords_of_rank(rank)
+    from paper_2509_07003_b200.placement import PlacementError
+    for seed in seeds:
+        xs, dsts, wants = [], [], []
+        for shape, src, dst, dt, vseed, _ in _random_cases(seed, mesh_sizes):
+            if not _path_valid(shape, src, dst, mesh):
+                # the reference raises PlacementError at the step that would shard a
+                # tensor dim twice; so does redistribute, before any data moves
+                x = from_local(torch.zeros(_local_shape(shape, src, mesh_sizes, me), device="cuda"),
+                               ShardSpec(mesh, parse_placements(_pl_text(src))), shape, me)
+                with pytest.raises(PlacementError):
+                    redistribute_many([x], [ShardSpec(mesh, parse_placements(_pl_text(dst)))])
+                continue
+            rs = np.random.default_rng(vseed)
+            pdims = [i for i, p in enumerate(src) if p[0] == "P"]
+            base = tuple(("R",) if p[0] == "P" else p for p in src)
+            glob, locs = {}, {}
+            for c in O.mesh_coords(mesh_sizes):
+                key = tuple(c[i] for i in pdims)  # one global per Partial coordinate
+                if key not in glob:
+                    g = rs.standard_normal(shape) * 10.0 ** rs.integers(-2, 3, shape)
+                    glob[key] = (np.rint(g * 100) if dt == "int64" else g).astype(np_dt[dt])
+                idx = O.window(shape, base, mesh_sizes, c)
+                locs[c] = np.ascontiguousarray(glob[key][np.ix_(*idx)])
+            out, _ = RO.redistribute(locs, shape, src, mesh_sizes, dst)
+            mine = locs[me]
+            t = torch.from_numpy(mine.view(np.uint16)).view(torch.bfloat16) if dt == "bfloat16" \
+                else torch.from_numpy(mine)
+            xs.append(from_local(t.cuda(), ShardSpec(mesh, parse_placements(_pl_text(src))), shape, me))
+            dsts.append(ShardSpec(mesh, parse_placements(_pl_text(dst))))
+            wants.append(np.ascontiguousarray(out[me]))
+        for rep in range(2):  # general path, then the cached plan (where one applies)
+            ys = redistribute_many(xs, dsts)
+            for y, w, d in zip(ys, wants, dsts):
+                got = y.local.cpu()
+                got = got.view(torch.int16).numpy() if got.dtype == torch.bfloat16 else got.numpy()
+                assert got.tobytes() == w.tobytes(), (seed, rep, d, me)
+                assert y.placements == d.placements
+    assert peer.STATS["all_gather"] + peer.STATS["reduce_scatter"] + peer.STATS["all_reduce"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mesh_sizes,seeds", [((2, 2), (11, 12, 13)), ((4,), (21, 22)), ((2, 4), (31,))])
+def test_random_redistribute_many_peer_vs_oracle(mesh_sizes, seeds):
+    _spawn(_worker_random_peer, int(np.prod(mesh_sizes)), mesh_sizes, seeds)
+
+
+def test_random_cases_are_valid_specs():
+    """CPU check of the generator: every random case is a valid spec pair
+    (no tensor dim sharded twice, no transition into Partial)."""
+    from paper_2509_07003_b200 import create_mesh
+    from paper_2509_07003_b200.placement import ShardSpec, parse_placements
+    for mesh_sizes, seeds in [((2, 2), (11, 12, 13)), ((4,), (21, 22)), ((2, 4), (31,))]:
+        mesh = create_mesh([(f"m{j}", s) for j, s in enumerate(mesh_sizes)])
+        for seed in seeds:
+            cs = _random_cases(seed, mesh_sizes)
+            assert any(c[5] for c in cs)  # some Partial sources
+            for shape, src, dst, *_ in cs:
+                ShardSpec(mesh, parse_placements(_pl_text(src))).validate_for_shape(shape)
+                ShardSpec(mesh, parse_placements(_pl_text(dst))).validate_for_shape(shape)
+            assert sum(_path_valid(c[0], c[1], c[2], mesh) for c in cs) >= len(cs) // 2
