@@ -224,7 +224,10 @@ int32_t sdr_peer_heap_close(void* base);  /* unmap a peer heap */
 int32_t sdr_peer_heap_free(void* base);   /* free this process's own heap */
 /* Device-side barrier of `nranks` fiber ranks: stores `epoch` (release, system
  * scope) into slot `rank` of every rank's flags, then waits (acquire) until
- * every slot of flags[rank] >= epoch.  flags: host array of nranks device
+ * every slot of flags[rank] >= epoch.  epoch == 0 takes the epoch from the
+ * device: this rank's barrier counter (flag word SDR_MAX_PEERS + 1 of its own
+ * heap) + 1, stored back -- the form a captured CUDA graph can replay; a heap
+ * must use one form or the other, not both.  flags: host array of nranks device
  * pointers (each rank's heap base).  A wait longer than timeout_ns traps (the
  * call fails loudly instead of hanging).  timeout_ns < 0 is the soft mode of
  * the transport's self-check: after |timeout_ns| the kernel sets flag word
@@ -248,17 +251,22 @@ int32_t sdr_reduce_scatter_peers(const sdr_pack_member* members, int32_t n,
 
 /* One whole peer collective per call (what the redistribute plan replays):
  * the three launches above behind one entry point, with the segments at
- * bases[q] + half_offset.  S->R: sdr_pack_local(send -> my segment),
+ * bases[q] + half_offset.  lead_barrier != 0 adds a barrier BEFORE the pack
+ * (same epoch rule, epoch + 0 / device epoch): every peer has then finished
+ * its pulls of earlier calls from this half, whatever half they used -- the
+ * mode for calls inside (or interleaved with) captured CUDA graphs, whose
+ * replays the host does not see.  With epoch != 0 the lead barrier uses
+ * epoch and the main one epoch + 1.  S->R: sdr_pack_local(send -> my segment),
  * sdr_peer_barrier(epoch), sdr_unpack_gathered_peers(recv). */
 int32_t sdr_peer_all_gather(const sdr_pack_member* send, const sdr_pack_member* recv, int32_t n,
                             void* const* bases, int32_t nranks, int32_t rank, int64_t half_offset,
-                            uint64_t epoch, int64_t timeout_ns, void* stream);
+                            uint64_t epoch, int64_t timeout_ns, int32_t lead_barrier, void* stream);
 /* P->S: sdr_pack_scatter(full -> my half, seg_bytes per rank),
  * sdr_peer_barrier(epoch), sdr_reduce_scatter_peers(piece). */
 int32_t sdr_peer_reduce_scatter(const sdr_pack_member* full, const sdr_pack_member* piece, int32_t n,
                                 void* const* bases, int32_t nranks, int32_t rank, int64_t half_offset,
                                 int64_t seg_bytes, int32_t dtype, uint64_t epoch, int64_t timeout_ns,
-                                void* stream);
+                                int32_t lead_barrier, void* stream);
 
 /* INT32 pipe microbenchmark: measured IMAD.WIDE.U32 and LOP3 throughput
  * (ops/s) on `device`, for the roofline denominator. */

@@ -120,10 +120,10 @@ def _load():
                                                  C.c_void_p]),
         "sdr_peer_all_gather": (C.c_int32, [P(SdrPackMember), P(SdrPackMember), C.c_int32, P(C.c_void_p),
                                             C.c_int32, C.c_int32, C.c_int64, C.c_uint64, C.c_int64,
-                                            C.c_void_p]),
+                                            C.c_int32, C.c_void_p]),
         "sdr_peer_reduce_scatter": (C.c_int32, [P(SdrPackMember), P(SdrPackMember), C.c_int32,
                                                 P(C.c_void_p), C.c_int32, C.c_int32, C.c_int64, C.c_int64,
-                                                C.c_int32, C.c_uint64, C.c_int64, C.c_void_p]),
+                                                C.c_int32, C.c_uint64, C.c_int64, C.c_int32, C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -173,13 +173,18 @@ int32_t sdr_reduce_scatter_peers(const sdr_pack_member* members, int32_t n,
 
 int32_t sdr_peer_all_gather(const sdr_pack_member* send, const sdr_pack_member* recv, int32_t n,
                             void* const* bases, int32_t nranks, int32_t rank, int64_t half_offset,
-                            uint64_t epoch, int64_t timeout_ns, void* stream) {
+                            uint64_t epoch, int64_t timeout_ns, int32_t lead_barrier, void* stream) {
   if (bases == nullptr || nranks < 1 || nranks > SDR_MAX_PEERS || rank < 0 || rank >= nranks || half_offset < 0)
     return SDR_E_INVALID;
   const void* segs[SDR_MAX_PEERS];
   for (int q = 0; q < nranks; ++q) segs[q] = static_cast<const char*>(bases[q]) + half_offset;
   const cudaStream_t s = as_stream(stream);
-  int st = sdr::pack_local(send, n, const_cast<void*>(segs[rank]), s);
+  int st = SDR_OK;
+  if (lead_barrier) {
+    st = sdr::peer_barrier(bases, rank, nranks, epoch, timeout_ns, s);
+    if (epoch != 0) ++epoch;
+  }
+  if (st == SDR_OK) st = sdr::pack_local(send, n, const_cast<void*>(segs[rank]), s);
   if (st == SDR_OK) st = sdr::peer_barrier(bases, rank, nranks, epoch, timeout_ns, s);
   if (st == SDR_OK) st = sdr::unpack_gathered_peers(recv, n, segs, nranks, s);
   return st;
@@ -188,13 +193,18 @@ int32_t sdr_peer_all_gather(const sdr_pack_member* send, const sdr_pack_member* 
 int32_t sdr_peer_reduce_scatter(const sdr_pack_member* full, const sdr_pack_member* piece, int32_t n,
                                 void* const* bases, int32_t nranks, int32_t rank, int64_t half_offset,
                                 int64_t seg_bytes, int32_t dtype, uint64_t epoch, int64_t timeout_ns,
-                                void* stream) {
+                                int32_t lead_barrier, void* stream) {
   if (bases == nullptr || nranks < 1 || nranks > SDR_MAX_PEERS || rank < 0 || rank >= nranks || half_offset < 0)
     return SDR_E_INVALID;
   const void* segs[SDR_MAX_PEERS];
   for (int q = 0; q < nranks; ++q) segs[q] = static_cast<const char*>(bases[q]) + half_offset;
   const cudaStream_t s = as_stream(stream);
-  int st = sdr::pack_scatter(full, n, const_cast<void*>(segs[rank]), seg_bytes, nranks, s);
+  int st = SDR_OK;
+  if (lead_barrier) {
+    st = sdr::peer_barrier(bases, rank, nranks, epoch, timeout_ns, s);
+    if (epoch != 0) ++epoch;
+  }
+  if (st == SDR_OK) st = sdr::pack_scatter(full, n, const_cast<void*>(segs[rank]), seg_bytes, nranks, s);
   if (st == SDR_OK) st = sdr::peer_barrier(bases, rank, nranks, epoch, timeout_ns, s);
   if (st == SDR_OK) st = sdr::reduce_scatter_peers(piece, n, segs, seg_bytes, nranks, rank, dtype, s);
   return st;

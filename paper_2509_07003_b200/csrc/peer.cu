@@ -251,6 +251,16 @@ __global__ void k_peer_barrier(const __grid_constant__ PeerFlags F, int rank, in
   // on every SM while we spin, starving other streams of the same GPU (with
   // ranks as streams of one GPU that deadlocks: tests/test_peer_gpu.py).
   const int t = threadIdx.x;
+  if (epoch == 0) {
+    // device epoch: this rank's barrier counter (flag word SDR_MAX_PEERS + 1
+    // of its own heap, touched by no other rank) advances once per barrier,
+    // so a CUDA graph that captured this launch replays with fresh epochs;
+    // every fiber rank runs the same barrier sequence, so the counters agree
+    __shared__ unsigned long long s_epoch;
+    if (t == 0) s_epoch = atomicAdd(F.p[rank] + SDR_MAX_PEERS + 1, 1ull) + 1ull;
+    __syncthreads();
+    epoch = s_epoch;
+  }
   if (t >= nranks) return;
   asm volatile("fence.acq_rel.sys;" ::: "memory");
   // max, not a plain store: a slot's epoch can never move backwards, whatever

@@ -17,6 +17,15 @@ reduce-scatter sums in ascending fiber-rank order -- the reference's
 `acc += b` loop (comm.py:113-125), bit for bit for every dtype.  Calls
 alternate halves, so one barrier per call is enough (include/sdrng.h).
 
+Barrier epochs come from a per-heap device counter (sdr_peer_barrier with
+epoch 0), so the launches can be captured in a CUDA graph and replayed:
+during capture a call that fits the existing heap records a LEADING barrier
+too (every peer has then finished its pulls of earlier calls, including
+replays the host never sees), and once a heap has been captured every later
+eager call on it does the same.  Heap creation and regrowth cannot be
+captured: warm a fiber up eagerly first, or its captured calls go to NCCL.
+The graph must replay in the same stream order on every rank.
+
 Selection (`transport()`): SDR_TRANSPORT=peer|nccl|auto (default auto = peer
 when every fiber rank is on this host and its device can reach ours; the
 decision is agreed by all fiber ranks).  SDR_PEER_HEAP_MB sizes the heap
@@ -65,8 +74,8 @@ class PeerHeap:
         self.P = len(fiber)
         self.rank = fiber.index(dist.get_rank())
         self.half = int(half_bytes) // 256 * 256
-        self.epoch = 0
         self.calls = 0
+        self.captured = False  # a call on this heap was captured in a CUDA graph
         self.ok = False
         self._stream = None  # stream of the last call (see _order)
         self.bases: list = [None] * self.P
@@ -160,6 +169,11 @@ class PeerHeap:
         one, it first waits for everything queued on that stream so far
         (which includes the last pull)."""
         s = torch.cuda.current_stream(self.dev)
+        if torch.cuda.is_current_stream_capturing():
+            # a captured call cannot wait on work outside the graph; its lead
+            # barrier (_lead) orders it against every earlier pull instead
+            self.captured = True
+            return
         if self._stream is not None and self._stream != s:
             ev = torch.cuda.Event()
             ev.record(self._stream)
@@ -171,10 +185,18 @@ class PeerHeap:
         return (C.c_void_p * self.P)(*[b + off for b in self.bases])
 
     def _barrier(self, stream=None):
-        self.epoch += 1
-        st = _lib.LIB.sdr_peer_barrier(self._flags, self.rank, self.P, self.epoch, _TIMEOUT_NS,
+        # epoch 0: the device counter picks it (graph-replayable)
+        st = _lib.LIB.sdr_peer_barrier(self._flags, self.rank, self.P, 0, _TIMEOUT_NS,
                                        _stream(self.dev) if stream is None else stream)
         _lib.check(st, "sdr_peer_barrier")
+
+    def _lead(self) -> int:
+        """1 when this call needs a barrier before its pack: inside a CUDA
+        graph capture, and on every call after one (replays are invisible to
+        the host, so the half-alternation argument no longer holds)."""
+        if torch.cuda.is_current_stream_capturing():
+            self.captured = True
+        return 1 if self.captured else 0
 
     def _next_half(self) -> int:
         h = self.calls & 1
@@ -199,9 +221,8 @@ class PeerHeap:
         if not ordered:
             self._order()
         off = _lib.PEER_FLAG_BYTES + self._next_half() * self.half
-        self.epoch += 1
         _lib.check(_lib.LIB.sdr_peer_all_gather(send_arr, recv_arr, n, self._flags, self.P, self.rank, off,
-                                                self.epoch, _TIMEOUT_NS, stream), "sdr_peer_all_gather")
+                                                0, _TIMEOUT_NS, self._lead(), stream), "sdr_peer_all_gather")
         STATS["all_gather"] += 1
 
     def reduce_scatter_arrays(self, full_arr, piece_arr, n: int, seg_bytes: int, dtype_code: int,
@@ -211,9 +232,8 @@ class PeerHeap:
         if not ordered:
             self._order()
         off = _lib.PEER_FLAG_BYTES + self._next_half() * self.half
-        self.epoch += 1
         _lib.check(_lib.LIB.sdr_peer_reduce_scatter(full_arr, piece_arr, n, self._flags, self.P, self.rank, off,
-                                                    seg_bytes, dtype_code, self.epoch, _TIMEOUT_NS, stream),
+                                                    seg_bytes, dtype_code, 0, _TIMEOUT_NS, self._lead(), stream),
                    "sdr_peer_reduce_scatter")
         STATS["reduce_scatter"] += 1
 
@@ -228,6 +248,8 @@ class PeerHeap:
         bufs = self._half_ptrs(h)
         arr = CudaMover._arr(full_members)
         with torch.cuda.device(self.dev):
+            if self._lead():
+                self._barrier()
             st = _lib.LIB.sdr_pack_scatter(arr, len(full_members), bufs[self.rank], seg_bytes, self.P,
                                            _stream(self.dev))
             _lib.check(st, "sdr_pack_scatter")
@@ -267,6 +289,8 @@ class PeerHeap:
         arr = CudaMover._arr(full)
         with torch.cuda.device(self.dev):
             s = _stream(self.dev)
+            if self._lead():
+                self._barrier()
             _lib.check(_lib.LIB.sdr_pack_scatter(arr, len(full), bufs[self.rank], seg, P, s),
                        "sdr_pack_scatter")
             self._barrier()
@@ -301,14 +325,15 @@ def heap_for(group, fiber, dev: torch.device, need_half: int = 0):
     (they all pass the same need, computed from padded segment sizes)."""
     if group is None or dev.type != "cuda" or transport() == "nccl" or len(fiber) > _lib.MAX_PEERS:
         return None
-    if torch.cuda.is_current_stream_capturing():
-        # barrier epochs and heap halves are chosen on the host per call, so a
-        # replayed graph would reuse them: captured collectives go to NCCL
-        # (every rank captures the same code, so all ranks agree)
-        return None
     need_half = -(-int(need_half) // 256) * 256
     key = (tuple(fiber), dev.index)
     hp = _HEAPS.get(key)
+    if torch.cuda.is_current_stream_capturing():
+        # a heap cannot be created or regrown inside a capture (allocation and
+        # the handle exchange are not capturable): captured calls use an
+        # existing heap that fits, else NCCL -- every rank captures the same
+        # code with the same heaps, so all ranks agree
+        return hp if hp is not None and hp.ok and need_half <= hp.half else None
     if hp is None:
         half = int(float(os.environ.get("SDR_PEER_HEAP_MB", "1024")) * (1 << 20)) // 2
         hp = _HEAPS[key] = PeerHeap(group, fiber, dev, max(half, min(need_half, _max_half())))

@@ -683,3 +683,103 @@ def test_random_cases_are_valid_specs():
                 ShardSpec(mesh, parse_placements(_pl_text(src))).validate_for_shape(shape)
                 ShardSpec(mesh, parse_placements(_pl_text(dst))).validate_for_shape(shape)
             assert sum(_path_valid(c[0], c[1], c[2], mesh) for c in cs) >= len(cs) // 2
+
+
+def _worker_graph_peer(rank, ws, interleave=True):
+    """redistribute_many captured in a CUDA graph on the peer transport (ranks
+    share one GPU, IPC heaps): replays with fresh inputs written into the
+    captured tensors, interleaved with eager calls on the same heaps, equal the
+    reference's sums (ascending rank order) bit for bit every time."""
+    os.environ["SDR_COMM_CPU_STAGING"] = "1"
+    os.environ["SDR_TRANSPORT"] = "peer"
+    torch.cuda.set_device(0)
+    from paper_2509_07003_b200 import create_mesh, peer
+    from paper_2509_07003_b200.dtensor import from_local, redistribute_many
+    from paper_2509_07003_b200.placement import ShardSpec, local_shape_and_offset, parse_placements
+    mesh = create_mesh([("dp", ws)])
+    me = mesh.coords_of_rank(rank)
+    spec = lambda t: ShardSpec(mesh, parse_placements(t))  # noqa: E731
+    shapes = {"a": ((37, 5), "S(0)", "R"), "b": ((9, 13), "P", "S(0)"), "c": ((6, 7), "P", "R"),
+              "d": ((4, 50), "S(1)", "R")}
+
+    def data(step):
+        """Every rank's locals for `step` (all ranks can compute all of them)."""
+        out = {}
+        for name, (shape, src, _) in shapes.items():
+            g = torch.Generator().manual_seed(1000 * step + ord(name))  # (str hash is per-process)
+            if src == "P":
+                out[name] = [torch.randn(shape, generator=g) for _ in range(ws)]
+            else:
+                out[name] = torch.randn(shape, generator=g)
+        return out
+
+    def local(d, name, q):
+        shape, src, _ = shapes[name]
+        if src == "P":
+            return d[name][q]
+        v = local_shape_and_offset(spec(src), shape, (q,))
+        sl = tuple(slice(o, o + n) for o, n in zip(v.local_offset, v.local_shape))
+        return d[name][sl].contiguous()
+
+    def expected(d, name):
+        shape, src, dst = shapes[name]
+        if src != "P":
+            return d[name]
+        acc = d[name][0].clone()
+        for t in d[name][1:]:
+            acc += t  # the reference's ascending loop (comm.py:91-101)
+        if dst == "R":
+            return acc
+        v = local_shape_and_offset(spec(dst), shape, me)
+        return acc[v.local_offset[0]:v.local_offset[0] + v.local_shape[0]]
+
+    names = list(shapes)
+    d0 = data(0)
+    xs = [from_local(local(d0, n, rank).cuda(), spec(shapes[n][1]), shapes[n][0], me) for n in names]
+    dsts = [spec(shapes[n][2]) for n in names]
+    for _ in range(2):  # eager warm-up: creates (and self-checks) the heaps
+        redistribute_many(xs, dsts)
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        redistribute_many(xs, dsts)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    cap0 = dict(peer.STATS)
+    with torch.cuda.graph(g):
+        ys = redistribute_many(xs, dsts)
+    before = dict(peer.STATS)
+    assert before["all_gather"] > cap0["all_gather"], (cap0, before)  # captured on the peer transport
+    for step in range(1, 5):
+        d = data(step)
+        for x, n in zip(xs, names):
+            x.local.copy_(local(d, n, rank))
+        g.replay()
+        # an eager call on the same heaps between replays (other data)
+        e = data(100 + step)
+        xe = [from_local(local(e, n, rank).cuda(), spec(shapes[n][1]), shapes[n][0], me) for n in names]
+        ye = redistribute_many(xe, dsts) if interleave else []
+        torch.cuda.synchronize()
+        for y, n in zip(ys, names):
+            got = y.local.cpu()
+            if not torch.equal(got, expected(d, n)):
+                stale = torch.equal(got, expected(d0, n))
+                raise AssertionError((step, n, "replay", "stale" if stale else "wrong",
+                                      float((got - expected(d, n)).abs().max()), rank))
+        for y, n in zip(ye, names):
+            assert torch.equal(y.local.cpu(), expected(e, n)), (step, n, "eager")
+    # the eager calls after the capture ran on the peer transport, not NCCL
+    assert peer.STATS["all_gather"] > before["all_gather"] or not interleave
+    assert all(hp.captured for hp in peer._HEAPS.values() if hp.ok)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("interleave", [False, True])
+def test_redistribute_many_captured_in_cuda_graph_peer(interleave):
+    os.environ["SDR_PEER_TIMEOUT_S"] = "60"
+    try:
+        _spawn(_worker_graph_peer, 4, interleave)
+    finally:
+        os.environ.pop("SDR_PEER_TIMEOUT_S", None)
