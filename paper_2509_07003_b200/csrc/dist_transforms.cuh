@@ -125,6 +125,12 @@ __constant__ double c_npoly[9] = {
 #ifndef SDR_NORMAL_BF16_F32
 #define SDR_NORMAL_BF16_F32 1  // certified float32 Box-Muller for bfloat16 outputs
 #endif
+#ifndef SDR_SKIP_MISS
+#define SDR_SKIP_MISS 0  // A/B only (WRONG results): skip the fallback of uncertified elements
+#endif
+#ifndef SDR_MISSQ
+#define SDR_MISSQ 1      // bfloat16 fast fills: queue uncertified elements per warp, resolve 32 at a time
+#endif
 #ifndef SDR_NORMAL_SPLIT
 #define SDR_NORMAL_SPLIT 1  // float64 phases of a chunk in SPLIT passes (register pressure)
 #endif
@@ -355,6 +361,28 @@ template <int DT>
 __device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, const NormalLut* L,
                                                            uint32_t w0, uint32_t w1);
 
+// Per-warp queue of the bfloat16 elements the float32 path could not
+// certify (~0.24% of them).  Resolving one inline costs a whole divergent
+// float64 evaluation with one lane active (measured: ~12% of a fill, ~17% of
+// the LLaMA-3-8B init); queued, they are resolved by the converged warp, one
+// element per lane (missq_flush at the end of a kernel / of a batch tile).
+// The queued element's slot already holds a placeholder from the chunk's
+// vector store; the flush overwrites it after a __syncwarp (memory order
+// between the warp's threads).  A full queue falls back to the inline path.
+constexpr int kMissQ = 64;
+struct MissQ {
+  uint4 e[kMissQ];  // (address lo, address hi, w0, w1)
+  uint32_t n;
+};
+__device__ __forceinline__ MissQ* missq() {
+  __shared__ MissQ s_mq[256 / 32];  // one per warp of a 256-thread CTA (the bfloat16 fill kernels)
+  return &s_mq[threadIdx.x >> 5];
+}
+__device__ __forceinline__ void missq_init() {
+  if ((threadIdx.x & 31) == 0) missq()->n = 0;
+  __syncwarp();
+}
+
 // A chunk of bfloat16 normals on the float32 path.  Elements go in pairs: one
 // F2FP packs the two lower ends RD(v - B) and one the two upper ends RU(v + B)
 // (bf16(RN32(.)) is monotone, so an element is certified iff both ends round
@@ -363,7 +391,8 @@ __device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, const
 // at which element differs; those take the float64 path, then the exact one.
 template <int NE>
 __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLut32* L32,
-                                                  const uint32_t* w0, const uint32_t* w1, uint16_t* out) {
+                                                  const uint32_t* w0, const uint32_t* w1, uint16_t* out,
+                                                  uint16_t* qdst = nullptr) {
   static_assert(NE % 2 == 0, "elements go in pairs");
   uint32_t diff = 0, hiw[NE / 2];
 #pragma unroll
@@ -387,18 +416,46 @@ __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLu
     diff |= l32 ^ h32;
     hiw[e / 2] = h32;
   }
-  if (__builtin_expect(diff != 0, 0)) {
+  if (__builtin_expect(diff != 0, 0) && !SDR_SKIP_MISS) {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       if (out[e] != static_cast<uint16_t>(hiw[e / 2] >> (16 * (e & 1)))) {
 #if SDR_COUNT_F32_MISS
         atomicAdd(P.nm.fallbacks, 1ull);
 #endif
+#if SDR_MISSQ
+        if (qdst != nullptr) {  // queue it (qdst = this chunk's destination in global memory)
+          MissQ* q = missq();
+          const uint32_t pos = atomicAdd(&q->n, 1u);
+          if (pos < kMissQ) {
+            const uint64_t a = reinterpret_cast<uint64_t>(qdst + e);
+            q->e[pos] = make_uint4(static_cast<uint32_t>(a), static_cast<uint32_t>(a >> 32), w0[e], w1[e]);
+            continue;
+          }
+        }
+#endif
         // float64 certified path (tables read through L1/L2), then the exact mirror
         out[e] = normal_value<SDR_BF16>(P, P.nm.lut, w0[e], w1[e]);
       }
     }
   }
+}
+
+// Resolve the warp's queued elements: the float64 certified path (tables
+// through L1), then the exact mirror, one element per lane.  The whole warp
+// must be converged here.
+__device__ __noinline__ void missq_flush(const DistP& P) {
+  MissQ* q = missq();
+  __syncwarp();
+  const uint32_t n = min(q->n, static_cast<uint32_t>(kMissQ));
+  for (uint32_t k = threadIdx.x & 31; k < n; k += 32) {
+    const uint4 t = q->e[k];
+    const uint16_t v = normal_value<SDR_BF16>(P, P.nm.lut, t.z, t.w);
+    *reinterpret_cast<uint16_t*>((static_cast<uint64_t>(t.y) << 32) | t.x) = v;
+  }
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) q->n = 0;
+  __syncwarp();
 }
 
 // CUDA libm value d of table point k corrected to NumPy's (ExactMirror).
@@ -492,7 +549,7 @@ __device__ __forceinline__ void normal_chunk(const DistP& P, const NormalLut* L,
     out[e] = normal_certified<DT>(P, rs[e], c[e], ok);
     badmask |= ok ? 0u : (1u << e);
   }
-  if (__builtin_expect(badmask != 0, 0)) {
+  if (__builtin_expect(badmask != 0, 0) && !SDR_SKIP_MISS) {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       if (badmask & (1u << e)) {

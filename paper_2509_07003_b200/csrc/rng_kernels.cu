@@ -100,6 +100,13 @@ template <int DIST, int DT, bool ALIGNED>
 __device__ __forceinline__ void fill_chunk_at(const FillArgs& A, const NormalLut* L, uint64_t q,
                                               uint64_t j0);
 
+// bfloat16 normal fills resolve uncertified elements through the per-warp
+// queue (dist_transforms.cuh, MissQ); the kernels init it and flush it.
+template <int DIST, int DT>
+constexpr bool uses_missq() {
+  return SDR_MISSQ && DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32 && SDR_NSPLIT == 1;
+}
+
 template <int DIST, int DT, bool ALIGNED>
 __device__ __forceinline__ void fill_chunk(const FillArgs& A, const NormalLut* L, uint64_t q) {
   fill_chunk_at<DIST, DT, ALIGNED>(A, L, q, chunk_base(A, q));
@@ -176,14 +183,22 @@ __device__ __forceinline__ void values_from_words(const FillArgs& A, const Norma
   }
 }
 
-// Chunk q whose first element has global index j0.
+// Chunk q whose first element has global index j0.  bfloat16 normals queue
+// their uncertified elements (MissQ) with this chunk's destination.
 template <int DIST, int DT, bool ALIGNED>
 __device__ __forceinline__ void fill_chunk_at(const FillArgs& A, const NormalLut* L, uint64_t q,
                                               uint64_t j0) {
   using T = typename St<DT>::T;
   T v[kV];
-  chunk_values<DIST, DT, ALIGNED>(A, L, j0, v);
-  store_chunk(static_cast<T*>(A.out) + q * kV, v);
+  T* dst = static_cast<T*>(A.out) + q * kV;
+  if constexpr (uses_missq<DIST, DT>()) {
+    uint32_t w0[kV], w1[kV];
+    fill_words<ALIGNED>(A, j0, w0, w1);
+    normal_chunk_bf16<kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v, dst);
+  } else {
+    chunk_values<DIST, DT, ALIGNED>(A, L, j0, v);
+  }
+  store_chunk(dst, v);
 }
 
 // Ragged rows (inner extent not a multiple of kV): chunk q = (row, cq) covers
@@ -251,6 +266,7 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
   // already be in flight: they are never written by a kernel)
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
+  if constexpr (uses_missq<DIST, DT>()) missq_init();
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (A.walk.on) {
@@ -315,8 +331,12 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
         fill_words<ALIGNED>(A, j, w0, w1);
         stage_lut_wait(bar);
         T v[kV];
-        values_from_words<DIST, DT>(A, L, w0, w1, v);
-        store_chunk(static_cast<T*>(A.out) + q * kV, v);
+        T* dst = static_cast<T*>(A.out) + q * kV;
+        if constexpr (uses_missq<DIST, DT>())
+          normal_chunk_bf16<kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v, dst);
+        else
+          values_from_words<DIST, DT>(A, L, w0, w1, v);
+        store_chunk(dst, v);
         walk_next(A.walk, A.chunks_per_row, j, cq);
         q += stride;
       } else {
@@ -334,6 +354,7 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
     if constexpr (DIST == SDR_NORMAL) stage_lut_wait(bar);
     for (; q < A.nchunks; q += stride) fill_chunk<DIST, DT, ALIGNED>(A, L, q);
   }
+  if constexpr (uses_missq<DIST, DT>()) missq_flush(A.d);  // every thread gets here: the warp is converged
 }
 
 template <int DIST, int DT>
@@ -382,6 +403,7 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
     stage_lut(&s_lut, descs[0].d.nm.lut);
     L = &s_lut;
   }
+  if constexpr (uses_missq<DIST, DT>()) missq_init();
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     // member f: last index with tile_prefix[f] <= t (uniform across the CTA)
     int lo = 0, hi = n - 1;
@@ -415,6 +437,9 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
       if (i1 > numel) i1 = numel;
       for (uint64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) fill_elem<DIST, DT>(A, L, i);
     }
+    // this tile's queued elements, with this member's parameters (converged:
+    // the tile loops are done; A is replaced only after the next barrier)
+    if constexpr (uses_missq<DIST, DT>()) missq_flush(A.d);
   }
 }
 

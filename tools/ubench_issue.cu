@@ -36,6 +36,26 @@ __global__ void __launch_bounds__(512) k(uint64_t* out, uint32_t seed) {
       if (MIX & 8) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(f[i]) : "f"(f[(i + 1) % CH]), "f"(1e-7f));
       if (MIX & 16) asm volatile("add.u32 %0, %0, %1;" : "+r"(c[i]) : "r"(a[(i + 3) % CH]));
       if (MIX & 32) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(c[i]) : "r"(0x9E3779B9u), "r"(a[(i + 1) % CH]));
+      if (MIX & 64) asm volatile("rsqrt.approx.ftz.f32 %0, %0;" : "+f"(f[i]));
+      if (MIX & 128) {  // I2FP in a chain: a -> float -> bits (+LOP3 to keep it from folding)
+        float t;
+        asm volatile("cvt.rn.f32.u32 %0, %1;" : "=f"(t) : "r"(a[i]));
+        a[i] = __float_as_uint(t) ^ b[i];
+      }
+      if (MIX & 256) asm volatile("shf.r.wrap.b32 %0, %0, %1, 3;" : "+r"(a[i]) : "r"(b[i]));
+      if (MIX & 512) {  // F2F pair in a chain: f64 -> f32 -> f64
+        float t;
+        asm volatile("cvt.rn.f32.f64 %0, %1;" : "=f"(t) : "d"(d[i]));
+        asm volatile("cvt.f64.f32 %0, %1;" : "=d"(d[i]) : "f"(t));
+      }
+      if (MIX & 2048) asm volatile("add.rm.f32 %0, %0, %1;" : "+f"(f[i]) : "f"(f[(i + 3) % CH]));
+      if (MIX & 4096) asm volatile("mul.f32 %0, %0, %1;" : "+f"(f[i]) : "f"(f[(i + 5) % CH]));
+      if (MIX & 8192) {  // random shared-memory LDS.64 (a 4 KiB table): bank conflicts as in the table lookups
+        extern __shared__ uint2 tab[];
+        const uint2 v = tab[(a[i] >> 7) & 511];
+        a[i] ^= v.x;
+      }
+      if (MIX & 16384) asm volatile("prmt.b32 %0, %0, %1, 0x1044;" : "+r"(c[i]) : "r"(b[i]));
     }
   }
   const uint64_t t1 = clock64();
@@ -53,9 +73,9 @@ void run(const char* name, int per_iter_instr) {
   cudaMemset(d, 0, 16);
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  k<MIX><<<sms, 512>>>(d, 12345u);  // warm-up
+  k<MIX><<<sms, 512, 4096>>>(d, 12345u);  // warm-up
   cudaMemset(d, 0, 16);
-  k<MIX><<<sms, 512>>>(d, 12345u);   // 16 warps per SM = 4 per SMSP
+  k<MIX><<<sms, 512, 4096>>>(d, 12345u);   // 16 warps per SM = 4 per SMSP
   uint64_t cyc;
   cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
   // per SMSP: 4 warps x ITERS x CH x per_iter_instr warp-instructions
@@ -81,5 +101,14 @@ int main() {
   run<1 | 4 | 8>("LOP3 + DFMA + FFMA", 3);
   run<1 | 32 | 4>("LOP3 + IMAD + DFMA", 3);
   run<2 | 4>("IMAD.WIDE(+xor) + DFMA", 3);
+  run<64>("MUFU.RSQ", 1);
+  run<128>("I2FP + LOP3 (chain)", 2);
+  run<256>("SHF (funnel)", 1);
+  run<512>("F2F.F32.F64 + F2F.F64.F32 (chain)", 2);
+  run<2048>("FADD.RM", 1);
+  run<4096>("FMUL", 1);
+  run<8192>("LDS.64 random (+LOP3)", 2);
+  run<16384>("PRMT", 1);
+  run<8 | 64>("FFMA + MUFU.RSQ", 2);
   return 0;
 }
