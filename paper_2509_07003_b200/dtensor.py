@@ -205,11 +205,18 @@ def _check_transition(src: Placement, dst: Placement):
         raise RedistributeError(f"public transition into Partial is unsupported ({src}->{dst})")
 
 
+_PATHS_OK: dict = {}
+
+
 def _check_path(x: DTensor, dst: ShardSpec):
     """Validate the whole left-to-right walk before any data moves: every
     intermediate spec must be valid (the reference raises PlacementError at
     the step that would shard a tensor dim twice, e.g. [P,S(0)] -> [S(0),R]),
-    so a coalesced call fails on every rank before its first collective."""
+    so a coalesced call fails on every rank before its first collective.
+    Valid (spec, destination, shape) triples are remembered."""
+    key = (x.meta.spec, dst, x.shape)
+    if key in _PATHS_OK:
+        return
     if dst.mesh != x.mesh:
         raise RedistributeError("redistribute requires the same mesh")
     dst.validate_for_shape(x.shape)
@@ -218,6 +225,9 @@ def _check_path(x: DTensor, dst: ShardSpec):
         _check_transition(spec.placements[md], dst.placements[md])
         if spec.placements[md] != dst.placements[md]:
             spec = spec.with_placement(md, dst.placements[md])
+    if len(_PATHS_OK) > 65536:
+        _PATHS_OK.clear()
+    _PATHS_OK[key] = True
 
 
 def redistribute_many(xs: list[DTensor], dsts: list[ShardSpec],
@@ -230,12 +240,12 @@ def redistribute_many(xs: list[DTensor], dsts: list[ShardSpec],
     mover = DEFAULT_MOVER if mover is None else mover
     if len(xs) != len(dsts):
         raise ValueError("one destination spec per tensor")
-    for x, d in zip(xs, dsts):
-        _check_path(x, d)
     if mover is DEFAULT_MOVER and xs and all(x.local.is_cuda for x in xs):
-        plan = _plan_for(xs, dsts)
+        plan = _plan_for(xs, dsts)  # (a plan exists only for validated walks)
         if plan is not None:
             return plan.run(xs, ledger)
+    for x, d in zip(xs, dsts):
+        _check_path(x, d)
     cur = [[x.meta.spec, x.local] for x in xs]
     ndim_max = max((x.mesh.ndim for x in xs), default=0)
     for md in range(ndim_max):
@@ -393,9 +403,11 @@ def _plan_for(xs, dsts):
     fk = (tuple(id(x.meta) for x in xs), tuple(id(d) for d in dsts), tuple(x.coord for x in xs),
           xs[0].local.device.index, peer.transport())
     hit = _FAST.get(fk)
-    if (hit is not None and all(a is x.meta for a, x in zip(hit[0], xs)) and all(a is d for a, d in zip(hit[1], dsts))
-            and hit[2].valid()):
-        return hit[2]
+    if hit is not None and all(a is x.meta for a, x in zip(hit[0], xs)) and all(a is d for a, d in zip(hit[1], dsts)):
+        if hit[2] is _NO_PLAN:
+            return None
+        if hit[2].valid():
+            return hit[2]
     key = _plan_key(xs, dsts)
     plan = _PLANS.get(key)
     if plan is None:
@@ -403,15 +415,13 @@ def _plan_for(xs, dsts):
         _PLANS[key] = plan
         if len(_PLANS) > 4096:
             _PLANS.pop(next(iter(_PLANS)))
-    if plan is _NO_PLAN:
-        return None
-    if not plan.valid():
+    if plan is not _NO_PLAN and not plan.valid():
         _PLANS.pop(key, None)
         return None
     _FAST[fk] = (tuple(x.meta for x in xs), tuple(dsts), plan)  # holds the objects: ids stay unique
     if len(_FAST) > 4096:
         _FAST.pop(next(iter(_FAST)))
-    return plan
+    return None if plan is _NO_PLAN else plan
 
 
 def _build_plan(xs, dsts):
@@ -421,11 +431,7 @@ def _build_plan(xs, dsts):
     order on every rank."""
     from . import _lib
     for x, d in zip(xs, dsts):
-        if d.mesh != x.mesh:
-            raise RedistributeError("redistribute requires the same mesh")
-        d.validate_for_shape(x.shape)
-        for md in range(x.mesh.ndim):
-            _check_transition(x.placements[md], d.placements[md])
+        _check_path(x, d)  # before the first (collective) heap lookup
     if any(x.mesh != xs[0].mesh for x in xs):
         return _NO_PLAN
     mesh = xs[0].mesh
