@@ -96,6 +96,7 @@ struct NormalMirror {
   // float32 fast path (bfloat16 outputs): calibrated errors and bound terms
   double err_r32, err_c32;
   float mean32, std32, b32_r, b32_c;  // B32 = r*b32_r + b32_c
+  float bm_r, bm_c, bm_i;             // r32_mufu path: B = r bm_r + h bm_i + bm_c
   unsigned long long* fallbacks;
 };
 
@@ -127,6 +128,12 @@ __constant__ double c_npoly[9] = {
 #endif
 #ifndef SDR_SKIP_MISS
 #define SDR_SKIP_MISS 0  // A/B only (WRONG results): skip the fallback of uncertified elements
+#endif
+#ifndef SDR_NORMAL_BF16_MUFU
+#define SDR_NORMAL_BF16_MUFU 1  // bfloat16 normals: r from MUFU lg2 / rsqrt (r32_mufu) instead of the log table
+#endif
+#ifndef SDR_C32_POLY
+#define SDR_C32_POLY 0   // c32_fast: low part of the angle by polynomial (A/B: 1-3% slower than the second table)
 #endif
 #ifndef SDR_MISSQ
 #define SDR_MISSQ 1      // bfloat16 fast fills: queue uncertified elements per warp, resolve 32 at a time
@@ -302,10 +309,39 @@ __device__ __forceinline__ float r32_fast(uint32_t w0, const NormalLut32* L) {
 #endif
 }
 
+// Table-free float32 r for the bfloat16 path (SDR_NORMAL_BF16_MUFU):
+// X = -2 ln2 lg2(w) with w = 1 - k 2^-24 exact, r = X rsqrt(X).  Two MUFU
+// ops (XU pipe, beside the integer / FP32 issue) and four other instructions
+// instead of r32_fast's ~15 with a bank-conflicted shared-memory load (issue
+// costs: profiles/r02_issue_ubench.txt).  lg2.approx has an absolute error,
+// so r's error is modelled as |r - r_np| <= Er r + Ei h, h = rsqrt(X) ~ 1/r,
+// with Er, Ei measured over all 2^24 inputs at load (k_normal_calibrate_mufu);
+// k = 0 clamps X to 2^-120 (h = 2^60: never certified).  It misses the
+// certification about twice as often as r32_fast (0.56% vs 0.24%), which the
+// per-warp miss queue (MissQ) absorbs.
+__device__ __forceinline__ float r32_mufu(uint32_t w0, float& h) {
+  const float w = fmaf(__uint2float_rn(w0 >> 8), -0x1p-24f, 1.0f);  // 1 - u1, exact
+  float l;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(w));
+  const float X = fmaxf(l * -1.38629436112f, 0x1p-120f);  // -2 ln w
+  h = rsqrt_ftz(X);
+  return X * h;
+}
+
 __device__ __forceinline__ float c32_fast(uint32_t w1, const NormalLut32* L) {
   const float2 a = lut_at(L->trig_hi, (w1 >> 17) & 0x7FF8u);  // hi = k >> 12
+#if SDR_C32_POLY
+  // (cos, sin) of the low part d = 2 pi lo 2^-24 < 1.6e-3 by polynomial
+  // instead of a second bank-conflicted table load: lo 2^8 = w1 & 0xFFF00 is
+  // exact in float32, cos d = 1 - d^2/2 (next term 3e-13), sin d = d - d^3/6
+  const float d = __uint2float_rn(w1 & 0x000FFF00u) * 0x1.921fb6p-30f;  // 2 pi / 2^32
+  const float d2 = d * d;
+  const float cl = fmaf(d2, -0.5f, 1.0f), sl = d * fmaf(d2, -0.16666667f, 1.0f);
+  return fmaf(a.x, cl, -a.y * sl);
+#else
   const float2 b = lut_at(L->trig_lo, (w1 >> 5) & 0x7FF8u);   // lo = k & 4095
   return fmaf(a.x, b.x, -a.y * b.y);
+#endif
 }
 
 // std * r(k) from NormalLut2 (see there): s and t = s (s/2 - 2/3) in float32
@@ -369,7 +405,7 @@ __device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, const
 // The queued element's slot already holds a placeholder from the chunk's
 // vector store; the flush overwrites it after a __syncwarp (memory order
 // between the warp's threads).  A full queue falls back to the inline path.
-constexpr int kMissQ = 64;
+constexpr int kMissQ = 96;
 struct MissQ {
   uint4 e[kMissQ];  // (address lo, address hi, w0, w1)
   uint32_t n;
@@ -400,10 +436,18 @@ __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLu
     float lo[2], hi[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
+#if SDR_NORMAL_BF16_MUFU
+      float h;
+      const float r = r32_mufu(w0[e + i], h), c = c32_fast(w1[e + i], L32);
+      const float v = fmaf(P.nm.std32, r * c, P.nm.mean32);
+      // |v - v_numpy| <= r*bm_r + h*bm_i + bm_c   (host: fill_dist_params)
+      const float B = fmaf(h, P.nm.bm_i, fmaf(r, P.nm.bm_r, P.nm.bm_c));
+#else
       const float r = r32_fast(w0[e + i], L32), c = c32_fast(w1[e + i], L32);
       const float v = fmaf(P.nm.std32, r * c, P.nm.mean32);
       // |v - v_numpy| <= r*b32_r + b32_c   (host: bound terms; |v| term folded)
       const float B = fmaf(r, P.nm.b32_r, P.nm.b32_c);
+#endif
       lo[i] = __fsub_rd(v, B);
       hi[i] = __fadd_ru(v, B);
     }

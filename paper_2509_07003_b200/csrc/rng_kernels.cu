@@ -523,6 +523,31 @@ __global__ void k_normal_calibrate(const double* ltab, const double* ctab, const
   }
 }
 
+// Calibration of r32_mufu (bfloat16 path) over k in [1, 2^24): out[0] = Er =
+// max |r - r_np| / r where r >= 1, out[1] = Ei = max |r - r_np| / h where r < 1,
+// so |r - r_np| <= Er r + Ei h everywhere.  k = 0 is never certified (h = 2^60).
+__global__ void k_normal_calibrate_mufu(const double* ltab, unsigned long long* out) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (1u << 24)) return;
+  const double inf = __longlong_as_double(0x7FF0000000000000ll);
+  float h;
+  const double r = r32_mufu(k << 8, h), rn = __dsqrt_rn(-2.0 * ltab[k]);
+  double er = 0.0, ei = 0.0;
+  if (k > 0) {
+    const double e = fabs(r - rn);
+    if (!(r > 0.0) || !(h > 0.0f) || isinf(r) || isinf(h)) er = ei = inf;
+    else if (r >= 1.0) er = e / r;
+    else ei = e / static_cast<double>(h);
+  }
+  unsigned long long b[2] = {static_cast<unsigned long long>(__double_as_longlong(er)),
+                             static_cast<unsigned long long>(__double_as_longlong(ei))};
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    for (int o = 16; o > 0; o >>= 1) b[i] = max(b[i], __shfl_xor_sync(0xffffffffu, b[i], o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out + i, b[i]);
+  }
+}
+
 // ExactMirror construction: thread t owns table points 16t .. 16t+15 (one code
 // word per function); exceptions are appended to unsorted lists.
 __device__ __forceinline__ uint32_t mirror_code(double np, double cu) {
@@ -687,6 +712,7 @@ struct NormalState {
   NormalLut2* lut2 = nullptr;
   unsigned long long* fallbacks = nullptr;
   double err_r = 0, err_c = 0, err_r32 = 0, err_c32 = 0, err_r2 = 0, err_c2 = 0;
+  double err_rm = 0, err_im = 0;  // r32_mufu (bfloat16 path)
   bool loaded = false;
 };
 static std::mutex g_nm_mu;
@@ -859,11 +885,22 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
         P.nm.b32_r = static_cast<float>(P.nm.b32_r + fabs(static_cast<double>(P.nm.std32)) * 0x1p-22 * (1.0 + 0x1p-20));
         P.nm.b32_c = static_cast<float>(P.nm.b32_c + fabs(static_cast<double>(P.nm.mean32)) * 0x1p-22 * (1.0 + 0x1p-20));
         if (!(Er32 < 0x1p-12) || !(Ac32 < 0x1p-12)) P.nm.b32_r = INFINITY;  // calibration failed
+        {  // r32_mufu: |r - r_np| <= Erm r + Eim h (h = 1/r to 2^-21); c32_fast: |c - c_np| <= Ac32;
+           // |v32 - v_np| <= |std| (r (Erm + Ac32 (1 + Erm) + 2^-23) + Eim h (1 + 2^-20)(1 + Ac32))
+           //                + the b32_c / |v| 2^-22 terms of the table path, doubled (x2.04).
+          const double Erm = g_nm[device].err_rm, Eim = g_nm[device].err_im;
+          P.nm.bm_r = static_cast<float>(2.04 * fabs(P.stdv) * (Erm + Ac32 * (1.0 + Erm) + 0x1p-23) + 0x1p-60 +
+                                         fabs(static_cast<double>(P.nm.std32)) * 0x1p-22 * (1.0 + 0x1p-20));
+          P.nm.bm_i = static_cast<float>(2.04 * fabs(P.stdv) * Eim * (1.0 + 0x1p-20) * (1.0 + Ac32) + 0x1p-140);
+          P.nm.bm_c = P.nm.b32_c;
+          if (!(Erm < 0x1p-12) || !(Eim < 0x1p-12) || !(P.nm.b32_r < INFINITY))
+            P.nm.bm_r = INFINITY;  // calibration failed: every element takes the float64 path
+        }
         // Test hook: SDR_NORMAL_PATH=exact sends every element through the NumPy
         // tables, =f64 skips the float32 path (results must be identical).
         if (const char* path = getenv("SDR_NORMAL_PATH")) {
-          if (strcmp(path, "exact") == 0) P.nm.kr = P.nm.kr2 = P.nm.b32_r = INFINITY;
-          if (strcmp(path, "f64") == 0) P.nm.b32_r = INFINITY;
+          if (strcmp(path, "exact") == 0) P.nm.kr = P.nm.kr2 = P.nm.b32_r = P.nm.bm_r = INFINITY;
+          if (strcmp(path, "f64") == 0) P.nm.b32_r = P.nm.bm_r = INFINITY;
         }
       }
       P.nm.fallbacks = g_nm[device].fallbacks;
@@ -1086,7 +1123,7 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
   cudaEventRecord(t0);
   cudaError_t e = cudaSuccess;
   if (S.lut == nullptr) {
-    e = cudaMalloc(&S.fallbacks, 7 * sizeof(unsigned long long));
+    e = cudaMalloc(&S.fallbacks, 9 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMalloc(&S.lut, sizeof(NormalLut));
     if (e == cudaSuccess) e = cudaMalloc(&S.lut32, sizeof(NormalLut32));
     if (e == cudaSuccess) e = cudaMalloc(&S.lut2, sizeof(NormalLut2));
@@ -1120,11 +1157,12 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
   if (e == cudaSuccess) e = cudaMalloc(&dc, bytes);
   if (e == cudaSuccess) e = cudaMemcpy(dl, l_host, bytes, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(dc, c_host, bytes, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemset(S.fallbacks, 0, 7 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(S.fallbacks, 0, 9 * sizeof(unsigned long long));
   // (3) calibration of the fast paths against the full tables
   if (e == cudaSuccess) {
     k_normal_calibrate<<<(1u << 24) / 256, 256>>>(dl, dc, S.lut, S.lut32, S.lut2, S.fallbacks + 1,
                                                   S.fallbacks + 2);
+    k_normal_calibrate_mufu<<<(1u << 24) / 256, 256>>>(dl, S.fallbacks + 7);
     e = cudaGetLastError();
   }
   // (1) codes + unsorted exceptions
@@ -1190,9 +1228,10 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
     S.code = S.xk = nullptr;
     S.xv = nullptr;
   }
-  // fallbacks[1..6] = max err of r, c (NormalLut), r32, c32 (float32 path), r2, c2 (NormalLut2)
-  unsigned long long bits[6] = {0, 0, 0, 0, 0, 0};
-  if (e == cudaSuccess) e = cudaMemcpy(bits, S.fallbacks + 1, 6 * sizeof(bits[0]), cudaMemcpyDeviceToHost);
+  // fallbacks[1..6] = max err of r, c (NormalLut), r32, c32 (float32 path), r2, c2 (NormalLut2);
+  // [7..8] = Er, Ei of r32_mufu
+  unsigned long long bits[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpy(bits, S.fallbacks + 1, 8 * sizeof(bits[0]), cudaMemcpyDeviceToHost);
   cudaFree(dl);
   cudaFree(dc);
   cudaFree(xk);
@@ -1215,6 +1254,8 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
   memcpy(&S.err_c32, &bits[3], 8);
   memcpy(&S.err_r2, &bits[4], 8);
   memcpy(&S.err_c2, &bits[5], 8);
+  memcpy(&S.err_rm, &bits[6], 8);
+  memcpy(&S.err_im, &bits[7], 8);
   S.build_ms = ms;
   S.device_bytes = compact ? (2 * sizeof(uint32_t) << 20) + (S.nx_l + S.nx_c) * (sizeof(uint32_t) + sizeof(double))
                            : 2 * bytes;
@@ -1222,9 +1263,9 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
   if (getenv("SDR_NORMAL_DEBUG"))
     fprintf(stderr,
             "sdr normal mirror: %s, exceptions log1p %d cos %d, verify-mismatch %llu, %.1f ms, %.2f MiB resident;"
-            " calibration r %.3g c %.3g r32 %.3g c32 %.3g r2 %.3g c2 %.3g\n",
+             " calibration r %.3g c %.3g r32 %.3g c32 %.3g r2 %.3g c2 %.3g r32m %.3g / %.3g h\n",
             compact ? "compact" : "full tables", S.nx_l, S.nx_c, bad, ms, S.device_bytes / 1048576.0, S.err_r,
-            S.err_c, S.err_r32, S.err_c32, S.err_r2, S.err_c2);
+            S.err_c, S.err_r32, S.err_c32, S.err_r2, S.err_c2, S.err_rm, S.err_im);
   S.loaded = true;
   if (er) *er = S.err_r;
   if (ec) *ec = S.err_c;
