@@ -126,9 +126,6 @@ __constant__ double c_npoly[9] = {
 #ifndef SDR_NORMAL_BF16_F32
 #define SDR_NORMAL_BF16_F32 1  // certified float32 Box-Muller for bfloat16 outputs
 #endif
-#ifndef SDR_SKIP_MISS
-#define SDR_SKIP_MISS 0  // A/B only (WRONG results): skip the fallback of uncertified elements
-#endif
 #ifndef SDR_NORMAL_BF16_MUFU
 #define SDR_NORMAL_BF16_MUFU 1  // bfloat16 normals: r from MUFU lg2 / rsqrt (r32_mufu) instead of the log table
 #endif
@@ -460,7 +457,7 @@ __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLu
     diff |= l32 ^ h32;
     hiw[e / 2] = h32;
   }
-  if (__builtin_expect(diff != 0, 0) && !SDR_SKIP_MISS) {
+  if (__builtin_expect(diff != 0, 0)) {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       if (out[e] != static_cast<uint16_t>(hiw[e / 2] >> (16 * (e & 1)))) {
@@ -593,7 +590,7 @@ __device__ __forceinline__ void normal_chunk(const DistP& P, const NormalLut* L,
     out[e] = normal_certified<DT>(P, rs[e], c[e], ok);
     badmask |= ok ? 0u : (1u << e);
   }
-  if (__builtin_expect(badmask != 0, 0) && !SDR_SKIP_MISS) {
+  if (__builtin_expect(badmask != 0, 0)) {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       if (badmask & (1u << e)) {
