@@ -50,6 +50,29 @@ def _time(fn, steps, warmup, dev, ws):
     return t.item()
 
 
+_PROBE: dict = {}
+
+
+def _int_roofline(per_gpu_elements_per_s: float, gpu: int) -> dict:
+    """INT-roofline object of a fill line: one Philox4x32-10 block (80 INT32
+    ops) per element, against the live Philox probe and
+    against the IMAD.WIDE pipe ceiling (as bench.py's headline line)."""
+    import ctypes as C
+    from paper_2509_07003_b200 import _lib
+    if gpu not in _PROBE:
+        imad, lop3, phx = C.c_double(), C.c_double(), C.c_double()
+        _lib.check(_lib.LIB.sdr_probe_int32(gpu, C.byref(imad), C.byref(lop3), C.byref(phx)), "sdr_probe_int32")
+        _PROBE[gpu] = phx.value
+    sms = torch.cuda.get_device_properties(gpu).multi_processor_count
+    ceiling = sms * 32 * 1.965e9 / 20  # IMAD.WIDE blocks/s at the 1965 MHz maximum clock
+    achieved = 80 * per_gpu_elements_per_s / 1e12
+    return {"bound": "int32", "achieved": round(achieved, 3), "peak": round(80 * _PROBE[gpu] / 1e12, 3),
+            "unit": "TOP/s INT32 (80 per Philox block, per GPU)",
+            "frac": round(per_gpu_elements_per_s / _PROBE[gpu], 4),
+            "pipe_ceiling": {"peak": round(80 * ceiling / 1e12, 3),
+                             "frac": round(per_gpu_elements_per_s / ceiling, 4)}}
+
+
 def run(a):
     from paper_2509_07003_b200 import create_mesh, init as I, rng as R
     from paper_2509_07003_b200.placement import ShardSpec, local_shape_and_offset, parse_placements
@@ -78,7 +101,8 @@ def run(a):
         line.update(metric="sharded randn GB/s (cfg1)", value=round(n * 4 / ms / 1e6, 3), unit="GB/s",
                     ms_per_step=round(ms, 4), scaling="strong", dtype="f32",
                     config={"workload": "cfg1: randn f32 [4096,4096] Shard(0)", "parallelism": f"dp{ws}",
-                            "elements_per_s": round(n / ms * 1e3, 1)})
+                            "elements_per_s": round(n / ms * 1e3, 1)},
+                    roofline=_int_roofline(math.prod(v.local_shape) / ms * 1e3, gpu))
     elif a.workload == "embed":
         shape = (50257, 4096)
         dp = 2 if ws % 2 == 0 else 1
@@ -103,7 +127,10 @@ def run(a):
                                         "(uniform and bf16 variants in `variants`)",
                             "parallelism": f"dp{dp}xtp{tp}", "local_shape": list(v.local_shape),
                             "elements_per_s": round(n / ms * 1e3, 1),
-                            "variants": {k: {"ms": round(m_, 4), "GB/s": round(g_, 1)} for k, (m_, g_) in rates.items()}})
+                            "variants": {k: {"ms": round(m_, 4), "GB/s": round(g_, 1),
+                                             "int_frac": _int_roofline(math.prod(v.local_shape) / m_ * 1e3, gpu)["frac"]}
+                                         for k, (m_, g_) in rates.items()}},
+                    roofline=_int_roofline(math.prod(v.local_shape) / ms * 1e3, gpu))
     elif a.workload == "init":
         params = I.llama3_8b_params(lambda nm, s: R.Normal(0.0, 0.02), "bfloat16")
         mesh = create_mesh([("tp", ws)])
@@ -123,7 +150,8 @@ def run(a):
                     unit="GB/s", ms_per_step=round(ms, 3), scaling="strong", dtype="bf16",
                     config={"workload": "cfg4: LLaMA-3-8B 291 params normal(0,0.02) bf16, TP placements",
                             "parallelism": f"tp{ws}", "per_gpu_elements": n_local,
-                            "elements_per_s": round(total / ms * 1e3, 1)})
+                            "elements_per_s": round(total / ms * 1e3, 1)},
+                    roofline=_int_roofline(n_local / ms * 1e3, gpu))
     elif a.workload == "peer":
         if ws > 1:
             raise SystemExit("--workload peer emulates all cfg5 ranks on one GPU: run it with N=1")
