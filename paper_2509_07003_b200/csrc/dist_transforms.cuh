@@ -425,7 +425,7 @@ __device__ __forceinline__ void missq_init() {
 template <int NE>
 __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLut32* L32,
                                                   const uint32_t* w0, const uint32_t* w1, uint16_t* out,
-                                                  uint16_t* qdst = nullptr) {
+                                                  uint16_t* qdst = nullptr, int nvalid = NE) {
   static_assert(NE % 2 == 0, "elements go in pairs");
   uint32_t diff = 0, hiw[NE / 2];
 #pragma unroll
@@ -460,7 +460,7 @@ __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLu
   if (__builtin_expect(diff != 0, 0)) {
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
-      if (out[e] != static_cast<uint16_t>(hiw[e / 2] >> (16 * (e & 1)))) {
+      if (e < nvalid && out[e] != static_cast<uint16_t>(hiw[e / 2] >> (16 * (e & 1)))) {
 #if SDR_COUNT_F32_MISS
         atomicAdd(P.nm.fallbacks, 1ull);
 #endif

@@ -223,8 +223,14 @@ __device__ __forceinline__ void fill_chunk_ragged(const FillArgs& A, const Norma
   const uint64_t lq = row * inner + cq * kV;
   const int nvalid = static_cast<int>(min(static_cast<uint64_t>(kV), inner - cq * kV));
   T v[kV];
-  chunk_values<DIST, DT, ALIGNED>(A, L, j0, v);
   T* out = static_cast<T*>(A.out) + lq;
+  if constexpr (uses_missq<DIST, DT>()) {  // queue only the elements this row owns
+    uint32_t w0[kV], w1[kV];
+    fill_words<ALIGNED>(A, j0, w0, w1);
+    normal_chunk_bf16<kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v, out, nvalid);
+  } else {
+    chunk_values<DIST, DT, ALIGNED>(A, L, j0, v);
+  }
 #pragma unroll
   for (int e = 0; e < kV; ++e)
     if (e < nvalid) out[e] = v[e];

@@ -328,14 +328,18 @@ def test_empty_and_single_element_windows():
     assert ops.dropout_apply(x, 0.5, R.RngState()).shape == (0, 4)
 
 
-@pytest.mark.parametrize("dt,mean,std", [(np.float32, 0.0, 1.0), ("bfloat16", 0.0, 0.02),
+@pytest.mark.parametrize("cols", [1400, 1401])  # 1401: ragged rows (per-element stores, queued misses)
+@pytest.mark.parametrize("dt,mean,std", [(np.float32, 0.0, 1.0), ("bfloat16", 0.0, 0.02), ("bfloat16", 3.0, 0.5),
                                          (np.float16, 3.0, 2.0), (np.float32, -7.5, 1e-3)])
-def test_normal_fast_paths_equal_exact_path(dt, mean, std, monkeypatch):
+def test_normal_fast_paths_equal_exact_path(dt, mean, std, cols, monkeypatch):
     """Every Normal element through the exact NumPy-table path (SDR_NORMAL_PATH=exact),
-    through the float64 certified path only (=f64), and the default (float32 path
-    for bfloat16): bit-identical over 2^21 elements of an uneven 2-D window."""
+    through the float64 certified path only (=f64: for bfloat16 every element
+    then misses the float32 path and goes through the per-warp queue, which
+    overflows), and the default: bit-identical over 2^21 elements of an uneven
+    2-D window."""
     shape = (1531, 2053)
-    view = S.ShardView(shape, windows=[S.placement.DimWindow(3, 1500), S.placement.DimWindow(7, 1400)])
+    view = S.ShardView(shape, windows=[S.placement.DimWindow(3, 1500), S.placement.DimWindow(7, cols)])
+    R.ensure_normal_tables()
     outs = {}
     for path in ("exact", "f64", None):
         if path is None:
@@ -345,8 +349,9 @@ def test_normal_fast_paths_equal_exact_path(dt, mean, std, monkeypatch):
         before = R.normal_fallback_count()
         outs[path] = bits(R.fill_random(view, R.RngState(2024, 5, 4096), R.Normal(mean, std), dt))
         torch.cuda.synchronize()
-        if path == "exact":
-            assert R.normal_fallback_count() - before == 1500 * 1400
+        if path == "exact":  # (ragged rows: the float paths also count the discarded tail of a row's last chunk)
+            n = R.normal_fallback_count() - before
+            assert n == 1500 * cols or (cols % 8 and 1500 * cols <= n <= 1500 * (cols + 7))
     assert torch.equal(outs["exact"], outs["f64"]) and torch.equal(outs["exact"], outs[None])
 
 
