@@ -97,6 +97,7 @@ struct NormalMirror {
   double err_r32, err_c32;
   float mean32, std32, b32_r, b32_c;  // B32 = r*b32_r + b32_c
   float bm_r, bm_c, bm_i;             // r32_mufu path: B = r bm_r + h bm_i + bm_c
+  float bmc_r, bmc_i;                 // the same with the MUFU cosine (SDR_BF16_COS_MUFU)
   unsigned long long* fallbacks;
 };
 
@@ -125,6 +126,9 @@ __constant__ double c_npoly[9] = {
     0x1.62e42fefa39efp0};                             // 2 ln 2
 #ifndef SDR_NORMAL_BF16_F32
 #define SDR_NORMAL_BF16_F32 1  // certified float32 Box-Muller for bfloat16 outputs
+#endif
+#ifndef SDR_BF16_COS_MUFU
+#define SDR_BF16_COS_MUFU 1  // bfloat16 normals: cosine from MUFU cos.approx (else the two-level table)
 #endif
 #ifndef SDR_NORMAL_BF16_MUFU
 #define SDR_NORMAL_BF16_MUFU 1  // bfloat16 normals: r from MUFU lg2 / rsqrt (r32_mufu) instead of the log table
@@ -163,7 +167,7 @@ __constant__ double c_npoly[9] = {
 #define SDR_NSPLIT 1      // Normal chunks in NSPLIT parts (Philox + transform per part: fewer live registers)
 #endif
 #ifndef SDR_BF16_MINB
-#define SDR_BF16_MINB SDR_FILL_MINB  // CTAs/SM for the bfloat16 Normal kernels' register budget
+#define SDR_BF16_MINB 3  // CTAs/SM for the bfloat16 Normal kernels' register budget (no tables to stage)
 #endif
 #ifndef SDR_N2_MINB
 #define SDR_N2_MINB 2     // CTAs/SM the NormalLut2 kernels' register budget is sized for (256 threads)
@@ -185,6 +189,14 @@ template <int DIST, int DT>
 constexpr bool uses_lut2() {
   return SDR_NORMAL_N2 && DIST == SDR_NORMAL && (DT == SDR_F32 || DT == SDR_F16);
 }
+// bfloat16 normals with both functions from MUFU need no tables in shared
+// memory (the rare float64 fallbacks read theirs through L1).
+template <int DIST, int DT>
+constexpr bool tablefree() {
+  return SDR_NORMAL_BF16_MUFU && SDR_BF16_COS_MUFU && SDR_NORMAL_BF16_F32 && DIST == SDR_NORMAL && DT == SDR_BF16;
+}
+template <int DIST, int DT>
+constexpr bool stages_lut() { return DIST == SDR_NORMAL && !tablefree<DIST, DT>(); }
 template <int DIST, int DT>
 constexpr int fill_threads() { return uses_lut2<DIST, DT>() ? SDR_N2_THREADS : 256; }
 template <int DIST, int DT>
@@ -325,6 +337,14 @@ __device__ __forceinline__ float r32_mufu(uint32_t w0, float& h) {
   return X * h;
 }
 
+// Hardware cosine of k2 2^-24 turns (cos.approx: the argument times 1/(2 pi)
+// feeds MUFU.COS), absolute error Acm calibrated over all 2^24 inputs.
+__device__ __forceinline__ float c32_mufu(uint32_t w1) {
+  float c;
+  asm("cos.approx.ftz.f32 %0, %1;" : "=f"(c) : "f"(__uint2float_rn(w1 >> 8) * 0x1.921fb6p-22f));
+  return c;
+}
+
 __device__ __forceinline__ float c32_fast(uint32_t w1, const NormalLut32* L) {
   const float2 a = lut_at(L->trig_hi, (w1 >> 17) & 0x7FF8u);  // hi = k >> 12
 #if SDR_C32_POLY
@@ -402,7 +422,10 @@ __device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, const
 // The queued element's slot already holds a placeholder from the chunk's
 // vector store; the flush overwrites it after a __syncwarp (memory order
 // between the warp's threads).  A full queue falls back to the inline path.
-constexpr int kMissQ = 96;
+#ifndef SDR_MISSQ_N
+#define SDR_MISSQ_N 256
+#endif
+constexpr int kMissQ = SDR_MISSQ_N;
 struct MissQ {
   uint4 e[kMissQ];  // (address lo, address hi, w0, w1)
   uint32_t n;
@@ -435,10 +458,16 @@ __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLu
     for (int i = 0; i < 2; ++i) {
 #if SDR_NORMAL_BF16_MUFU
       float h;
+#if SDR_BF16_COS_MUFU
+      const float r = r32_mufu(w0[e + i], h), c = c32_mufu(w1[e + i]);
+      const float v = fmaf(P.nm.std32, r * c, P.nm.mean32);
+      const float B = fmaf(h, P.nm.bmc_i, fmaf(r, P.nm.bmc_r, P.nm.bm_c));
+#else
       const float r = r32_mufu(w0[e + i], h), c = c32_fast(w1[e + i], L32);
       const float v = fmaf(P.nm.std32, r * c, P.nm.mean32);
       // |v - v_numpy| <= r*bm_r + h*bm_i + bm_c   (host: fill_dist_params)
       const float B = fmaf(h, P.nm.bm_i, fmaf(r, P.nm.bm_r, P.nm.bm_c));
+#endif
 #else
       const float r = r32_fast(w0[e + i], L32), c = c32_fast(w1[e + i], L32);
       const float v = fmaf(P.nm.std32, r * c, P.nm.mean32);

@@ -239,6 +239,7 @@ __device__ __forceinline__ void fill_chunk_ragged(const FillArgs& A, const Norma
 template <int DIST, int DT>
 __device__ __forceinline__ void fill_elem(const FillArgs& A, const NormalLut* L, uint64_t i) {
   using T = typename St<DT>::T;
+  if constexpr (tablefree<DIST, DT>()) L = A.d.nm.lut;  // nothing staged: the float64 tables through L1
   uint32_t w0, w1;
   elem_words(A.g, A.ix.global_of(i), w0, w1);
   static_cast<T*>(A.out)[i] = dist_value<DIST, DT>(A.d, L, w0, w1);
@@ -252,7 +253,9 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
 #endif
   const NormalLut* L = nullptr;
   uint32_t bar = 0;  // Normal: tables arriving by TMA (waited on before first use)
-  if constexpr (uses_lut2<DIST, DT>()) {
+  if constexpr (tablefree<DIST, DT>()) {
+    // bfloat16 on the MUFU functions: nothing to stage
+  } else if constexpr (uses_lut2<DIST, DT>()) {
     extern __shared__ __align__(16) unsigned char s_dyn[];  // sizeof(NormalLut2), set at launch
     NormalLut2* s_lut2 = reinterpret_cast<NormalLut2*>(s_dyn);
     bar = stage_lut_begin(s_lut2, A.d.nm.lut2);
@@ -289,7 +292,7 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
       ChunkHoist H = hoist_chunk(A.g, j);
       uint32_t a0[4], a1[4], b0[4], b1[4];
       words_part<4, 0>(A.g.keys, H, a0, a1);
-      stage_lut_wait(bar);
+      if constexpr (stages_lut<DIST, DT>()) stage_lut_wait(bar);
       for (; q < A.nchunks; q += stride) {
         T v[kV];
         words_part<4, 4>(A.g.keys, H, b0, b1);
@@ -312,7 +315,7 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
       using T = typename St<DT>::T;
       uint32_t w0[kV], w1[kV];
       fill_words<ALIGNED>(A, j, w0, w1);
-      stage_lut_wait(bar);
+      if constexpr (stages_lut<DIST, DT>()) stage_lut_wait(bar);
       for (; q < A.nchunks; q += stride) {
         uint64_t jn = j, cqn = cq;
         walk_next(A.walk, A.chunks_per_row, jn, cqn);
@@ -335,7 +338,7 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
         using T = typename St<DT>::T;
         uint32_t w0[kV], w1[kV];
         fill_words<ALIGNED>(A, j, w0, w1);
-        stage_lut_wait(bar);
+        if constexpr (stages_lut<DIST, DT>()) stage_lut_wait(bar);
         T v[kV];
         T* dst = static_cast<T*>(A.out) + q * kV;
         if constexpr (uses_missq<DIST, DT>())
@@ -345,7 +348,7 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
         store_chunk(dst, v);
         walk_next(A.walk, A.chunks_per_row, j, cq);
         q += stride;
-      } else {
+      } else if constexpr (stages_lut<DIST, DT>()) {
         stage_lut_wait(bar);
       }
     }
@@ -354,10 +357,10 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
       walk_next(A.walk, A.chunks_per_row, j, cq);
     }
   } else if (A.ragged) {
-    if constexpr (DIST == SDR_NORMAL) stage_lut_wait(bar);
+    if constexpr (stages_lut<DIST, DT>()) stage_lut_wait(bar);
     for (; q < A.nchunks; q += stride) fill_chunk_ragged<DIST, DT, ALIGNED>(A, L, q);
   } else {
-    if constexpr (DIST == SDR_NORMAL) stage_lut_wait(bar);
+    if constexpr (stages_lut<DIST, DT>()) stage_lut_wait(bar);
     for (; q < A.nchunks; q += stride) fill_chunk<DIST, DT, ALIGNED>(A, L, q);
   }
   if constexpr (uses_missq<DIST, DT>()) missq_flush(A.d);  // every thread gets here: the warp is converged
@@ -394,7 +397,9 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
   __shared__ __align__(16) unsigned char smem[sizeof(FillArgs)];
   FillArgs& A = *reinterpret_cast<FillArgs*>(smem);
   const NormalLut* L = nullptr;
-  if constexpr (uses_lut2<DIST, DT>()) {
+  if constexpr (tablefree<DIST, DT>()) {
+    // bfloat16 on the MUFU functions: nothing to stage
+  } else if constexpr (uses_lut2<DIST, DT>()) {
     extern __shared__ __align__(16) unsigned char s_dyn[];  // sizeof(NormalLut2), set at launch
     NormalLut2* s_lut2 = reinterpret_cast<NormalLut2*>(s_dyn);
     stage_lut(s_lut2, descs[0].d.nm.lut2);
@@ -532,7 +537,7 @@ __global__ void k_normal_calibrate(const double* ltab, const double* ctab, const
 // Calibration of r32_mufu (bfloat16 path) over k in [1, 2^24): out[0] = Er =
 // max |r - r_np| / r where r >= 1, out[1] = Ei = max |r - r_np| / h where r < 1,
 // so |r - r_np| <= Er r + Ei h everywhere.  k = 0 is never certified (h = 2^60).
-__global__ void k_normal_calibrate_mufu(const double* ltab, unsigned long long* out) {
+__global__ void k_normal_calibrate_mufu(const double* ltab, const double* ctab, unsigned long long* out) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= (1u << 24)) return;
   const double inf = __longlong_as_double(0x7FF0000000000000ll);
@@ -545,10 +550,12 @@ __global__ void k_normal_calibrate_mufu(const double* ltab, unsigned long long* 
     else if (r >= 1.0) er = e / r;
     else ei = e / static_cast<double>(h);
   }
-  unsigned long long b[2] = {static_cast<unsigned long long>(__double_as_longlong(er)),
-                             static_cast<unsigned long long>(__double_as_longlong(ei))};
+  const double ec = fabs(static_cast<double>(c32_mufu(k << 8)) - ctab[k]);  // MUFU cosine, absolute
+  unsigned long long b[3] = {static_cast<unsigned long long>(__double_as_longlong(er)),
+                             static_cast<unsigned long long>(__double_as_longlong(ei)),
+                             static_cast<unsigned long long>(__double_as_longlong(isnan(ec) ? inf : ec))};
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 3; ++i) {
     for (int o = 16; o > 0; o >>= 1) b[i] = max(b[i], __shfl_xor_sync(0xffffffffu, b[i], o));
     if ((threadIdx.x & 31) == 0) atomicMax(out + i, b[i]);
   }
@@ -718,7 +725,7 @@ struct NormalState {
   NormalLut2* lut2 = nullptr;
   unsigned long long* fallbacks = nullptr;
   double err_r = 0, err_c = 0, err_r32 = 0, err_c32 = 0, err_r2 = 0, err_c2 = 0;
-  double err_rm = 0, err_im = 0;  // r32_mufu (bfloat16 path)
+  double err_rm = 0, err_im = 0, err_cm = 0;  // r32_mufu, c32_mufu (bfloat16 path)
   bool loaded = false;
 };
 static std::mutex g_nm_mu;
@@ -899,14 +906,19 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
                                          fabs(static_cast<double>(P.nm.std32)) * 0x1p-22 * (1.0 + 0x1p-20));
           P.nm.bm_i = static_cast<float>(2.04 * fabs(P.stdv) * Eim * (1.0 + 0x1p-20) * (1.0 + Ac32) + 0x1p-140);
           P.nm.bm_c = P.nm.b32_c;
+          const double Acm = g_nm[device].err_cm;  // the same bound with the MUFU cosine
+          P.nm.bmc_r = static_cast<float>(2.04 * fabs(P.stdv) * (Erm + Acm * (1.0 + Erm) + 0x1p-23) + 0x1p-60 +
+                                          fabs(static_cast<double>(P.nm.std32)) * 0x1p-22 * (1.0 + 0x1p-20));
+          P.nm.bmc_i = static_cast<float>(2.04 * fabs(P.stdv) * Eim * (1.0 + 0x1p-20) * (1.0 + Acm) + 0x1p-140);
+          if (!(Acm < 0x1p-12)) P.nm.bmc_r = INFINITY;
           if (!(Erm < 0x1p-12) || !(Eim < 0x1p-12) || !(P.nm.b32_r < INFINITY))
-            P.nm.bm_r = INFINITY;  // calibration failed: every element takes the float64 path
+            P.nm.bm_r = P.nm.bmc_r = INFINITY;  // calibration failed: every element takes the float64 path
         }
         // Test hook: SDR_NORMAL_PATH=exact sends every element through the NumPy
         // tables, =f64 skips the float32 path (results must be identical).
         if (const char* path = getenv("SDR_NORMAL_PATH")) {
-          if (strcmp(path, "exact") == 0) P.nm.kr = P.nm.kr2 = P.nm.b32_r = P.nm.bm_r = INFINITY;
-          if (strcmp(path, "f64") == 0) P.nm.b32_r = P.nm.bm_r = INFINITY;
+          if (strcmp(path, "exact") == 0) P.nm.kr = P.nm.kr2 = P.nm.b32_r = P.nm.bm_r = P.nm.bmc_r = INFINITY;
+          if (strcmp(path, "f64") == 0) P.nm.b32_r = P.nm.bm_r = P.nm.bmc_r = INFINITY;
         }
       }
       P.nm.fallbacks = g_nm[device].fallbacks;
@@ -941,7 +953,8 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
 template <int DIST, int DT>
 static constexpr size_t fill_dyn_smem() {
   return uses_lut2<DIST, DT>() ? sizeof(NormalLut2)
-         : (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) ? sizeof(NormalLut32) : 0;
+         : (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32 && !tablefree<DIST, DT>())
+               ? sizeof(NormalLut32) : 0;
 }
 template <typename K>
 static void allow_dyn_smem(K kernel, size_t bytes) {
@@ -1129,7 +1142,7 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
   cudaEventRecord(t0);
   cudaError_t e = cudaSuccess;
   if (S.lut == nullptr) {
-    e = cudaMalloc(&S.fallbacks, 9 * sizeof(unsigned long long));
+    e = cudaMalloc(&S.fallbacks, 10 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMalloc(&S.lut, sizeof(NormalLut));
     if (e == cudaSuccess) e = cudaMalloc(&S.lut32, sizeof(NormalLut32));
     if (e == cudaSuccess) e = cudaMalloc(&S.lut2, sizeof(NormalLut2));
@@ -1163,12 +1176,12 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
   if (e == cudaSuccess) e = cudaMalloc(&dc, bytes);
   if (e == cudaSuccess) e = cudaMemcpy(dl, l_host, bytes, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(dc, c_host, bytes, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemset(S.fallbacks, 0, 9 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(S.fallbacks, 0, 10 * sizeof(unsigned long long));
   // (3) calibration of the fast paths against the full tables
   if (e == cudaSuccess) {
     k_normal_calibrate<<<(1u << 24) / 256, 256>>>(dl, dc, S.lut, S.lut32, S.lut2, S.fallbacks + 1,
                                                   S.fallbacks + 2);
-    k_normal_calibrate_mufu<<<(1u << 24) / 256, 256>>>(dl, S.fallbacks + 7);
+    k_normal_calibrate_mufu<<<(1u << 24) / 256, 256>>>(dl, dc, S.fallbacks + 7);
     e = cudaGetLastError();
   }
   // (1) codes + unsorted exceptions
@@ -1235,9 +1248,9 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
     S.xv = nullptr;
   }
   // fallbacks[1..6] = max err of r, c (NormalLut), r32, c32 (float32 path), r2, c2 (NormalLut2);
-  // [7..8] = Er, Ei of r32_mufu
-  unsigned long long bits[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (e == cudaSuccess) e = cudaMemcpy(bits, S.fallbacks + 1, 8 * sizeof(bits[0]), cudaMemcpyDeviceToHost);
+  // [7..9] = Er, Ei of r32_mufu, Ac of c32_mufu
+  unsigned long long bits[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpy(bits, S.fallbacks + 1, 9 * sizeof(bits[0]), cudaMemcpyDeviceToHost);
   cudaFree(dl);
   cudaFree(dc);
   cudaFree(xk);
@@ -1262,6 +1275,7 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
   memcpy(&S.err_c2, &bits[5], 8);
   memcpy(&S.err_rm, &bits[6], 8);
   memcpy(&S.err_im, &bits[7], 8);
+  memcpy(&S.err_cm, &bits[8], 8);
   S.build_ms = ms;
   S.device_bytes = compact ? (2 * sizeof(uint32_t) << 20) + (S.nx_l + S.nx_c) * (sizeof(uint32_t) + sizeof(double))
                            : 2 * bytes;
@@ -1269,9 +1283,9 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
   if (getenv("SDR_NORMAL_DEBUG"))
     fprintf(stderr,
             "sdr normal mirror: %s, exceptions log1p %d cos %d, verify-mismatch %llu, %.1f ms, %.2f MiB resident;"
-             " calibration r %.3g c %.3g r32 %.3g c32 %.3g r2 %.3g c2 %.3g r32m %.3g / %.3g h\n",
+             " calibration r %.3g c %.3g r32 %.3g c32 %.3g r2 %.3g c2 %.3g r32m %.3g / %.3g h c32m %.3g\n",
             compact ? "compact" : "full tables", S.nx_l, S.nx_c, bad, ms, S.device_bytes / 1048576.0, S.err_r,
-            S.err_c, S.err_r32, S.err_c32, S.err_r2, S.err_c2, S.err_rm, S.err_im);
+            S.err_c, S.err_r32, S.err_c32, S.err_r2, S.err_c2, S.err_rm, S.err_im, S.err_cm);
   S.loaded = true;
   if (er) *er = S.err_r;
   if (ec) *ec = S.err_c;
