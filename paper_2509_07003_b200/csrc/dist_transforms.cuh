@@ -481,7 +481,7 @@ __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLu
     uint32_t l32, h32;
     memcpy(&l32, &pl, 4);
     memcpy(&h32, &ph, 4);
-    out[e] = static_cast<uint16_t>(l32);
+    out[e] = static_cast<uint16_t>(l32);  // (copying the packed word whole measured 3% slower)
     out[e + 1] = static_cast<uint16_t>(l32 >> 16);
     diff |= l32 ^ h32;
     hiw[e / 2] = h32;
