@@ -36,6 +36,12 @@ def _time(fn, steps, warmup, dev, ws):
     if ws > 1:
         dist.barrier()
     a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+    # a short device spin queued before the start event lets the host enqueue
+    # the first step while the GPU is busy, so the timed region measures the
+    # steady state (a step's host work -- e.g. 3 ms to build the 291
+    # descriptors of the LLaMA-3-8B init -- overlaps the previous step's GPU
+    # work) instead of the first step's host latency
+    torch.cuda._sleep(int(5e6))
     a.record()
     for _ in range(steps):
         fn()
