@@ -361,3 +361,26 @@ def test_materialize_captures_in_cuda_graph():
     torch.cuda.synchronize()
     for name in eager:
         assert torch.equal(bits(got[name]), bits(eager[name])), name
+
+
+def test_materialize_bf16_normal_miss_queue_overflow(monkeypatch):
+    """The batched bfloat16 Normal init resolves uncertified elements through
+    the per-warp queue, flushed per tile.  With SDR_NORMAL_PATH=f64 every
+    element misses the float32 path (the queue overflows into the inline
+    path); with =exact every element takes the NumPy mirror: all three runs
+    are bit-identical."""
+    def params():
+        return {f"w{i}": I.Parameter((300 + 7 * i, 520), R.Normal(0.5 * i, 0.02 + 0.1 * i), "bfloat16")
+                for i in range(5)}
+    R.ensure_normal_tables()
+    outs = {}
+    for path in (None, "f64", "exact"):
+        if path is None:
+            monkeypatch.delenv("SDR_NORMAL_PATH", raising=False)
+        else:
+            monkeypatch.setenv("SDR_NORMAL_PATH", path)
+        outs[path] = I.materialize(params(), R.RngState(99))
+    torch.cuda.synchronize()
+    for name in outs[None]:
+        assert torch.equal(bits(outs[None][name]), bits(outs["f64"][name])), name
+        assert torch.equal(bits(outs[None][name]), bits(outs["exact"][name])), name
