@@ -106,6 +106,7 @@ template <int DIST, int DT>
 constexpr bool uses_missq() {
   return SDR_MISSQ && DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32 && SDR_NSPLIT == 1;
 }
+static_assert(fill_threads<SDR_NORMAL, SDR_BF16>() <= 256, "MissQ (dist_transforms.cuh) holds 8 warps' queues");
 
 template <int DIST, int DT, bool ALIGNED>
 __device__ __forceinline__ void fill_chunk(const FillArgs& A, const NormalLut* L, uint64_t q) {
