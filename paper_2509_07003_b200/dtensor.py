@@ -324,14 +324,18 @@ def _alloc_layout(shapes, dtypes):
 
 def _alloc_outputs(layout_, dev):
     """The step's output tensors: one caching-allocator call per dtype (the
-    members share that storage's lifetime) instead of one per member."""
+    members share that storage's lifetime) instead of one per member, and
+    their data pointers (None for empty members) from the base address."""
     groups, n = layout_
-    outs = [None] * n
+    outs, ptrs = [None] * n, [None] * n
     for dt, total, views in groups:
         buf = torch.empty(total, dtype=dt, device=dev)
+        base, es = buf.data_ptr(), dt.itemsize
         for j, shp, st, off in views:
             outs[j] = buf.as_strided(shp, st, off)
-    return outs
+            if math.prod(shp):
+                ptrs[j] = base + off * es
+    return outs, ptrs
 
 
 class _Plan:
@@ -356,19 +360,19 @@ class _Plan:
             for kind, d in self.steps:
                 if kind == "slice":
                     idxs, shapes, full_arr, piece_arr, k, P, lay = d
-                    outs = _alloc_outputs(lay, dev)
+                    outs, optr = _alloc_outputs(lay, dev)
                     for j, i in enumerate(idxs):
                         full_arr[j].data = cur[i].data_ptr() if cur[i].numel() else None
-                        piece_arr[j].data = outs[j].data_ptr() if outs[j].numel() else None
+                        piece_arr[j].data = optr[j]
                     _lib.check(_lib.LIB.sdr_slice_local(full_arr, piece_arr, len(idxs), k, P, s), "sdr_slice_local")
                 else:
                     idxs, shapes, hp, buckets, led, lay = d
-                    outs = _alloc_outputs(lay, dev)
+                    outs, optr = _alloc_outputs(lay, dev)
                     for bidx, seg, a_in, a_out, dcode, nbytes in buckets:
                         for j, b in enumerate(bidx):
-                            t_in, t_out = cur[idxs[b]], outs[b]
+                            t_in = cur[idxs[b]]
                             a_in[j].data = t_in.data_ptr() if t_in.numel() else None
-                            a_out[j].data = t_out.data_ptr() if t_out.numel() else None
+                            a_out[j].data = optr[b]
                         if kind == "gather":
                             hp.all_gather_arrays(a_in, a_out, len(bidx), s, ordered=True)
                         else:
