@@ -94,6 +94,7 @@ def _load():
         "sdr_normal_tables_load": (C.c_int32, [C.c_int32, C.c_void_p, C.c_void_p,
                                                P(C.c_double), P(C.c_double)]),
         "sdr_normal_tables_loaded": (C.c_int32, [C.c_int32]),
+        "sdr_normal_delta_info": (C.c_int32, [C.c_int32] + [P(C.c_uint64)] * 5),
         "sdr_normal_mirror_info": (C.c_int32, [C.c_int32, P(C.c_uint64), P(C.c_uint64), P(C.c_int32),
                                                P(C.c_double)]),
         "sdr_normal_fallback_count": (C.c_int32, [C.c_int32, P(C.c_uint64)]),
@@ -137,7 +138,7 @@ LIB = _load()
 EXPORTED = (
     "sdr_version", "sdr_strerror", "sdr_last_cuda_error", "sdr_philox_block_host",
     "sdr_philox_blocks", "sdr_fill", "sdr_transform", "sdr_fill_batch", "sdr_dropout", "sdr_normal_tables_load",
-    "sdr_normal_tables_loaded", "sdr_normal_mirror_info", "sdr_normal_fallback_count", "sdr_unpack_gathered",
+    "sdr_normal_tables_loaded", "sdr_normal_mirror_info", "sdr_normal_delta_info", "sdr_normal_fallback_count", "sdr_unpack_gathered",
     "sdr_pack_scatter", "sdr_pack_local", "sdr_unpack_local", "sdr_slice_local", "sdr_probe_int32",
     "sdr_peer_heap_alloc", "sdr_peer_heap_open", "sdr_peer_heap_close", "sdr_peer_heap_free",
     "sdr_peer_barrier", "sdr_peer_flag_read", "sdr_unpack_gathered_peers", "sdr_reduce_scatter_peers",

@@ -17,6 +17,8 @@ int normal_tables_load(int device, const double* r_host, const double* c_host, d
 int normal_tables_loaded(int device);
 int normal_mirror_info(int device, uint64_t* device_bytes, uint64_t* exceptions, int32_t* compact,
                        double* build_ms);
+int normal_delta_info(int device, uint64_t* device_bytes, uint64_t* escapes_r, uint64_t* escapes_c,
+                      uint64_t* max_abs_r, uint64_t* max_abs_c);
 int normal_fallback_count(int device, uint64_t* count);
 int probe_int32(int device, double* imad_per_s, double* lop3_per_s, double* philox_per_s);
 const char* last_cuda_error();
@@ -110,6 +112,10 @@ int32_t sdr_normal_mirror_info(int32_t device, uint64_t* device_bytes, uint64_t*
   return sdr::normal_mirror_info(device, device_bytes, exceptions, compact, build_ms);
 }
 
+int32_t sdr_normal_delta_info(int32_t device, uint64_t* device_bytes, uint64_t* escapes_r, uint64_t* escapes_c,
+                              uint64_t* max_abs_r, uint64_t* max_abs_c) {
+  return sdr::normal_delta_info(device, device_bytes, escapes_r, escapes_c, max_abs_r, max_abs_c);
+}
 int32_t sdr_normal_fallback_count(int32_t device, uint64_t* count) {
   return sdr::normal_fallback_count(device, count);
 }

@@ -173,7 +173,9 @@ __device__ __forceinline__ void values_from_words(const FillArgs& A, const Norma
     normal_chunk_bf16<kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v);
   } else if constexpr (uses_lut2<DIST, DT>()) {
     normal_chunk2<DT, kV>(A.d, reinterpret_cast<const NormalLut2*>(L), w0, w1, v);
-  } else if constexpr (DIST == SDR_NORMAL && DT != SDR_F64) {
+  } else if constexpr (DIST == SDR_NORMAL && DT == SDR_F64) {
+    normal_chunk_f64<kV>(A.d, L, w0, w1, v);
+  } else if constexpr (DIST == SDR_NORMAL) {
     constexpr int NS = SDR_NORMAL_SPLIT;
 #pragma unroll
     for (int h = 0; h < NS; ++h)
@@ -649,6 +651,40 @@ __global__ void k_mirror_verify(const ExactMirror M, const double* __restrict__ 
   if (!ok) atomicAdd(bad, 1ull);
 }
 
+// float64 Normal corrections (normal_chunk_f64): for every table point k the
+// difference between the bits of NumPy's r[k] / c[k] (the verified mirror, or
+// the full tables) and of the fast functions, kDeltaEsc when it does not fit
+// in 16 bits.  stats[0..1]: escapes of r / c, stats[2..3]: max |difference|
+// stored.
+__global__ void k_normal_deltas(const ExactMirror M, const double* __restrict__ rtab,
+                                const double* __restrict__ ctab, const NormalLut* lut, int16_t* dr,
+                                int16_t* dc, unsigned long long* stats) {
+  __shared__ __align__(16) NormalLut s_lut;
+  stage_lut(&s_lut, lut);  // as the fill kernels read it
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (1u << 24)) return;
+  const double rn = rtab != nullptr ? rtab[k] : mirror_r(M, k);
+  const double cn = ctab != nullptr ? ctab[k] : mirror_c(M, k);
+  const long long a = __double_as_longlong(rn) - __double_as_longlong(r_fast(k << 8, &s_lut, -0.5, 1.5));
+  const long long b = __double_as_longlong(cn) - __double_as_longlong(c_fast(k << 8, &s_lut));
+  const bool fa = a > kDeltaEsc && a < 32768, fb = b > kDeltaEsc && b < 32768;
+  dr[k] = static_cast<int16_t>(fa ? a : kDeltaEsc);
+  dc[k] = static_cast<int16_t>(fb ? b : kDeltaEsc);
+  const unsigned ea = __popc(__ballot_sync(0xffffffffu, !fa)), eb = __popc(__ballot_sync(0xffffffffu, !fb));
+  unsigned long long ma = fa ? static_cast<unsigned long long>(a < 0 ? -a : a) : 0ull;
+  unsigned long long mb = fb ? static_cast<unsigned long long>(b < 0 ? -b : b) : 0ull;
+  for (int o = 16; o > 0; o >>= 1) {
+    ma = max(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+    mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (ea) atomicAdd(stats, static_cast<unsigned long long>(ea));
+    if (eb) atomicAdd(stats + 1, static_cast<unsigned long long>(eb));
+    atomicMax(stats + 2, ma);
+    atomicMax(stats + 3, mb);
+  }
+}
+
 // Full-table fallback: r[k] = sqrt(-2 L[k]) in place.
 __global__ void k_r_from_l(double* t) {
   const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -764,6 +800,8 @@ struct NormalState {
   unsigned long long* fallbacks = nullptr;
   double err_r = 0, err_c = 0, err_r32 = 0, err_c32 = 0, err_r2 = 0, err_c2 = 0;
   double err_rm = 0, err_im = 0, err_cm = 0;  // r32_mufu, c32_mufu (bfloat16 path)
+  int16_t* delta = nullptr;            // float64 corrections dr[2^24] then dc[2^24], or null
+  unsigned long long delta_stats[4] = {0, 0, 0, 0};  // escapes r / c, max |difference| r / c
   bool loaded = false;
 };
 static std::mutex g_nm_mu;
@@ -898,6 +936,8 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
       P.nm.lut = g_nm[device].lut;
       P.nm.lut32 = g_nm[device].lut32;
       P.nm.lut2 = g_nm[device].lut2;
+      P.nm.dr = g_nm[device].delta;
+      P.nm.dc = g_nm[device].delta ? g_nm[device].delta + (1u << 24) : nullptr;
       {
         // float64 fast path (see normal_certified): with Er, Ec the calibrated
         // errors of r_fast / c_fast and u = 2^-53,
@@ -955,7 +995,10 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
         // Test hook: SDR_NORMAL_PATH=exact sends every element through the NumPy
         // tables, =f64 skips the float32 path (results must be identical).
         if (const char* path = getenv("SDR_NORMAL_PATH")) {
-          if (strcmp(path, "exact") == 0) P.nm.kr = P.nm.kr2 = P.nm.b32_r = P.nm.bm_r = P.nm.bmc_r = INFINITY;
+          if (strcmp(path, "exact") == 0) {
+            P.nm.kr = P.nm.kr2 = P.nm.b32_r = P.nm.bm_r = P.nm.bmc_r = INFINITY;
+            P.nm.dr = P.nm.dc = nullptr;
+          }
           if (strcmp(path, "f64") == 0) P.nm.b32_r = P.nm.bm_r = P.nm.bmc_r = INFINITY;
         }
       }
@@ -1197,6 +1240,8 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
     }
   }
   // a reload replaces the previous mirror
+  cudaFree(S.delta);
+  S.delta = nullptr;
   cudaFree(S.rtab);
   cudaFree(S.ctab);
   cudaFree(S.code);
@@ -1285,6 +1330,27 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
     S.code = S.xk = nullptr;
     S.xv = nullptr;
   }
+  // float64 corrections against whichever exact form is resident
+  // (SDR_NORMAL_F64_DELTA=0: float64 outputs take the mirror per element)
+  const char* dflag = getenv("SDR_NORMAL_F64_DELTA");
+  if (e == cudaSuccess && !(dflag != nullptr && strcmp(dflag, "0") == 0)) {
+    unsigned long long* st = nullptr;
+    e = cudaMalloc(&S.delta, sizeof(int16_t) << 25);
+    if (e == cudaSuccess) e = cudaMalloc(&st, 4 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(st, 0, 4 * sizeof(unsigned long long));
+    if (e == cudaSuccess) {
+      ExactMirror M{S.code, S.code ? S.code + (1u << 20) : nullptr, S.xk, S.xv,
+                    S.xk ? S.xk + S.nx_l : nullptr, S.xv ? S.xv + S.nx_l : nullptr, S.nx_l, S.nx_c};
+      k_normal_deltas<<<(1u << 24) / 256, 256>>>(M, S.rtab, S.ctab, S.lut, S.delta, S.delta + (1u << 24), st);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(S.delta_stats, st, sizeof(S.delta_stats), cudaMemcpyDeviceToHost);
+    cudaFree(st);
+    if (e != cudaSuccess) {
+      cudaFree(S.delta);
+      S.delta = nullptr;
+    }
+  }
   // fallbacks[1..6] = max err of r, c (NormalLut), r32, c32 (float32 path), r2, c2 (NormalLut2);
   // [7..9] = Er, Ei of r32_mufu, Ac of c32_mufu
   unsigned long long bits[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -1324,6 +1390,9 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
              " calibration r %.3g c %.3g r32 %.3g c32 %.3g r2 %.3g c2 %.3g r32m %.3g / %.3g h c32m %.3g\n",
             compact ? "compact" : "full tables", S.nx_l, S.nx_c, bad, ms, S.device_bytes / 1048576.0, S.err_r,
             S.err_c, S.err_r32, S.err_c32, S.err_r2, S.err_c2, S.err_rm, S.err_im, S.err_cm);
+  if (getenv("SDR_NORMAL_DEBUG"))
+    fprintf(stderr, "sdr normal float64 corrections: %s, escapes r %llu c %llu, max |d| r %llu c %llu\n",
+            S.delta ? "built" : "off", S.delta_stats[0], S.delta_stats[1], S.delta_stats[2], S.delta_stats[3]);
   S.loaded = true;
   if (er) *er = S.err_r;
   if (ec) *ec = S.err_c;
@@ -1339,6 +1408,20 @@ int normal_mirror_info(int device, uint64_t* device_bytes, uint64_t* exceptions,
   if (exceptions) *exceptions = static_cast<uint64_t>(S.nx_l + S.nx_c);
   if (compact) *compact = S.rtab == nullptr ? 1 : 0;
   if (build_ms) *build_ms = S.build_ms;
+  return SDR_OK;
+}
+
+int normal_delta_info(int device, uint64_t* device_bytes, uint64_t* escapes_r, uint64_t* escapes_c,
+                      uint64_t* max_abs_r, uint64_t* max_abs_c) {
+  std::lock_guard<std::mutex> lk(g_nm_mu);
+  if (device < 0 || device >= 64 || !g_nm[device].loaded) return SDR_E_NOTABLES;
+  const NormalState& S = g_nm[device];
+  const bool on = S.delta != nullptr;
+  if (device_bytes) *device_bytes = on ? sizeof(int16_t) << 25 : 0;
+  if (escapes_r) *escapes_r = on ? S.delta_stats[0] : 0;
+  if (escapes_c) *escapes_c = on ? S.delta_stats[1] : 0;
+  if (max_abs_r) *max_abs_r = on ? S.delta_stats[2] : 0;
+  if (max_abs_c) *max_abs_c = on ? S.delta_stats[3] : 0;
   return SDR_OK;
 }
 

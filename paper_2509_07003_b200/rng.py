@@ -256,6 +256,18 @@ def normal_mirror_info(device=None) -> dict:
             "build_ms": ms.value}
 
 
+def normal_delta_info(device=None) -> dict:
+    """The float64 Normal corrections on `device` (sdr_normal_delta_info):
+    resident bytes (0 when SDR_NORMAL_F64_DELTA=0), the table points that
+    escape to the mirror, and the largest stored correction of r and c."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    v = [C.c_uint64() for _ in range(5)]
+    _lib.check(_lib.LIB.sdr_normal_delta_info(idx, *[C.byref(x) for x in v]), "sdr_normal_delta_info")
+    return {"device_bytes": v[0].value, "escapes_r": v[1].value, "escapes_c": v[2].value,
+            "max_abs_r": v[3].value, "max_abs_c": v[4].value}
+
+
 def normal_fallback_count(device=None) -> int:
     idx = torch.cuda.current_device() if device is None else torch.device(device).index
     n = C.c_uint64()
