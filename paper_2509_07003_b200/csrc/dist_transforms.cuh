@@ -159,6 +159,9 @@ __constant__ double c_npoly[9] = {
 #ifndef SDR_FILL_MINB
 #define SDR_FILL_MINB 2   // CTAs/SM the register budget of the fill kernels is sized for
 #endif
+#ifndef SDR_F64N_MINB
+#define SDR_F64N_MINB 2   // CTAs/SM for the float64 Normal fills (latency-bound on their L2 gathers)
+#endif
 #ifndef SDR_NORMAL_N2
 #define SDR_NORMAL_N2 0   // float32/float16 normals on the NormalLut2 tables (else NormalLut)
 #endif
@@ -204,7 +207,8 @@ constexpr int fill_threads() { return uses_lut2<DIST, DT>() ? SDR_N2_THREADS : 2
 template <int DIST, int DT>
 constexpr int fill_minb() {
   return uses_lut2<DIST, DT>() ? SDR_N2_MINB * 256 / SDR_N2_THREADS
-         : (DIST == SDR_NORMAL && DT == SDR_BF16) ? SDR_BF16_MINB : SDR_FILL_MINB;
+         : (DIST == SDR_NORMAL && DT == SDR_BF16) ? SDR_BF16_MINB
+         : (DIST == SDR_NORMAL && DT == SDR_F64) ? SDR_F64N_MINB : SDR_FILL_MINB;
 }
 
 __host__ __device__ __forceinline__ double hilo(uint32_t hi, uint32_t lo) {
