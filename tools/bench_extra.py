@@ -1,7 +1,8 @@
 """Secondary bench workloads (BASELINE configs 1, 3, 4, 5), same JSON shape as
 bench.py's main line.  `python bench.py --workload randn|embed|init|redistribute`.
 
-randn        cfg1: Normal(0,1) f32 [4096,4096] Shard(0) over N ranks (strong)
+randn        cfg1: Normal(0,1) f32 [4096,4096] Shard(0) over N ranks (strong); plus the
+             same window in float64 (the reference's default dtype) as a sub-object
 embed        cfg3: [50257,4096] embedding on a DP x TP mesh, Shard(0),Shard(1)
              (uneven rows): Normal(0,0.02) and the std-matched Uniform, f32 and
              bf16 (strong; value = normal f32)
@@ -109,6 +110,13 @@ def run(a):
                     config={"workload": "cfg1: randn f32 [4096,4096] Shard(0)", "parallelism": f"dp{ws}",
                             "elements_per_s": round(n / ms * 1e3, 1)},
                     roofline=_int_roofline(math.prod(v.local_shape) / ms * 1e3, gpu))
+        # the same window in float64, the reference's default dtype (per-point corrections)
+        out64 = torch.empty(v.local_shape, dtype=torch.float64, device=dev)
+        ms64 = _time(lambda: R.fill_random(v, st, R.Normal(0, 1), np.float64, out=out64), a.steps, a.warmup, dev, ws)
+        line["float64"] = {"ms_per_step": round(ms64, 4), "GB/s": round(n * 8 / ms64 / 1e6, 3),
+                           "elements_per_s": round(n / ms64 * 1e3, 1),
+                           "int_frac": _int_roofline(math.prod(v.local_shape) / ms64 * 1e3, gpu)["frac"]}
+        line["gpu_launches"] = a.steps  # (the float64 steps are a separate timed region)
     elif a.workload == "embed":
         shape = (50257, 4096)
         dp = 2 if ws % 2 == 0 else 1
