@@ -148,7 +148,7 @@ int32_t sdr_normal_tables_loaded(int32_t device);
 int32_t sdr_normal_mirror_info(int32_t device, uint64_t* device_bytes, uint64_t* exceptions,
                                int32_t* compact, double* build_ms);
 /* float64 Normal outputs read NumPy's r[k] / c[k] as the fast functions plus
- * a 16-bit correction per table point (2 x 32 MiB, built and checked on all
+ * a correction per table point (8-bit for r, 16-bit for c: 48 MiB; built and checked on all
  * 2^24 points by sdr_normal_tables_load; SDR_NORMAL_F64_DELTA=0 leaves them
  * out and float64 normals take the mirror per element).  Reports their bytes
  * on `device` (0 when off), the points that escape to the mirror, and the

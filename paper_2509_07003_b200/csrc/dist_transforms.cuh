@@ -83,6 +83,19 @@ struct ExactMirror {
   int32_t nx_l, nx_c;
 };
 
+// Per-point float64 corrections of r (normal_chunk_f64): 8 bits against
+// r_unit's two Newton steps (SDR_F64_R8), else 16 bits against one.
+#ifndef SDR_F64_R8
+#define SDR_F64_R8 1
+#endif
+#if SDR_F64_R8
+using DeltaR = int8_t;
+#else
+using DeltaR = int16_t;
+#endif
+constexpr int kDeltaEscR = SDR_F64_R8 ? -128 : -32768;
+constexpr int kDeltaMaxR = SDR_F64_R8 ? 127 : 32767;
+
 struct NormalMirror {
   const double* rtab;   // full NumPy r[k] table, only when the compact mirror failed verification
   const double* ctab;   // full NumPy c[k] table (same)
@@ -98,7 +111,7 @@ struct NormalMirror {
   float mean32, std32, b32_r, b32_c;  // B32 = r*b32_r + b32_c
   float bm_r, bm_c, bm_i;             // r32_mufu path: B = r bm_r + h bm_i + bm_c
   float bmc_r, bmc_i;                 // the same with the MUFU cosine (SDR_BF16_COS_MUFU)
-  const int16_t* dr;                  // float64 outputs: per-point corrections (normal_chunk_f64), or null
+  const DeltaR* dr;                   // float64 outputs: per-point corrections (normal_chunk_f64), or null
   const int16_t* dc;
   unsigned long long* fallbacks;
 };
@@ -261,6 +274,7 @@ __device__ __forceinline__ const T& lut_at(const T* base, uint32_t byte_off) {
 // std * r(k), r(k) = sqrt(-2*log1p(-k*2^-24)), k = w0 >> 8, as described at
 // NormalLut; nh = -0.5*std, th = 1.5*std fold std into the Newton step.  No
 // select for k = 0: the 2^-1000 in logt[0] keeps X > 0 and r ~ 2^-499.5.
+template <bool NEWTON2 = (SDR_R_NEWTON2 != 0)>
 __device__ __forceinline__ double r_fast(uint32_t w0, const NormalLut* L, double nh, double th) {
   const double* C = c_npoly;
   const double nd = hilo(0x43300000u, (w0 >> 8) ^ 0xFFFFFFu) - kTwo52m1;  // n, exact
@@ -281,9 +295,7 @@ __device__ __forceinline__ double r_fast(uint32_t w0, const NormalLut* L, double
 #else
   double h = rsqrt_seed(X);
 #endif
-#if SDR_R_NEWTON2
-  h = h * fma(X * h, h * -0.5, 1.5);                                     // seed to ~2^-40
-#endif
+  if constexpr (NEWTON2) h = h * fma(X * h, h * -0.5, 1.5);              // seed to ~2^-45
   const double gx = X * h;
   return gx * fma(gx * h, nh, th);                                       // std * sqrt(X)
 }
@@ -582,15 +594,19 @@ __device__ __noinline__ typename St<DT>::T normal_exact(const DistP& P, uint32_t
 }
 
 // float64 outputs: NumPy's r[k] and c[k] bit for bit as the fast functions
-// (r_fast with std = 1, c_fast) plus a 16-bit signed correction of their bit
-// patterns per table point, dr[k] = bits(r_np[k]) - bits(r_fast(k)) (64 MiB
-// per device for both functions).  Built and checked against the verified
+// (r_unit, c_fast) plus a signed correction of their bit patterns per table
+// point, dr[k] = bits(r_np[k]) - bits(r_unit(k)) (8 bits, SDR_F64_R8) and
+// dc[k] likewise (16 bits): 48 MiB per device.  Built and checked against the verified
 // mirror on all 2^24 points at load (k_normal_deltas); kDeltaEsc marks the
 // points whose difference does not fit (k = 0 for r, the cosine next to its
 // zeros), which take the mirror.  Replaces two libm calls, a square root and
 // two code lookups per element by ~25 float64 operations and two 2-byte loads
 // that hit L2.
 constexpr int kDeltaEsc = -32768;
+// r with std = 1 as the corrections are taken against
+__device__ __forceinline__ double r_unit(uint32_t w0, const NormalLut* L) {
+  return r_fast<SDR_F64_R8 != 0>(w0, L, -0.5, 1.5);
+}
 __device__ __forceinline__ double apply_delta(double a, int d) {
   return __longlong_as_double(__double_as_longlong(a) + d);
 }
@@ -608,6 +624,16 @@ __device__ __forceinline__ int ld_delta(const int16_t* p, uint64_t pol) {
 #if SDR_DELTA_EVICT_LAST
   short v;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.b16 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+  return v;
+#else
+  (void)pol;
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ int ld_delta(const int8_t* p, uint64_t pol) {
+#if SDR_DELTA_EVICT_LAST
+  int v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s8 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return v;
 #else
   (void)pol;
@@ -641,8 +667,8 @@ __device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, const
   if constexpr (DT == SDR_F64) {
     if (P.nm.dr != nullptr) {
       const int dr = __ldg(P.nm.dr + (w0 >> 8)), dc = __ldg(P.nm.dc + (w1 >> 8));
-      if (dr != kDeltaEsc && dc != kDeltaEsc)
-        return normal_f64_of(P, apply_delta(r_fast(w0, L, -0.5, 1.5), dr), apply_delta(c_fast(w1, L), dc));
+      if (dr != kDeltaEscR && dc != kDeltaEsc)
+        return normal_f64_of(P, apply_delta(r_unit(w0, L), dr), apply_delta(c_fast(w1, L), dc));
     }
   } else {
     bool ok;
@@ -673,19 +699,19 @@ __device__ __forceinline__ void normal_chunk_f64(const DistP& P, const NormalLut
   }
   double r[NE], c[NE];
 #pragma unroll
-  for (int e = 0; e < NE; ++e) r[e] = r_fast(w0[e], L, -0.5, 1.5);
+  for (int e = 0; e < NE; ++e) r[e] = r_unit(w0[e], L);
 #pragma unroll
   for (int e = 0; e < NE; ++e) c[e] = c_fast(w1[e], L);
-  int lo = 0;
+  bool esc = false;
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
-    lo = min(lo, min(dr[e], dc[e]));
+    esc |= (dr[e] == kDeltaEscR) | (dc[e] == kDeltaEsc);
     out[e] = normal_f64_of(P, apply_delta(r[e], dr[e]), apply_delta(c[e], dc[e]));
   }
-  if (__builtin_expect(lo == kDeltaEsc, 0)) {
+  if (__builtin_expect(esc, 0)) {
 #pragma unroll
     for (int e = 0; e < NE; ++e)
-      if (dr[e] == kDeltaEsc || dc[e] == kDeltaEsc) out[e] = normal_exact<SDR_F64>(P, w0[e], w1[e]);
+      if (dr[e] == kDeltaEscR || dc[e] == kDeltaEsc) out[e] = normal_exact<SDR_F64>(P, w0[e], w1[e]);
   }
 }
 

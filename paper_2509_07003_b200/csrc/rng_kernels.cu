@@ -657,7 +657,7 @@ __global__ void k_mirror_verify(const ExactMirror M, const double* __restrict__ 
 // in 16 bits.  stats[0..1]: escapes of r / c, stats[2..3]: max |difference|
 // stored.
 __global__ void k_normal_deltas(const ExactMirror M, const double* __restrict__ rtab,
-                                const double* __restrict__ ctab, const NormalLut* lut, int16_t* dr,
+                                const double* __restrict__ ctab, const NormalLut* lut, DeltaR* dr,
                                 int16_t* dc, unsigned long long* stats) {
   __shared__ __align__(16) NormalLut s_lut;
   stage_lut(&s_lut, lut);  // as the fill kernels read it
@@ -665,10 +665,10 @@ __global__ void k_normal_deltas(const ExactMirror M, const double* __restrict__ 
   if (k >= (1u << 24)) return;
   const double rn = rtab != nullptr ? rtab[k] : mirror_r(M, k);
   const double cn = ctab != nullptr ? ctab[k] : mirror_c(M, k);
-  const long long a = __double_as_longlong(rn) - __double_as_longlong(r_fast(k << 8, &s_lut, -0.5, 1.5));
+  const long long a = __double_as_longlong(rn) - __double_as_longlong(r_unit(k << 8, &s_lut));
   const long long b = __double_as_longlong(cn) - __double_as_longlong(c_fast(k << 8, &s_lut));
-  const bool fa = a > kDeltaEsc && a < 32768, fb = b > kDeltaEsc && b < 32768;
-  dr[k] = static_cast<int16_t>(fa ? a : kDeltaEsc);
+  const bool fa = a > kDeltaEscR && a <= kDeltaMaxR, fb = b > kDeltaEsc && b < 32768;
+  dr[k] = static_cast<DeltaR>(fa ? a : kDeltaEscR);
   dc[k] = static_cast<int16_t>(fb ? b : kDeltaEsc);
   const unsigned ea = __popc(__ballot_sync(0xffffffffu, !fa)), eb = __popc(__ballot_sync(0xffffffffu, !fb));
   unsigned long long ma = fa ? static_cast<unsigned long long>(a < 0 ? -a : a) : 0ull;
@@ -785,6 +785,7 @@ int canonicalize(const sdr_view& v, CanonView& cv) {
 }
 
 // Per-device Normal mirror tables.
+constexpr size_t kDeltaBytes = (sizeof(int16_t) + sizeof(DeltaR)) << 24;  // dc then dr
 struct NormalState {
   double* rtab = nullptr;  // full tables: only if the compact mirror failed verification
   double* ctab = nullptr;
@@ -800,7 +801,7 @@ struct NormalState {
   unsigned long long* fallbacks = nullptr;
   double err_r = 0, err_c = 0, err_r32 = 0, err_c32 = 0, err_r2 = 0, err_c2 = 0;
   double err_rm = 0, err_im = 0, err_cm = 0;  // r32_mufu, c32_mufu (bfloat16 path)
-  int16_t* delta = nullptr;            // float64 corrections dr[2^24] then dc[2^24], or null
+  int16_t* delta = nullptr;            // float64 corrections dc[2^24] then dr[2^24] (DeltaR), or null
   unsigned long long delta_stats[4] = {0, 0, 0, 0};  // escapes r / c, max |difference| r / c
   bool loaded = false;
 };
@@ -936,8 +937,8 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
       P.nm.lut = g_nm[device].lut;
       P.nm.lut32 = g_nm[device].lut32;
       P.nm.lut2 = g_nm[device].lut2;
-      P.nm.dr = g_nm[device].delta;
-      P.nm.dc = g_nm[device].delta ? g_nm[device].delta + (1u << 24) : nullptr;
+      P.nm.dc = g_nm[device].delta;  // dc[2^24] (int16), then dr[2^24] (DeltaR)
+      P.nm.dr = g_nm[device].delta ? reinterpret_cast<const DeltaR*>(g_nm[device].delta + (1u << 24)) : nullptr;
       {
         // float64 fast path (see normal_certified): with Er, Ec the calibrated
         // errors of r_fast / c_fast and u = 2^-53,
@@ -997,7 +998,8 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
         if (const char* path = getenv("SDR_NORMAL_PATH")) {
           if (strcmp(path, "exact") == 0) {
             P.nm.kr = P.nm.kr2 = P.nm.b32_r = P.nm.bm_r = P.nm.bmc_r = INFINITY;
-            P.nm.dr = P.nm.dc = nullptr;
+            P.nm.dr = nullptr;
+            P.nm.dc = nullptr;
           }
           if (strcmp(path, "f64") == 0) P.nm.b32_r = P.nm.bm_r = P.nm.bmc_r = INFINITY;
         }
@@ -1335,13 +1337,14 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
   const char* dflag = getenv("SDR_NORMAL_F64_DELTA");
   if (e == cudaSuccess && !(dflag != nullptr && strcmp(dflag, "0") == 0)) {
     unsigned long long* st = nullptr;
-    e = cudaMalloc(&S.delta, sizeof(int16_t) << 25);
+    e = cudaMalloc(&S.delta, kDeltaBytes);
     if (e == cudaSuccess) e = cudaMalloc(&st, 4 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemset(st, 0, 4 * sizeof(unsigned long long));
     if (e == cudaSuccess) {
       ExactMirror M{S.code, S.code ? S.code + (1u << 20) : nullptr, S.xk, S.xv,
                     S.xk ? S.xk + S.nx_l : nullptr, S.xv ? S.xv + S.nx_l : nullptr, S.nx_l, S.nx_c};
-      k_normal_deltas<<<(1u << 24) / 256, 256>>>(M, S.rtab, S.ctab, S.lut, S.delta, S.delta + (1u << 24), st);
+      k_normal_deltas<<<(1u << 24) / 256, 256>>>(M, S.rtab, S.ctab, S.lut,
+                                                  reinterpret_cast<DeltaR*>(S.delta + (1u << 24)), S.delta, st);
       e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaMemcpy(S.delta_stats, st, sizeof(S.delta_stats), cudaMemcpyDeviceToHost);
@@ -1417,7 +1420,7 @@ int normal_delta_info(int device, uint64_t* device_bytes, uint64_t* escapes_r, u
   if (device < 0 || device >= 64 || !g_nm[device].loaded) return SDR_E_NOTABLES;
   const NormalState& S = g_nm[device];
   const bool on = S.delta != nullptr;
-  if (device_bytes) *device_bytes = on ? sizeof(int16_t) << 25 : 0;
+  if (device_bytes) *device_bytes = on ? kDeltaBytes : 0;
   if (escapes_r) *escapes_r = on ? S.delta_stats[0] : 0;
   if (escapes_c) *escapes_c = on ? S.delta_stats[1] : 0;
   if (max_abs_r) *max_abs_r = on ? S.delta_stats[2] : 0;

@@ -362,11 +362,12 @@ def test_float64_normal_corrections_exhaustive():
     16-bit correction per table point (normal_chunk_f64).  Every one of the
     2^24 points of both functions goes through sdr_transform and must equal
     the oracle's float64 Box-Muller bit for bit; the corrections are resident
-    (2 x 32 MiB) and only a few points escape to the mirror."""
+    (48 MiB: 8-bit for r, 16-bit for c) and only a few points escape to the
+    mirror."""
     R.ensure_normal_tables()
     info = R.normal_delta_info()
     print(info)
-    assert info["device_bytes"] == 64 << 20, info
+    assert info["device_bytes"] in (48 << 20, 64 << 20), info  # 8- or 16-bit r corrections (SDR_F64_R8)
     assert 1 <= info["escapes_r"] <= 16 and info["escapes_c"] <= 1 << 14, info  # k = 0; cosine near its zeros
     n = 1 << 24
     rs = np.random.default_rng(20240917)
