@@ -147,12 +147,14 @@ int32_t sdr_normal_tables_loaded(int32_t device);
  * is in use (0: full tables), and the build time of the last load. */
 int32_t sdr_normal_mirror_info(int32_t device, uint64_t* device_bytes, uint64_t* exceptions,
                                int32_t* compact, double* build_ms);
-/* float64 Normal outputs read NumPy's r[k] / c[k] as the fast functions plus
- * a correction per table point (8-bit for r, 16-bit for c: 48 MiB; built and checked on all
- * 2^24 points by sdr_normal_tables_load; SDR_NORMAL_F64_DELTA=0 leaves them
- * out and float64 normals take the mirror per element).  Reports their bytes
- * on `device` (0 when off), the points that escape to the mirror, and the
- * largest stored correction (in units of the last place) of each function.
+/* float64 Normal outputs read NumPy's r[k] as a fast function plus an 8-bit
+ * correction per table point and c[k] from a double-double cosine that is
+ * correctly rounded outside a flagged band (flagged points read an 8-bit
+ * correction): 32 MiB, built and checked on all 2^24 points by
+ * sdr_normal_tables_load (SDR_NORMAL_F64_DELTA=0 leaves them out and float64
+ * normals take the mirror per element).  Reports their bytes on `device`
+ * (0 when off), the points that escape to the mirror, and the largest stored
+ * correction (in units of the last place) of each function.
  * No reference counterpart: rng.py:150-156 evaluates log1p / cos per element. */
 int32_t sdr_normal_delta_info(int32_t device, uint64_t* device_bytes, uint64_t* escapes_r,
                               uint64_t* escapes_c, uint64_t* max_abs_r, uint64_t* max_abs_c);

@@ -96,6 +96,18 @@ using DeltaR = int16_t;
 constexpr int kDeltaEscR = SDR_F64_R8 ? -128 : -32768;
 constexpr int kDeltaMaxR = SDR_F64_R8 ? 127 : 32767;
 
+// float64 outputs, cosine: c_cr evaluates cos(RN(2pi u2)) -- NumPy's own
+// argument -- in double-double from a (cos, sin)(i pi/1024) table stored as
+// double-doubles (absolute error < 2^-76).  Rounded to nearest it equals
+// NumPy's (glibc's) value except within a narrow band around rounding
+// midpoints (glibc misses there) and where |c| < 2^-10 (the table's precision
+// runs out); those elements are flagged and read a correction instead.  The
+// load verifies on all 2^24 points that every unflagged one matches.
+struct __align__(16) CosDD {
+  double ch, cl, sh, sl;
+};
+constexpr int kCosDD = 2049;
+
 struct NormalMirror {
   const double* rtab;   // full NumPy r[k] table, only when the compact mirror failed verification
   const double* ctab;   // full NumPy c[k] table (same)
@@ -112,7 +124,12 @@ struct NormalMirror {
   float bm_r, bm_c, bm_i;             // r32_mufu path: B = r bm_r + h bm_i + bm_c
   float bmc_r, bmc_i;                 // the same with the MUFU cosine (SDR_BF16_COS_MUFU)
   const DeltaR* dr;                   // float64 outputs: per-point corrections (normal_chunk_f64), or null
-  const int16_t* dc;
+  const int16_t* dc;                  // against c_fast (cmode 0)
+  const int8_t* dc8;                  // against c_cr, flagged points only (cmode 1)
+  const CosDD* cdd;                   // c_cr's table
+  double q1, q2, q3;                  // pi/1024 = q1 + q2 + q3 (40 + 40 + 53 bits)
+  double ctau;                        // flag band around midpoints, in ulps
+  int32_t cmode;                      // 1: c_cr verified at load; 0: c_fast + 16-bit corrections
   unsigned long long* fallbacks;
 };
 
@@ -640,6 +657,45 @@ __device__ __forceinline__ int ld_delta(const int8_t* p, uint64_t pol) {
   return __ldg(p);
 #endif
 }
+// NumPy's cosine argument (rng.py:155) and cos of it in double-double; the
+// result is RN(c) and `flag` marks the elements c_cr cannot vouch for.  T is
+// M.cdd or its copy in shared memory.
+__device__ __forceinline__ double c_cr(uint32_t w1, const CosDD* T, const NormalMirror& M, bool& flag) {
+  const uint32_t k = w1 >> 8;
+  const double u = hilo(0x43300000u - (24u << 20), k) - 0x1p28;            // k 2^-24, exact
+  const double arg = __dmul_rn(6.283185307179586, u);                     // (2.0 * pi) * u2
+  const uint32_t i = (k + 4096u) >> 13;                                    // nearest i pi/1024
+  const double fi = hilo(0x43300000u, i) - 0x1p52;
+  const double d1 = fma(-fi, M.q1, arg);                                   // exact
+  const double p2 = fi * M.q2;                                             // exact
+  const double dh = d1 - p2;                                               // TwoSum
+  const double bb = dh - d1;
+  const double dl = fma(-fi, M.q3, (d1 - (dh - bb)) + (-p2 - bb));         // d = dh + dl
+  const CosDD t = T[i];
+  const double ph = dh * dh;
+  const double pl = fma(dh, dh, -ph) + 2.0 * dh * dl;                      // d^2 = ph + pl
+  const double cmh = -0.5 * ph;                                            // cos d - 1 = cmh + cml
+  const double cml = fma(-0.5, pl, ph * ph * fma(ph, -1.0 / 720.0, 1.0 / 24.0));
+  const double sdl = fma(dh * ph, fma(ph, 1.0 / 120.0, -1.0 / 6.0), dl);   // sin d = dh + sdl
+  // c = C (1 + cm) - S sin d
+  const double t1 = t.sh * dh, e1 = fma(t.sh, dh, -t1);
+  const double t2 = t.ch * cmh, e2 = fma(t.ch, cmh, -t2);
+  const double s1 = t.ch - t1, b1 = s1 - t.ch, r1 = (t.ch - (s1 - b1)) + (-t1 - b1);
+  const double s2 = s1 + t2, b2 = s2 - s1, r2 = (s1 - (s2 - b2)) + (t2 - b2);
+  double lo = (r1 + r2) + ((e2 - e1) + t.cl);
+  lo = fma(-t.sh, sdl, lo);
+  lo = fma(-t.sl, dh, lo);
+  lo = fma(t.ch, cml, lo);
+  lo = fma(t.cl, cmh, lo);
+  const double c = s2 + lo;
+  const double rem = lo - (c - s2);                                        // exact: c + rem
+  const uint32_t hw = dhi(c), ex = hw & 0x7FF00000u;
+  const double ulp = hilo(ex - (52u << 20), 0u);
+  flag = ex < ((1023u - 10u) << 20) || (dlo(c) == 0u && (hw & 0xFFFFFu) == 0u) ||
+         fabs(fabs(rem) - 0.5 * ulp) < M.ctau * ulp;
+  return c;
+}
+
 __device__ __forceinline__ double normal_f64_of(const DistP& P, double r, double c) {
   return __dadd_rn(P.mean, __dmul_rn(P.stdv, __dmul_rn(r, c)));  // rng.py:156, as normal_exact
 }
@@ -666,9 +722,18 @@ __device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, const
                                                            uint32_t w0, uint32_t w1) {
   if constexpr (DT == SDR_F64) {
     if (P.nm.dr != nullptr) {
-      const int dr = __ldg(P.nm.dr + (w0 >> 8)), dc = __ldg(P.nm.dc + (w1 >> 8));
-      if (dr != kDeltaEscR && dc != kDeltaEsc)
-        return normal_f64_of(P, apply_delta(r_unit(w0, L), dr), apply_delta(c_fast(w1, L), dc));
+      const int dr = __ldg(P.nm.dr + (w0 >> 8));
+      if (P.nm.cmode == 1) {
+        bool flag;
+        double c = c_cr(w1, P.nm.cdd, P.nm, flag);
+        int dc = 0;
+        if (flag) dc = __ldg(P.nm.dc8 + (w1 >> 8));
+        if (dr != kDeltaEscR && dc != -128) return normal_f64_of(P, apply_delta(r_unit(w0, L), dr), apply_delta(c, dc));
+      } else {
+        const int dc = __ldg(P.nm.dc + (w1 >> 8));
+        if (dr != kDeltaEscR && dc != kDeltaEsc)
+          return normal_f64_of(P, apply_delta(r_unit(w0, L), dr), apply_delta(c_fast(w1, L), dc));
+      }
     }
   } else {
     bool ok;
@@ -692,26 +757,42 @@ __device__ __forceinline__ void normal_chunk_f64(const DistP& P, const NormalLut
   }
   int dr[NE], dc[NE];
   const uint64_t pol = delta_policy();
-#pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    dr[e] = ld_delta(P.nm.dr + (w0[e] >> 8), pol);
-    dc[e] = ld_delta(P.nm.dc + (w1[e] >> 8), pol);
-  }
   double r[NE], c[NE];
-#pragma unroll
-  for (int e = 0; e < NE; ++e) r[e] = r_unit(w0[e], L);
-#pragma unroll
-  for (int e = 0; e < NE; ++e) c[e] = c_fast(w1[e], L);
   bool esc = false;
+  if (P.nm.cmode == 1) {
+    // the cosine from c_cr: only its flagged elements (a few percent) read a correction
 #pragma unroll
-  for (int e = 0; e < NE; ++e) {
-    esc |= (dr[e] == kDeltaEscR) | (dc[e] == kDeltaEsc);
-    out[e] = normal_f64_of(P, apply_delta(r[e], dr[e]), apply_delta(c[e], dc[e]));
+    for (int e = 0; e < NE; ++e) dr[e] = ld_delta(P.nm.dr + (w0[e] >> 8), pol);
+    bool flag[NE];
+    const CosDD* T = P.nm.cdd;  // 64 KiB, through L1 (prefer_l1)
+#pragma unroll
+    for (int e = 0; e < NE; ++e) c[e] = c_cr(w1[e], T, P.nm, flag[e]);
+#pragma unroll
+    for (int e = 0; e < NE; ++e) dc[e] = flag[e] ? ld_delta(P.nm.dc8 + (w1[e] >> 8), pol) : 0;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) r[e] = r_unit(w0[e], L);
+#pragma unroll
+    for (int e = 0; e < NE; ++e) esc |= (dr[e] == kDeltaEscR) | (dc[e] == -128);
+  } else {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      dr[e] = ld_delta(P.nm.dr + (w0[e] >> 8), pol);
+      dc[e] = ld_delta(P.nm.dc + (w1[e] >> 8), pol);
+    }
+#pragma unroll
+    for (int e = 0; e < NE; ++e) r[e] = r_unit(w0[e], L);
+#pragma unroll
+    for (int e = 0; e < NE; ++e) c[e] = c_fast(w1[e], L);
+#pragma unroll
+    for (int e = 0; e < NE; ++e) esc |= (dr[e] == kDeltaEscR) | (dc[e] == kDeltaEsc);
   }
+#pragma unroll
+  for (int e = 0; e < NE; ++e) out[e] = normal_f64_of(P, apply_delta(r[e], dr[e]), apply_delta(c[e], dc[e]));
   if (__builtin_expect(esc, 0)) {
 #pragma unroll
     for (int e = 0; e < NE; ++e)
-      if (dr[e] == kDeltaEscR || dc[e] == kDeltaEsc) out[e] = normal_exact<SDR_F64>(P, w0[e], w1[e]);
+      if (dr[e] == kDeltaEscR || dc[e] == (P.nm.cmode == 1 ? -128 : kDeltaEsc))
+        out[e] = normal_exact<SDR_F64>(P, w0[e], w1[e]);
   }
 }
 

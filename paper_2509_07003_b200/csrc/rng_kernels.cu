@@ -21,6 +21,7 @@
 // error is measured exhaustively at load, a rigorous bound, and the exact
 // NumPy tables for the few elements the bound cannot certify.
 // The SDR_* macros below are A/B knobs; their defaults are the measured best.
+#include <quadmath.h>
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -667,12 +668,12 @@ __global__ void k_normal_deltas(const ExactMirror M, const double* __restrict__ 
   const double cn = ctab != nullptr ? ctab[k] : mirror_c(M, k);
   const long long a = __double_as_longlong(rn) - __double_as_longlong(r_unit(k << 8, &s_lut));
   const long long b = __double_as_longlong(cn) - __double_as_longlong(c_fast(k << 8, &s_lut));
-  const bool fa = a > kDeltaEscR && a <= kDeltaMaxR, fb = b > kDeltaEsc && b < 32768;
+  const bool fa = a > kDeltaEscR && a <= kDeltaMaxR, fb = dc == nullptr || (b > kDeltaEsc && b < 32768);
   dr[k] = static_cast<DeltaR>(fa ? a : kDeltaEscR);
-  dc[k] = static_cast<int16_t>(fb ? b : kDeltaEsc);
+  if (dc != nullptr) dc[k] = static_cast<int16_t>(fb ? b : kDeltaEsc);
   const unsigned ea = __popc(__ballot_sync(0xffffffffu, !fa)), eb = __popc(__ballot_sync(0xffffffffu, !fb));
   unsigned long long ma = fa ? static_cast<unsigned long long>(a < 0 ? -a : a) : 0ull;
-  unsigned long long mb = fb ? static_cast<unsigned long long>(b < 0 ? -b : b) : 0ull;
+  unsigned long long mb = fb && dc != nullptr ? static_cast<unsigned long long>(b < 0 ? -b : b) : 0ull;
   for (int o = 16; o > 0; o >>= 1) {
     ma = max(ma, __shfl_xor_sync(0xffffffffu, ma, o));
     mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
@@ -682,6 +683,33 @@ __global__ void k_normal_deltas(const ExactMirror M, const double* __restrict__ 
     if (eb) atomicAdd(stats + 1, static_cast<unsigned long long>(eb));
     atomicMax(stats + 2, ma);
     atomicMax(stats + 3, mb);
+  }
+}
+
+// c_cr against NumPy's c[k] on every table point: dc8[k] = bits(c_np) -
+// bits(c_cr) for the flagged points (-128 when it does not fit), 0 elsewhere.
+// stats: [0] flagged, [1] escapes, [2] unflagged mismatches (must be 0 for
+// c_cr to be used), [3] max |difference| stored.
+__global__ void k_normal_cos_cr(const ExactMirror M, const double* __restrict__ ctab, const NormalMirror NM,
+                                int8_t* dc8, unsigned long long* stats) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (1u << 24)) return;
+  const double cn = ctab != nullptr ? ctab[k] : mirror_c(M, k);
+  bool flag;
+  const double c = c_cr(k << 8, NM.cdd, NM, flag);
+  const long long d = __double_as_longlong(cn) - __double_as_longlong(c);
+  const bool fits = d > -128 && d < 128;
+  dc8[k] = static_cast<int8_t>(flag ? (fits ? d : -128) : 0);
+  const unsigned nf = __popc(__ballot_sync(0xffffffffu, flag));
+  const unsigned ne = __popc(__ballot_sync(0xffffffffu, flag && !fits));
+  const unsigned nb = __popc(__ballot_sync(0xffffffffu, !flag && d != 0));
+  unsigned long long m = flag && fits ? static_cast<unsigned long long>(d < 0 ? -d : d) : 0ull;
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) {
+    if (nf) atomicAdd(stats, static_cast<unsigned long long>(nf));
+    if (ne) atomicAdd(stats + 1, static_cast<unsigned long long>(ne));
+    if (nb) atomicAdd(stats + 2, static_cast<unsigned long long>(nb));
+    atomicMax(stats + 3, m);
   }
 }
 
@@ -785,7 +813,8 @@ int canonicalize(const sdr_view& v, CanonView& cv) {
 }
 
 // Per-device Normal mirror tables.
-constexpr size_t kDeltaBytes = (sizeof(int16_t) + sizeof(DeltaR)) << 24;  // dc then dr
+constexpr size_t kDeltaBytes = (sizeof(int16_t) + sizeof(DeltaR)) << 24;  // cmode 0: dc then dr
+constexpr size_t kDeltaBytesCr = (sizeof(int8_t) + sizeof(DeltaR)) << 24;  // cmode 1: dr then dc8
 struct NormalState {
   double* rtab = nullptr;  // full tables: only if the compact mirror failed verification
   double* ctab = nullptr;
@@ -801,8 +830,13 @@ struct NormalState {
   unsigned long long* fallbacks = nullptr;
   double err_r = 0, err_c = 0, err_r32 = 0, err_c32 = 0, err_r2 = 0, err_c2 = 0;
   double err_rm = 0, err_im = 0, err_cm = 0;  // r32_mufu, c32_mufu (bfloat16 path)
-  int16_t* delta = nullptr;            // float64 corrections dc[2^24] then dr[2^24] (DeltaR), or null
+  unsigned char* delta = nullptr;      // float64 corrections (layout by cmode, kDeltaBytes / kDeltaBytesCr), or null
   unsigned long long delta_stats[4] = {0, 0, 0, 0};  // escapes r / c, max |difference| r / c
+  unsigned long long cr_stats[4] = {0, 0, 0, 0};     // c_cr: flagged, escapes, unflagged mismatches, max |d|
+  CosDD* cdd = nullptr;                // c_cr's table (cmode 1)
+  double q[3] = {0, 0, 0};
+  double ctau = 0.03;
+  int cmode = 0;
   bool loaded = false;
 };
 static std::mutex g_nm_mu;
@@ -814,6 +848,29 @@ static double round_sig(long double x, int bits) {
 }
 
 // Host construction of the fast-path tables (long double arithmetic).
+// c_cr's table: (cos, sin)(i pi/1024) for i in [0, 2048] as double-doubles
+// from quad precision, and pi/1024 split as 40 + 40 + 53 bits.
+static double trunc_bits(double x, int keep) {
+  uint64_t b;
+  memcpy(&b, &x, 8);
+  b &= ~((uint64_t{1} << (53 - keep)) - 1);
+  memcpy(&x, &b, 8);
+  return x;
+}
+static void build_cos_dd(CosDD* T, double* q) {
+  const __float128 Q = strtoflt128("3.14159265358979323846264338327950288419716939937510", nullptr) / 1024;
+  for (int i = 0; i < kCosDD; ++i) {
+    const __float128 c = cosq(Q * i), s = sinq(Q * i);
+    T[i].ch = static_cast<double>(c);
+    T[i].cl = static_cast<double>(c - static_cast<__float128>(T[i].ch));
+    T[i].sh = static_cast<double>(s);
+    T[i].sl = static_cast<double>(s - static_cast<__float128>(T[i].sh));
+  }
+  q[0] = trunc_bits(static_cast<double>(Q), 40);
+  q[1] = trunc_bits(static_cast<double>(Q - q[0]), 40);
+  q[2] = static_cast<double>(Q - q[0] - q[1]);
+}
+
 static void build_normal_lut(NormalLut& L) {
   for (int j = 0; j < 512; ++j) {
     long double inv, mult;
@@ -937,8 +994,25 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
       P.nm.lut = g_nm[device].lut;
       P.nm.lut32 = g_nm[device].lut32;
       P.nm.lut2 = g_nm[device].lut2;
-      P.nm.dc = g_nm[device].delta;  // dc[2^24] (int16), then dr[2^24] (DeltaR)
-      P.nm.dr = g_nm[device].delta ? reinterpret_cast<const DeltaR*>(g_nm[device].delta + (1u << 24)) : nullptr;
+      {
+        const NormalState& S = g_nm[device];
+        P.nm.cmode = S.delta != nullptr ? S.cmode : 0;
+        P.nm.dr = nullptr;
+        P.nm.dc = nullptr;
+        P.nm.dc8 = nullptr;
+        if (S.delta != nullptr && S.cmode == 1) {  // dr[2^24], then dc8[2^24]
+          P.nm.dr = reinterpret_cast<const DeltaR*>(S.delta);
+          P.nm.dc8 = reinterpret_cast<const int8_t*>(S.delta + (sizeof(DeltaR) << 24));
+        } else if (S.delta != nullptr) {           // dc[2^24] (int16), then dr[2^24]
+          P.nm.dc = reinterpret_cast<const int16_t*>(S.delta);
+          P.nm.dr = reinterpret_cast<const DeltaR*>(S.delta + (sizeof(int16_t) << 24));
+        }
+        P.nm.cdd = S.cdd;
+        P.nm.q1 = S.q[0];
+        P.nm.q2 = S.q[1];
+        P.nm.q3 = S.q[2];
+        P.nm.ctau = S.ctau;
+      }
       {
         // float64 fast path (see normal_certified): with Er, Ec the calibrated
         // errors of r_fast / c_fast and u = 2^-53,
@@ -1043,6 +1117,16 @@ template <typename K>
 static void allow_dyn_smem(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
 }
+// float64 Normal kernels read c_cr's 64 KiB table through L1: ask for the
+// smallest shared-memory carve-out that holds their two CTAs' static tables.
+#ifndef SDR_F64_CARVEOUT
+#define SDR_F64_CARVEOUT 40
+#endif
+template <int DIST, int DT, typename K>
+static void prefer_l1(K kernel) {
+  if constexpr (DIST == SDR_NORMAL && DT == SDR_F64 && SDR_F64_CARVEOUT > 0)
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, SDR_F64_CARVEOUT);
+}
 
 template <int DIST, int DT>
 static void launch_fill(const FillArgs& A0, bool fast, cudaStream_t s) {
@@ -1051,11 +1135,13 @@ static void launch_fill(const FillArgs& A0, bool fast, cudaStream_t s) {
   constexpr int nt = fill_threads<DIST, DT>();
   if (fast && A.aligned) {
     allow_dyn_smem(k_fill_fast<DIST, DT, true>, dsm);
+    prefer_l1<DIST, DT>(k_fill_fast<DIST, DT, true>);
     const int grid = grid_for(k_fill_fast<DIST, DT, true>, A.nchunks, nt, dsm);
     set_walk(A.walk, A.ix.cv, A.chunks_per_row, static_cast<uint64_t>(grid) * nt, kV);
     launch_pdl(k_fill_fast<DIST, DT, true>, grid, s, A, dsm, nt);
   } else if (fast) {
     allow_dyn_smem(k_fill_fast<DIST, DT, false>, dsm);
+    prefer_l1<DIST, DT>(k_fill_fast<DIST, DT, false>);
     const int grid = grid_for(k_fill_fast<DIST, DT, false>, A.nchunks, nt, dsm);
     set_walk(A.walk, A.ix.cv, A.chunks_per_row, static_cast<uint64_t>(grid) * nt, kV);
     launch_pdl(k_fill_fast<DIST, DT, false>, grid, s, A, dsm, nt);
@@ -1244,6 +1330,9 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
   // a reload replaces the previous mirror
   cudaFree(S.delta);
   S.delta = nullptr;
+  cudaFree(S.cdd);
+  S.cdd = nullptr;
+  S.cmode = 0;
   cudaFree(S.rtab);
   cudaFree(S.ctab);
   cudaFree(S.code);
@@ -1337,21 +1426,64 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
   const char* dflag = getenv("SDR_NORMAL_F64_DELTA");
   if (e == cudaSuccess && !(dflag != nullptr && strcmp(dflag, "0") == 0)) {
     unsigned long long* st = nullptr;
-    e = cudaMalloc(&S.delta, kDeltaBytes);
-    if (e == cudaSuccess) e = cudaMalloc(&st, 4 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMemset(st, 0, 4 * sizeof(unsigned long long));
-    if (e == cudaSuccess) {
-      ExactMirror M{S.code, S.code ? S.code + (1u << 20) : nullptr, S.xk, S.xv,
-                    S.xk ? S.xk + S.nx_l : nullptr, S.xv ? S.xv + S.nx_l : nullptr, S.nx_l, S.nx_c};
-      k_normal_deltas<<<(1u << 24) / 256, 256>>>(M, S.rtab, S.ctab, S.lut,
-                                                  reinterpret_cast<DeltaR*>(S.delta + (1u << 24)), S.delta, st);
-      e = cudaGetLastError();
+    ExactMirror M{S.code, S.code ? S.code + (1u << 20) : nullptr, S.xk, S.xv,
+                  S.xk ? S.xk + S.nx_l : nullptr, S.xv ? S.xv + S.nx_l : nullptr, S.nx_l, S.nx_c};
+    e = cudaMalloc(&st, 8 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(st, 0, 8 * sizeof(unsigned long long));
+    // cosine: c_cr where it verifies on every point (cmode 1), else 16-bit corrections of c_fast
+    const char* cflag = getenv("SDR_NORMAL_COS_CR");
+    if (const char* tau = getenv("SDR_NORMAL_COS_TAU")) S.ctau = atof(tau);
+    bool cr = e == cudaSuccess && !(cflag != nullptr && strcmp(cflag, "0") == 0);
+    if (cr) {
+      std::vector<CosDD> h(kCosDD);
+      build_cos_dd(h.data(), S.q);
+      e = cudaMalloc(&S.delta, kDeltaBytesCr);
+      if (e == cudaSuccess) e = cudaMalloc(&S.cdd, kCosDD * sizeof(CosDD));
+      if (e == cudaSuccess) e = cudaMemcpy(S.cdd, h.data(), kCosDD * sizeof(CosDD), cudaMemcpyHostToDevice);
+      if (e == cudaSuccess) {
+        NormalMirror NM;
+        memset(static_cast<void*>(&NM), 0, sizeof(NM));
+        NM.cdd = S.cdd;
+        NM.q1 = S.q[0];
+        NM.q2 = S.q[1];
+        NM.q3 = S.q[2];
+        NM.ctau = S.ctau;
+        k_normal_cos_cr<<<(1u << 24) / 256, 256>>>(M, S.ctab, NM, reinterpret_cast<int8_t*>(S.delta + (sizeof(DeltaR) << 24)),
+                                                    st + 4);
+        k_normal_deltas<<<(1u << 24) / 256, 256>>>(M, S.rtab, S.ctab, S.lut, reinterpret_cast<DeltaR*>(S.delta),
+                                                    nullptr, st);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) e = cudaMemcpy(S.cr_stats, st + 4, sizeof(S.cr_stats), cudaMemcpyDeviceToHost);
+      cr = e == cudaSuccess && S.cr_stats[2] == 0;
+      if (cr) {
+        S.cmode = 1;
+      } else {
+        cudaFree(S.delta);
+        cudaFree(S.cdd);
+        S.delta = nullptr;
+        S.cdd = nullptr;
+        if (e == cudaSuccess) e = cudaMemset(st, 0, 8 * sizeof(unsigned long long));
+      }
+    }
+    if (!cr && e == cudaSuccess) {
+      S.cmode = 0;
+      e = cudaMalloc(&S.delta, kDeltaBytes);
+      if (e == cudaSuccess) {
+        k_normal_deltas<<<(1u << 24) / 256, 256>>>(M, S.rtab, S.ctab, S.lut,
+                                                    reinterpret_cast<DeltaR*>(S.delta + (sizeof(int16_t) << 24)),
+                                                    reinterpret_cast<int16_t*>(S.delta), st);
+        e = cudaGetLastError();
+      }
     }
     if (e == cudaSuccess) e = cudaMemcpy(S.delta_stats, st, sizeof(S.delta_stats), cudaMemcpyDeviceToHost);
     cudaFree(st);
     if (e != cudaSuccess) {
       cudaFree(S.delta);
+      cudaFree(S.cdd);
       S.delta = nullptr;
+      S.cdd = nullptr;
+      S.cmode = 0;
     }
   }
   // fallbacks[1..6] = max err of r, c (NormalLut), r32, c32 (float32 path), r2, c2 (NormalLut2);
@@ -1394,8 +1526,12 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
             compact ? "compact" : "full tables", S.nx_l, S.nx_c, bad, ms, S.device_bytes / 1048576.0, S.err_r,
             S.err_c, S.err_r32, S.err_c32, S.err_r2, S.err_c2, S.err_rm, S.err_im, S.err_cm);
   if (getenv("SDR_NORMAL_DEBUG"))
-    fprintf(stderr, "sdr normal float64 corrections: %s, escapes r %llu c %llu, max |d| r %llu c %llu\n",
-            S.delta ? "built" : "off", S.delta_stats[0], S.delta_stats[1], S.delta_stats[2], S.delta_stats[3]);
+    fprintf(stderr,
+            "sdr normal float64 corrections: %s, cosine %s (tau %.3f: flagged %llu, escapes %llu, unflagged"
+            " mismatches %llu, max |d| %llu), escapes r %llu c %llu, max |d| r %llu c %llu\n",
+            S.delta ? "built" : "off", S.cmode == 1 ? "c_cr" : "c_fast + 16-bit", S.ctau, S.cr_stats[0],
+            S.cr_stats[1], S.cr_stats[2], S.cr_stats[3], S.delta_stats[0], S.delta_stats[1], S.delta_stats[2],
+            S.delta_stats[3]);
   S.loaded = true;
   if (er) *er = S.err_r;
   if (ec) *ec = S.err_c;
@@ -1420,11 +1556,12 @@ int normal_delta_info(int device, uint64_t* device_bytes, uint64_t* escapes_r, u
   if (device < 0 || device >= 64 || !g_nm[device].loaded) return SDR_E_NOTABLES;
   const NormalState& S = g_nm[device];
   const bool on = S.delta != nullptr;
-  if (device_bytes) *device_bytes = on ? kDeltaBytes : 0;
+  const bool cr = on && S.cmode == 1;
+  if (device_bytes) *device_bytes = on ? (cr ? kDeltaBytesCr + kCosDD * sizeof(CosDD) : kDeltaBytes) : 0;
   if (escapes_r) *escapes_r = on ? S.delta_stats[0] : 0;
-  if (escapes_c) *escapes_c = on ? S.delta_stats[1] : 0;
+  if (escapes_c) *escapes_c = on ? (cr ? S.cr_stats[1] : S.delta_stats[1]) : 0;
   if (max_abs_r) *max_abs_r = on ? S.delta_stats[2] : 0;
-  if (max_abs_c) *max_abs_c = on ? S.delta_stats[3] : 0;
+  if (max_abs_c) *max_abs_c = on ? (cr ? S.cr_stats[3] : S.delta_stats[3]) : 0;
   return SDR_OK;
 }
 
@@ -1477,6 +1614,7 @@ static void launch_batch(const FillArgs* d_descs, const uint64_t* d_prefix, int 
   constexpr size_t dsm = fill_dyn_smem<DIST, DT>();
   constexpr int nt = fill_threads<DIST, DT>();
   allow_dyn_smem(k_fill_batch<DIST, DT>, dsm);
+  prefer_l1<DIST, DT>(k_fill_batch<DIST, DT>);
   // persistent: one wave of resident CTAs (SMs x occupancy) taking tiles from
   // the counter at d_prefix[n]
   const int grid = grid_for(k_fill_batch<DIST, DT>, ntiles * nt, nt, dsm);

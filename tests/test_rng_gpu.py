@@ -362,12 +362,14 @@ def test_float64_normal_corrections_exhaustive():
     16-bit correction per table point (normal_chunk_f64).  Every one of the
     2^24 points of both functions goes through sdr_transform and must equal
     the oracle's float64 Box-Muller bit for bit; the corrections are resident
-    (48 MiB: 8-bit for r, 16-bit for c) and only a few points escape to the
-    mirror."""
+    (32 MiB with the double-double cosine c_cr, 48 MiB without) and only a
+    few points escape to the mirror.  The same with c_cr switched off
+    (SDR_NORMAL_COS_CR=0, a reload) on a sample."""
     R.ensure_normal_tables()
     info = R.normal_delta_info()
     print(info)
-    assert info["device_bytes"] in (48 << 20, 64 << 20), info  # 8- or 16-bit r corrections (SDR_F64_R8)
+    # 8-bit r corrections, plus 8-bit cosine corrections and c_cr's 64 KiB table (or 16-bit ones for c_fast)
+    assert 32 << 20 <= info["device_bytes"] <= 64 << 20, info
     assert 1 <= info["escapes_r"] <= 16 and info["escapes_c"] <= 1 << 14, info  # k = 0; cosine near its zeros
     n = 1 << 24
     rs = np.random.default_rng(20240917)
@@ -382,6 +384,21 @@ def test_float64_normal_corrections_exhaustive():
         g = got.cpu().numpy()
         bad = np.flatnonzero(g.view(np.uint64) != want.view(np.uint64))
         assert bad.size == 0, (mean, std, bad[:8], g[bad[:4]], want[bad[:4]])
+    idx = torch.cuda.current_device()
+    try:
+        os.environ["SDR_NORMAL_COS_CR"] = "0"
+        R._TABLE_ERRORS.pop(idx, None)
+        R.ensure_normal_tables()
+        assert R.normal_delta_info()["device_bytes"] == 48 << 20
+        sl = slice(0, n, 7)
+        w = np.ascontiguousarray(words[:, sl])
+        want = O.transform("normal", (0.5, 3.0), w, np.float64)
+        got = R.Normal(0.5, 3.0).transform(tuple(w), np.float64).cpu().numpy()
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    finally:
+        os.environ.pop("SDR_NORMAL_COS_CR", None)
+        R._TABLE_ERRORS.pop(idx, None)
+        R.ensure_normal_tables()
 
 
 def test_randomized_windows_match_oracle():
