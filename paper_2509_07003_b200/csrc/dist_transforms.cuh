@@ -107,6 +107,11 @@ struct __align__(16) CosDD {
   double ch, cl, sh, sl;
 };
 constexpr int kCosDD = 2049;
+// pi/1024 = kQ1 + kQ2 + kQ3 (40 + 40 + 29 significant bits, from quad precision)
+constexpr double kQ1 = 0x1.921fb54442p-9, kQ2 = 0x1.a308d31318p-50, kQ3 = 0x1.8a2e037p-90;
+#ifndef SDR_COS_TAU
+#define SDR_COS_TAU 0.03  // c_cr's flag band around rounding midpoints, in ulps (glibc misses within 0.016)
+#endif
 
 struct NormalMirror {
   const double* rtab;   // full NumPy r[k] table, only when the compact mirror failed verification
@@ -124,12 +129,9 @@ struct NormalMirror {
   float bm_r, bm_c, bm_i;             // r32_mufu path: B = r bm_r + h bm_i + bm_c
   float bmc_r, bmc_i;                 // the same with the MUFU cosine (SDR_BF16_COS_MUFU)
   const DeltaR* dr;                   // float64 outputs: per-point corrections (normal_chunk_f64), or null
-  const int16_t* dc;                  // against c_fast (cmode 0)
-  const int8_t* dc8;                  // against c_cr, flagged points only (cmode 1)
-  const CosDD* cdd;                   // c_cr's table
-  double q1, q2, q3;                  // pi/1024 = q1 + q2 + q3 (40 + 40 + 53 bits)
-  double ctau;                        // flag band around midpoints, in ulps
-  int32_t cmode;                      // 1: c_cr verified at load; 0: c_fast + 16-bit corrections
+  const int16_t* dc;                  // against c_fast (no c_cr)
+  const CosDD* cdd;                   // c_cr's table when it verified at load (its 8-bit corrections
+                                      // follow dr: dc8()), else null
   unsigned long long* fallbacks;
 };
 
@@ -660,17 +662,17 @@ __device__ __forceinline__ int ld_delta(const int8_t* p, uint64_t pol) {
 // NumPy's cosine argument (rng.py:155) and cos of it in double-double; the
 // result is RN(c) and `flag` marks the elements c_cr cannot vouch for.  T is
 // M.cdd or its copy in shared memory.
-__device__ __forceinline__ double c_cr(uint32_t w1, const CosDD* T, const NormalMirror& M, bool& flag) {
+__device__ __forceinline__ double c_cr(uint32_t w1, const CosDD* T, bool& flag) {
   const uint32_t k = w1 >> 8;
   const double u = hilo(0x43300000u - (24u << 20), k) - 0x1p28;            // k 2^-24, exact
   const double arg = __dmul_rn(6.283185307179586, u);                     // (2.0 * pi) * u2
   const uint32_t i = (k + 4096u) >> 13;                                    // nearest i pi/1024
   const double fi = hilo(0x43300000u, i) - 0x1p52;
-  const double d1 = fma(-fi, M.q1, arg);                                   // exact
-  const double p2 = fi * M.q2;                                             // exact
+  const double d1 = fma(-fi, kQ1, arg);                                   // exact
+  const double p2 = fi * kQ2;                                             // exact
   const double dh = d1 - p2;                                               // TwoSum
   const double bb = dh - d1;
-  const double dl = fma(-fi, M.q3, (d1 - (dh - bb)) + (-p2 - bb));         // d = dh + dl
+  const double dl = fma(-fi, kQ3, (d1 - (dh - bb)) + (-p2 - bb));         // d = dh + dl
   const CosDD t = T[i];
   const double ph = dh * dh;
   const double pl = fma(dh, dh, -ph) + 2.0 * dh * dl;                      // d^2 = ph + pl
@@ -692,8 +694,12 @@ __device__ __forceinline__ double c_cr(uint32_t w1, const CosDD* T, const Normal
   const uint32_t hw = dhi(c), ex = hw & 0x7FF00000u;
   const double ulp = hilo(ex - (52u << 20), 0u);
   flag = ex < ((1023u - 10u) << 20) || (dlo(c) == 0u && (hw & 0xFFFFFu) == 0u) ||
-         fabs(fabs(rem) - 0.5 * ulp) < M.ctau * ulp;
+         fabs(fabs(rem) - 0.5 * ulp) < SDR_COS_TAU * ulp;
   return c;
+}
+
+__device__ __forceinline__ const int8_t* dc8(const NormalMirror& M) {
+  return reinterpret_cast<const int8_t*>(M.dr) + (sizeof(DeltaR) << 24);
 }
 
 __device__ __forceinline__ double normal_f64_of(const DistP& P, double r, double c) {
@@ -723,11 +729,11 @@ __device__ __forceinline__ typename St<DT>::T normal_value(const DistP& P, const
   if constexpr (DT == SDR_F64) {
     if (P.nm.dr != nullptr) {
       const int dr = __ldg(P.nm.dr + (w0 >> 8));
-      if (P.nm.cmode == 1) {
+      if (P.nm.cdd != nullptr) {
         bool flag;
-        double c = c_cr(w1, P.nm.cdd, P.nm, flag);
+        double c = c_cr(w1, P.nm.cdd, flag);
         int dc = 0;
-        if (flag) dc = __ldg(P.nm.dc8 + (w1 >> 8));
+        if (flag) dc = __ldg(dc8(P.nm) + (w1 >> 8));
         if (dr != kDeltaEscR && dc != -128) return normal_f64_of(P, apply_delta(r_unit(w0, L), dr), apply_delta(c, dc));
       } else {
         const int dc = __ldg(P.nm.dc + (w1 >> 8));
@@ -759,16 +765,17 @@ __device__ __forceinline__ void normal_chunk_f64(const DistP& P, const NormalLut
   const uint64_t pol = delta_policy();
   double r[NE], c[NE];
   bool esc = false;
-  if (P.nm.cmode == 1) {
+  const bool cr = P.nm.cdd != nullptr;
+  if (cr) {
     // the cosine from c_cr: only its flagged elements (a few percent) read a correction
 #pragma unroll
     for (int e = 0; e < NE; ++e) dr[e] = ld_delta(P.nm.dr + (w0[e] >> 8), pol);
     bool flag[NE];
     const CosDD* T = P.nm.cdd;  // 64 KiB, through L1 (prefer_l1)
 #pragma unroll
-    for (int e = 0; e < NE; ++e) c[e] = c_cr(w1[e], T, P.nm, flag[e]);
+    for (int e = 0; e < NE; ++e) c[e] = c_cr(w1[e], T, flag[e]);
 #pragma unroll
-    for (int e = 0; e < NE; ++e) dc[e] = flag[e] ? ld_delta(P.nm.dc8 + (w1[e] >> 8), pol) : 0;
+    for (int e = 0; e < NE; ++e) dc[e] = flag[e] ? ld_delta(dc8(P.nm) + (w1[e] >> 8), pol) : 0;
 #pragma unroll
     for (int e = 0; e < NE; ++e) r[e] = r_unit(w0[e], L);
 #pragma unroll
@@ -791,7 +798,7 @@ __device__ __forceinline__ void normal_chunk_f64(const DistP& P, const NormalLut
   if (__builtin_expect(esc, 0)) {
 #pragma unroll
     for (int e = 0; e < NE; ++e)
-      if (dr[e] == kDeltaEscR || dc[e] == (P.nm.cmode == 1 ? -128 : kDeltaEsc))
+      if (dr[e] == kDeltaEscR || dc[e] == (cr ? -128 : kDeltaEsc))
         out[e] = normal_exact<SDR_F64>(P, w0[e], w1[e]);
   }
 }

@@ -696,7 +696,7 @@ __global__ void k_normal_cos_cr(const ExactMirror M, const double* __restrict__ 
   if (k >= (1u << 24)) return;
   const double cn = ctab != nullptr ? ctab[k] : mirror_c(M, k);
   bool flag;
-  const double c = c_cr(k << 8, NM.cdd, NM, flag);
+  const double c = c_cr(k << 8, NM.cdd, flag);
   const long long d = __double_as_longlong(cn) - __double_as_longlong(c);
   const bool fits = d > -128 && d < 128;
   dc8[k] = static_cast<int8_t>(flag ? (fits ? d : -128) : 0);
@@ -834,8 +834,6 @@ struct NormalState {
   unsigned long long delta_stats[4] = {0, 0, 0, 0};  // escapes r / c, max |difference| r / c
   unsigned long long cr_stats[4] = {0, 0, 0, 0};     // c_cr: flagged, escapes, unflagged mismatches, max |d|
   CosDD* cdd = nullptr;                // c_cr's table (cmode 1)
-  double q[3] = {0, 0, 0};
-  double ctau = 0.03;
   int cmode = 0;
   bool loaded = false;
 };
@@ -849,15 +847,8 @@ static double round_sig(long double x, int bits) {
 
 // Host construction of the fast-path tables (long double arithmetic).
 // c_cr's table: (cos, sin)(i pi/1024) for i in [0, 2048] as double-doubles
-// from quad precision, and pi/1024 split as 40 + 40 + 53 bits.
-static double trunc_bits(double x, int keep) {
-  uint64_t b;
-  memcpy(&b, &x, 8);
-  b &= ~((uint64_t{1} << (53 - keep)) - 1);
-  memcpy(&x, &b, 8);
-  return x;
-}
-static void build_cos_dd(CosDD* T, double* q) {
+// from quad precision.
+static void build_cos_dd(CosDD* T) {
   const __float128 Q = strtoflt128("3.14159265358979323846264338327950288419716939937510", nullptr) / 1024;
   for (int i = 0; i < kCosDD; ++i) {
     const __float128 c = cosq(Q * i), s = sinq(Q * i);
@@ -866,9 +857,9 @@ static void build_cos_dd(CosDD* T, double* q) {
     T[i].sh = static_cast<double>(s);
     T[i].sl = static_cast<double>(s - static_cast<__float128>(T[i].sh));
   }
-  q[0] = trunc_bits(static_cast<double>(Q), 40);
-  q[1] = trunc_bits(static_cast<double>(Q - q[0]), 40);
-  q[2] = static_cast<double>(Q - q[0] - q[1]);
+  // c_cr's constant split of pi/1024 (kQ1 + kQ2 + kQ3) must match the quad value
+  const __float128 r = Q - kQ1 - kQ2 - kQ3;
+  if (fabsq(r) > Q * static_cast<__float128>(1e-32)) fprintf(stderr, "sdr: pi/1024 split is off by %g\n", static_cast<double>(r));
 }
 
 static void build_normal_lut(NormalLut& L) {
@@ -996,22 +987,16 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
       P.nm.lut2 = g_nm[device].lut2;
       {
         const NormalState& S = g_nm[device];
-        P.nm.cmode = S.delta != nullptr ? S.cmode : 0;
         P.nm.dr = nullptr;
         P.nm.dc = nullptr;
-        P.nm.dc8 = nullptr;
-        if (S.delta != nullptr && S.cmode == 1) {  // dr[2^24], then dc8[2^24]
+        P.nm.cdd = nullptr;
+        if (S.delta != nullptr && S.cmode == 1) {  // dr[2^24], then the 8-bit c_cr corrections (dc8)
           P.nm.dr = reinterpret_cast<const DeltaR*>(S.delta);
-          P.nm.dc8 = reinterpret_cast<const int8_t*>(S.delta + (sizeof(DeltaR) << 24));
+          P.nm.cdd = S.cdd;
         } else if (S.delta != nullptr) {           // dc[2^24] (int16), then dr[2^24]
           P.nm.dc = reinterpret_cast<const int16_t*>(S.delta);
           P.nm.dr = reinterpret_cast<const DeltaR*>(S.delta + (sizeof(int16_t) << 24));
         }
-        P.nm.cdd = S.cdd;
-        P.nm.q1 = S.q[0];
-        P.nm.q2 = S.q[1];
-        P.nm.q3 = S.q[2];
-        P.nm.ctau = S.ctau;
       }
       {
         // float64 fast path (see normal_certified): with Er, Ec the calibrated
@@ -1432,11 +1417,10 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
     if (e == cudaSuccess) e = cudaMemset(st, 0, 8 * sizeof(unsigned long long));
     // cosine: c_cr where it verifies on every point (cmode 1), else 16-bit corrections of c_fast
     const char* cflag = getenv("SDR_NORMAL_COS_CR");
-    if (const char* tau = getenv("SDR_NORMAL_COS_TAU")) S.ctau = atof(tau);
     bool cr = e == cudaSuccess && !(cflag != nullptr && strcmp(cflag, "0") == 0);
     if (cr) {
       std::vector<CosDD> h(kCosDD);
-      build_cos_dd(h.data(), S.q);
+      build_cos_dd(h.data());
       e = cudaMalloc(&S.delta, kDeltaBytesCr);
       if (e == cudaSuccess) e = cudaMalloc(&S.cdd, kCosDD * sizeof(CosDD));
       if (e == cudaSuccess) e = cudaMemcpy(S.cdd, h.data(), kCosDD * sizeof(CosDD), cudaMemcpyHostToDevice);
@@ -1444,10 +1428,6 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
         NormalMirror NM;
         memset(static_cast<void*>(&NM), 0, sizeof(NM));
         NM.cdd = S.cdd;
-        NM.q1 = S.q[0];
-        NM.q2 = S.q[1];
-        NM.q3 = S.q[2];
-        NM.ctau = S.ctau;
         k_normal_cos_cr<<<(1u << 24) / 256, 256>>>(M, S.ctab, NM, reinterpret_cast<int8_t*>(S.delta + (sizeof(DeltaR) << 24)),
                                                     st + 4);
         k_normal_deltas<<<(1u << 24) / 256, 256>>>(M, S.rtab, S.ctab, S.lut, reinterpret_cast<DeltaR*>(S.delta),
@@ -1529,7 +1509,7 @@ int normal_tables_load(int device, const double* l_host, const double* c_host, d
     fprintf(stderr,
             "sdr normal float64 corrections: %s, cosine %s (tau %.3f: flagged %llu, escapes %llu, unflagged"
             " mismatches %llu, max |d| %llu), escapes r %llu c %llu, max |d| r %llu c %llu\n",
-            S.delta ? "built" : "off", S.cmode == 1 ? "c_cr" : "c_fast + 16-bit", S.ctau, S.cr_stats[0],
+            S.delta ? "built" : "off", S.cmode == 1 ? "c_cr" : "c_fast + 16-bit", SDR_COS_TAU, S.cr_stats[0],
             S.cr_stats[1], S.cr_stats[2], S.cr_stats[3], S.delta_stats[0], S.delta_stats[1], S.delta_stats[2],
             S.delta_stats[3]);
   S.loaded = true;
