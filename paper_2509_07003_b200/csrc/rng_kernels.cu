@@ -845,7 +845,6 @@ static double round_sig(long double x, int bits) {
   return static_cast<double>(ldexpl(nearbyintl(ldexpl(m, bits)), e - bits));
 }
 
-// Host construction of the fast-path tables (long double arithmetic).
 // c_cr's table: (cos, sin)(i pi/1024) for i in [0, 2048] as double-doubles
 // from quad precision.
 static void build_cos_dd(CosDD* T) {
@@ -862,6 +861,7 @@ static void build_cos_dd(CosDD* T) {
   if (fabsq(r) > Q * static_cast<__float128>(1e-32)) fprintf(stderr, "sdr: pi/1024 split is off by %g\n", static_cast<double>(r));
 }
 
+// Host construction of the fast-path tables (long double arithmetic).
 static void build_normal_lut(NormalLut& L) {
   for (int j = 0; j < 512; ++j) {
     long double inv, mult;
