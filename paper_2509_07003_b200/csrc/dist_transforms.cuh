@@ -222,15 +222,24 @@ __constant__ double c_npoly[9] = {
 // Kernels drawing float32 / float16 normals stage NormalLut2 (64 KiB; 160 KiB
 // with SDR_N2_COS2, then one 512-thread CTA per SM).  Everything else:
 // 256-thread CTAs, SDR_FILL_MINB per SM.
+// 16-bit outputs whose Normal fast path runs in float32 (the bfloat16 path;
+// float16 too with SDR_NORMAL_F16_F32)
+#ifndef SDR_NORMAL_F16_F32
+#define SDR_NORMAL_F16_F32 1
+#endif
+template <int DT>
+constexpr bool half_dt() {
+  return DT == SDR_BF16 || (SDR_NORMAL_F16_F32 && DT == SDR_F16);
+}
 template <int DIST, int DT>
 constexpr bool uses_lut2() {
-  return SDR_NORMAL_N2 && DIST == SDR_NORMAL && (DT == SDR_F32 || DT == SDR_F16);
+  return SDR_NORMAL_N2 && DIST == SDR_NORMAL && (DT == SDR_F32 || (DT == SDR_F16 && !half_dt<DT>()));
 }
 // bfloat16 normals with both functions from MUFU need no tables in shared
 // memory (the rare float64 fallbacks read theirs through L1).
 template <int DIST, int DT>
 constexpr bool tablefree() {
-  return SDR_NORMAL_BF16_MUFU && SDR_BF16_COS_MUFU && SDR_NORMAL_BF16_F32 && DIST == SDR_NORMAL && DT == SDR_BF16;
+  return SDR_NORMAL_BF16_MUFU && SDR_BF16_COS_MUFU && SDR_NORMAL_BF16_F32 && DIST == SDR_NORMAL && half_dt<DT>();
 }
 template <int DIST, int DT>
 constexpr bool stages_lut() { return DIST == SDR_NORMAL && !tablefree<DIST, DT>(); }
@@ -239,7 +248,7 @@ constexpr int fill_threads() { return uses_lut2<DIST, DT>() ? SDR_N2_THREADS : 2
 template <int DIST, int DT>
 constexpr int fill_minb() {
   return uses_lut2<DIST, DT>() ? SDR_N2_MINB * 256 / SDR_N2_THREADS
-         : (DIST == SDR_NORMAL && DT == SDR_BF16) ? SDR_BF16_MINB
+         : (DIST == SDR_NORMAL && half_dt<DT>() && SDR_NORMAL_BF16_F32) ? SDR_BF16_MINB
          : (DIST == SDR_NORMAL && DT == SDR_F64) ? SDR_F64N_MINB : SDR_FILL_MINB;
 }
 
@@ -485,7 +494,7 @@ __device__ __forceinline__ void missq_init() {
 // to the same bfloat16); the lower pack is the output word, and the XOR of the
 // two packs is OR-accumulated (one LOP3 per pair).  Only the rare branch looks
 // at which element differs; those take the float64 path, then the exact one.
-template <int NE>
+template <int DT, int NE>
 __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLut32* L32,
                                                   const uint32_t* w0, const uint32_t* w1, uint16_t* out,
                                                   uint16_t* qdst = nullptr, int nvalid = NE) {
@@ -517,10 +526,16 @@ __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLu
       lo[i] = __fsub_rd(v, B);
       hi[i] = __fadd_ru(v, B);
     }
-    const __nv_bfloat162 pl = __floats2bfloat162_rn(lo[0], lo[1]), ph = __floats2bfloat162_rn(hi[0], hi[1]);
     uint32_t l32, h32;
-    memcpy(&l32, &pl, 4);
-    memcpy(&h32, &ph, 4);
+    if constexpr (DT == SDR_BF16) {
+      const __nv_bfloat162 pl = __floats2bfloat162_rn(lo[0], lo[1]), ph = __floats2bfloat162_rn(hi[0], hi[1]);
+      memcpy(&l32, &pl, 4);
+      memcpy(&h32, &ph, 4);
+    } else {  // float16: the same monotone-rounding argument with its packed conversion
+      const __half2 pl = __floats2half2_rn(lo[0], lo[1]), ph = __floats2half2_rn(hi[0], hi[1]);
+      memcpy(&l32, &pl, 4);
+      memcpy(&h32, &ph, 4);
+    }
     out[e] = static_cast<uint16_t>(l32);  // (copying the packed word whole measured 3% slower)
     out[e + 1] = static_cast<uint16_t>(l32 >> 16);
     diff |= l32 ^ h32;
@@ -545,7 +560,7 @@ __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLu
         }
 #endif
         // float64 certified path (tables read through L1/L2), then the exact mirror
-        out[e] = normal_value<SDR_BF16>(P, P.nm.lut, w0[e], w1[e]);
+        out[e] = normal_value<DT>(P, P.nm.lut, w0[e], w1[e]);
       }
     }
   }
@@ -554,13 +569,14 @@ __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLu
 // Resolve the warp's queued elements: the float64 certified path (tables
 // through L1), then the exact mirror, one element per lane.  The whole warp
 // must be converged here.
+template <int DT>
 __device__ __noinline__ void missq_flush(const DistP& P) {
   MissQ* q = missq();
   __syncwarp();
   const uint32_t n = min(q->n, static_cast<uint32_t>(kMissQ));
   for (uint32_t k = threadIdx.x & 31; k < n; k += 32) {
     const uint4 t = q->e[k];
-    const uint16_t v = normal_value<SDR_BF16>(P, P.nm.lut, t.z, t.w);
+    const uint16_t v = normal_value<DT>(P, P.nm.lut, t.z, t.w);
     *reinterpret_cast<uint16_t*>((static_cast<uint64_t>(t.y) << 32) | t.x) = v;
   }
   __syncwarp();

@@ -105,7 +105,7 @@ __device__ __forceinline__ void fill_chunk_at(const FillArgs& A, const NormalLut
 // queue (dist_transforms.cuh, MissQ); the kernels init it and flush it.
 template <int DIST, int DT>
 constexpr bool uses_missq() {
-  return SDR_MISSQ && DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32 && SDR_NSPLIT == 1;
+  return SDR_MISSQ && DIST == SDR_NORMAL && half_dt<DT>() && SDR_NORMAL_BF16_F32 && SDR_NSPLIT == 1;
 }
 static_assert(fill_threads<SDR_NORMAL, SDR_BF16>() <= 256, "MissQ (dist_transforms.cuh) holds 8 warps' queues");
 
@@ -135,7 +135,7 @@ __device__ __forceinline__ void normal_half(const FillArgs& A, const NormalLut* 
   if constexpr (uses_lut2<SDR_NORMAL, DT>())
     normal_chunk2<DT, 4>(A.d, reinterpret_cast<const NormalLut2*>(L), w0, w1, v + E0);
   else
-    normal_chunk_bf16<4>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v + E0);
+    normal_chunk_bf16<DT, 4>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v + E0);
 }
 
 // Normal values of a chunk in SDR_NSPLIT parts (Philox words of a part, then
@@ -148,7 +148,7 @@ __device__ __forceinline__ void normal_part(const FillArgs& A, const NormalLut* 
   if constexpr (uses_lut2<SDR_NORMAL, DT>())
     normal_chunk2<DT, NE>(A.d, reinterpret_cast<const NormalLut2*>(L), w0, w1, v + E0);
   else
-    normal_chunk_bf16<NE>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v + E0);
+    normal_chunk_bf16<DT, NE>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v + E0);
   if constexpr (E0 + NE < kV) normal_part<DT, NE, E0 + NE>(A, L, H, v);
 }
 
@@ -156,7 +156,7 @@ template <int DIST, int DT, bool ALIGNED>
 __device__ __forceinline__ void chunk_values(const FillArgs& A, const NormalLut* L, uint64_t j0,
                                              typename St<DT>::T (&v)[kV]) {
   if constexpr (ALIGNED && SDR_NSPLIT > 1 && DIST == SDR_NORMAL &&
-                (uses_lut2<DIST, DT>() || (DT == SDR_BF16 && SDR_NORMAL_BF16_F32))) {
+                (uses_lut2<DIST, DT>() || (half_dt<DT>() && SDR_NORMAL_BF16_F32))) {
     const ChunkHoist H = hoist_chunk(A.g, j0);
     normal_part<DT, kV / SDR_NSPLIT, 0>(A, L, H, v);
   } else {
@@ -170,8 +170,8 @@ template <int DIST, int DT>
 __device__ __forceinline__ void values_from_words(const FillArgs& A, const NormalLut* L,
                                                   const uint32_t (&w0)[kV], const uint32_t (&w1)[kV],
                                                   typename St<DT>::T (&v)[kV]) {
-  if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
-    normal_chunk_bf16<kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v);
+  if constexpr (DIST == SDR_NORMAL && half_dt<DT>() && SDR_NORMAL_BF16_F32) {
+    normal_chunk_bf16<DT, kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v);
   } else if constexpr (uses_lut2<DIST, DT>()) {
     normal_chunk2<DT, kV>(A.d, reinterpret_cast<const NormalLut2*>(L), w0, w1, v);
   } else if constexpr (DIST == SDR_NORMAL && DT == SDR_F64) {
@@ -198,7 +198,7 @@ __device__ __forceinline__ void fill_chunk_at(const FillArgs& A, const NormalLut
   if constexpr (uses_missq<DIST, DT>()) {
     uint32_t w0[kV], w1[kV];
     fill_words<ALIGNED>(A, j0, w0, w1);
-    normal_chunk_bf16<kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v, dst);
+    normal_chunk_bf16<DT, kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v, dst);
   } else {
     chunk_values<DIST, DT, ALIGNED>(A, L, j0, v);
   }
@@ -231,7 +231,7 @@ __device__ __forceinline__ void fill_chunk_ragged(const FillArgs& A, const Norma
   if constexpr (uses_missq<DIST, DT>()) {  // queue only the elements this row owns
     uint32_t w0[kV], w1[kV];
     fill_words<ALIGNED>(A, j0, w0, w1);
-    normal_chunk_bf16<kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v, out, nvalid);
+    normal_chunk_bf16<DT, kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v, out, nvalid);
   } else {
     chunk_values<DIST, DT, ALIGNED>(A, L, j0, v);
   }
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
     NormalLut2* s_lut2 = reinterpret_cast<NormalLut2*>(s_dyn);
     bar = stage_lut_begin(s_lut2, A.d.nm.lut2);
     L = reinterpret_cast<const NormalLut*>(s_lut2);
-  } else if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
+  } else if constexpr (DIST == SDR_NORMAL && half_dt<DT>() && SDR_NORMAL_BF16_F32) {
     extern __shared__ __align__(16) unsigned char s_dyn[];  // sizeof(NormalLut32), set at launch
     NormalLut32* s_lut32 = reinterpret_cast<NormalLut32*>(s_dyn);
     bar = stage_lut_begin(s_lut32, A.d.nm.lut32);
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
     uint64_t cq;
     uint64_t j = walk_start(A.ix, A.div_cpr, q, kV, cq);
     if constexpr (DIST == SDR_NORMAL && SDR_FILL_PIPE == 2 && ALIGNED &&
-                  (uses_lut2<DIST, DT>() || (DT == SDR_BF16 && SDR_NORMAL_BF16_F32))) {
+                  (uses_lut2<DIST, DT>() || (half_dt<DT>() && SDR_NORMAL_BF16_F32))) {
       // Half-chunk software pipeline: every step computes the Philox words of
       // the NEXT half chunk (4 elements; pure arithmetic, computed past the end
       // too and discarded) in the same basic block as the transform of the
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
         T v[kV];
         T* dst = static_cast<T*>(A.out) + q * kV;
         if constexpr (uses_missq<DIST, DT>())
-          normal_chunk_bf16<kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v, dst);
+          normal_chunk_bf16<DT, kV>(A.d, reinterpret_cast<const NormalLut32*>(L), w0, w1, v, dst);
         else
           values_from_words<DIST, DT>(A, L, w0, w1, v);
         store_chunk(dst, v);
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
         q += stride;
         if ((it & 7u) == 7u) {
           __syncwarp();
-          if (missq()->n >= 64u) missq_flush(A.d);  // n is the warp's own: a uniform branch
+          if (missq()->n >= 64u) missq_flush<DT>(A.d);  // n is the warp's own: a uniform branch
         }
       }
     } else {
@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
     if constexpr (stages_lut<DIST, DT>()) stage_lut_wait(bar);
     for (; q < A.nchunks; q += stride) fill_chunk<DIST, DT, ALIGNED>(A, L, q);
   }
-  if constexpr (uses_missq<DIST, DT>()) missq_flush(A.d);  // every thread gets here: the warp is converged
+  if constexpr (uses_missq<DIST, DT>()) missq_flush<DT>(A.d);  // every thread gets here: the warp is converged
 }
 
 template <int DIST, int DT>
@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
     NormalLut2* s_lut2 = reinterpret_cast<NormalLut2*>(s_dyn);
     stage_lut(s_lut2, descs[0].d.nm.lut2);
     L = reinterpret_cast<const NormalLut*>(s_lut2);
-  } else if constexpr (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32) {
+  } else if constexpr (DIST == SDR_NORMAL && half_dt<DT>() && SDR_NORMAL_BF16_F32) {
     extern __shared__ __align__(16) unsigned char s_dyn[];  // sizeof(NormalLut32), set at launch
     NormalLut32* s_lut32 = reinterpret_cast<NormalLut32*>(s_dyn);
     stage_lut(s_lut32, descs[0].d.nm.lut32);
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(fill_threads<DIST, DT>(), fill_minb<DIST, DT>(
     }
     // this tile's queued elements, with this member's parameters (converged:
     // the tile loops are done; A is replaced only after the next barrier)
-    if constexpr (uses_missq<DIST, DT>()) missq_flush(A.d);
+    if constexpr (uses_missq<DIST, DT>()) missq_flush<DT>(A.d);
   }
 }
 
@@ -1095,7 +1095,7 @@ static int fill_dist_params(const sdr_dist& dist, int dt, DistP& P, int device) 
 template <int DIST, int DT>
 static constexpr size_t fill_dyn_smem() {
   return uses_lut2<DIST, DT>() ? sizeof(NormalLut2)
-         : (DIST == SDR_NORMAL && DT == SDR_BF16 && SDR_NORMAL_BF16_F32 && !tablefree<DIST, DT>())
+         : (DIST == SDR_NORMAL && half_dt<DT>() && SDR_NORMAL_BF16_F32 && !tablefree<DIST, DT>())
                ? sizeof(NormalLut32) : 0;
 }
 template <typename K>
