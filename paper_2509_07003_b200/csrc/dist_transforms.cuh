@@ -231,6 +231,15 @@ template <int DT>
 constexpr bool half_dt() {
   return DT == SDR_BF16 || (SDR_NORMAL_F16_F32 && DT == SDR_F16);
 }
+// MUFU cosine on the float32 path (float16 may use the table cosine: its
+// narrower misses band, SDR_F16_COS_MUFU=0)
+#ifndef SDR_F16_COS_MUFU
+#define SDR_F16_COS_MUFU 1
+#endif
+template <int DT>
+constexpr bool cos_mufu() {
+  return SDR_BF16_COS_MUFU && (DT == SDR_BF16 || SDR_F16_COS_MUFU);
+}
 template <int DIST, int DT>
 constexpr bool uses_lut2() {
   return SDR_NORMAL_N2 && DIST == SDR_NORMAL && (DT == SDR_F32 || (DT == SDR_F16 && !half_dt<DT>()));
@@ -239,7 +248,7 @@ constexpr bool uses_lut2() {
 // memory (the rare float64 fallbacks read theirs through L1).
 template <int DIST, int DT>
 constexpr bool tablefree() {
-  return SDR_NORMAL_BF16_MUFU && SDR_BF16_COS_MUFU && SDR_NORMAL_BF16_F32 && DIST == SDR_NORMAL && half_dt<DT>();
+  return SDR_NORMAL_BF16_MUFU && cos_mufu<DT>() && SDR_NORMAL_BF16_F32 && DIST == SDR_NORMAL && half_dt<DT>();
 }
 template <int DIST, int DT>
 constexpr bool stages_lut() { return DIST == SDR_NORMAL && !tablefree<DIST, DT>(); }
@@ -507,16 +516,18 @@ __device__ __forceinline__ void normal_chunk_bf16(const DistP& P, const NormalLu
     for (int i = 0; i < 2; ++i) {
 #if SDR_NORMAL_BF16_MUFU
       float h;
-#if SDR_BF16_COS_MUFU
-      const float r = r32_mufu(w0[e + i], h), c = c32_mufu(w1[e + i]);
+      float r, c, B;
+      if constexpr (cos_mufu<DT>()) {
+        r = r32_mufu(w0[e + i], h);
+        c = c32_mufu(w1[e + i]);
+        B = fmaf(h, P.nm.bmc_i, fmaf(r, P.nm.bmc_r, P.nm.bm_c));
+      } else {
+        r = r32_mufu(w0[e + i], h);
+        c = c32_fast(w1[e + i], L32);
+        // |v - v_numpy| <= r*bm_r + h*bm_i + bm_c   (host: fill_dist_params)
+        B = fmaf(h, P.nm.bm_i, fmaf(r, P.nm.bm_r, P.nm.bm_c));
+      }
       const float v = fmaf(P.nm.std32, r * c, P.nm.mean32);
-      const float B = fmaf(h, P.nm.bmc_i, fmaf(r, P.nm.bmc_r, P.nm.bm_c));
-#else
-      const float r = r32_mufu(w0[e + i], h), c = c32_fast(w1[e + i], L32);
-      const float v = fmaf(P.nm.std32, r * c, P.nm.mean32);
-      // |v - v_numpy| <= r*bm_r + h*bm_i + bm_c   (host: fill_dist_params)
-      const float B = fmaf(h, P.nm.bm_i, fmaf(r, P.nm.bm_r, P.nm.bm_c));
-#endif
 #else
       const float r = r32_fast(w0[e + i], L32), c = c32_fast(w1[e + i], L32);
       const float v = fmaf(P.nm.std32, r * c, P.nm.mean32);
