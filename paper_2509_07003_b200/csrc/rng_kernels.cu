@@ -23,6 +23,7 @@
 // The SDR_* macros below are A/B knobs; their defaults are the measured best.
 #include <quadmath.h>
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1109,8 +1110,16 @@ static void allow_dyn_smem(K kernel, size_t bytes) {
 #endif
 template <int DIST, int DT, typename K>
 static void prefer_l1(K kernel) {
-  if constexpr (DIST == SDR_NORMAL && DT == SDR_F64 && SDR_F64_CARVEOUT > 0)
-    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, SDR_F64_CARVEOUT);
+  if constexpr (DIST == SDR_NORMAL && DT == SDR_F64 && SDR_F64_CARVEOUT > 0) {
+    static std::atomic<uint64_t> done{0};  // once per (kernel, device)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = uint64_t{1} << (dev & 63);
+    if ((done.load(std::memory_order_relaxed) & bit) == 0) {
+      cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, SDR_F64_CARVEOUT);
+      done.fetch_or(bit, std::memory_order_relaxed);
+    }
+  }
 }
 
 template <int DIST, int DT>
