@@ -370,3 +370,25 @@ def test_redistribute_rejects_double_sharding_path_like_reference():
         x = from_local(torch.zeros(v.local_shape), src, (6, 8), (0, 0))
         with pytest.raises(PlacementError):
             redistribute_many([x], [ShardSpec(mesh, parse_placements(d))])
+
+
+def test_cos_cr_constants_split_pi_over_1024():
+    """c_cr's argument reduction (dist_transforms.cuh): pi/1024 = kQ1 + kQ2 +
+    kQ3 to about 2^-110, with kQ1 and kQ2 of at most 40 significant bits so
+    that i*kQ1 and i*kQ2 are exact for every table index i <= 2048."""
+    import re
+    from decimal import Decimal, getcontext
+    from fractions import Fraction
+    src = open(os.path.join(ROOT, "paper_2509_07003_b200", "csrc", "dist_transforms.cuh")).read()
+    m = re.search(r"kQ1 = (\S+), kQ2 = (\S+), kQ3 = (\S+);", src)
+    assert m, "constants not found"
+    q = [float.fromhex(x) for x in m.groups()]
+    getcontext().prec = 60
+    pi = Fraction(Decimal("3.14159265358979323846264338327950288419716939937510582097494459"))
+    err = abs(sum(Fraction(x) for x in q) - pi / 1024)
+    assert err < Fraction(1, 2 ** 110), float(err)
+    import math
+    for x in q[:2]:
+        m53 = int(math.frexp(x)[0] * 2 ** 53)  # the 53-bit significand as an integer
+        assert m53 % 2 ** 13 == 0, x           # at most 40 significant bits
+        assert 2048 * (m53 >> 13) < 2 ** 53     # i * q exact for i <= 2048
